@@ -1,0 +1,136 @@
+/*
+ * gs_b200.h -- C-ABI of the B200-native generalized-sampling hot path:
+ * the change-of-basis operator T (Fourier samples <- boundary-corrected
+ * Daubechies / Haar scaling coefficients), its adjoint T*, and the CGLS
+ * least-squares loop that applies them, all resident on one sm_100a GPU.
+ *
+ * This is the drop-in boundary for the reference C++ API (namespace gs,
+ * /root/reference/proj).  Every entry point names the reference interface it
+ * replaces.  Plain pointers and sizes only; complex vectors are interleaved
+ * (re, im) float64, layout-identical to std::complex<double> / double2.
+ * Vector arguments may be host or device pointers (cudaPointerGetAttributes
+ * decides); host buffers are staged through pinned memory inside the call.
+ *
+ * Return codes mirror gs::ErrorClass (include/gs/error.hpp:9-15):
+ *   0 ok, 2 usage (null handle / bad argument), 4 shape, 5 domain,
+ *   6 numerical, 7 CUDA runtime failure (no GPU, launch error, OOM).
+ * The message of the last failure on the calling thread is gs_last_error().
+ * A C++ wrapper rethrows the matching gs::Error subclass.
+ */
+#ifndef GS_B200_H
+#define GS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GS_OK 0
+#define GS_ERR_USAGE 2
+#define GS_ERR_SHAPE 4
+#define GS_ERR_DOMAIN 5
+#define GS_ERR_NUMERICAL 6
+#define GS_ERR_CUDA 7
+
+/* Route the operator took (freq2wave.cpp:170-191 plus the new exact tensor route). */
+#define GS_ROUTE_UNIFORM_1D 1  /* exact zero-embedded DFT (uniform_ndft_fft)       */
+#define GS_ROUTE_NFFT_1D 2     /* Kaiser-Bessel gridding NFFT, 1D                   */
+#define GS_ROUTE_NFFT_2D 3     /* 2D KB-NFFT + 4p side NFFTs + corners (9 blocks)   */
+#define GS_ROUTE_TENSOR_2D 4   /* exact: T = T_x (x) T_y on a uniform tensor grid   */
+
+typedef struct gs_op gs_op; /* opaque; replaces gs::Freq2WaveOp (freq2wave.hpp:32-55) */
+
+/* Construction description: gs::freq2wave(SamplingSet, Family, J, Freq2WaveOptions)
+ * (freq2wave.hpp:12-24, 57-58).  `batch` >= 1 independent problems of equal
+ * shape (dim, family, J, M) share one handle; their coords / weights arrays
+ * are concatenated problem-major. */
+typedef struct {
+  int dim;                 /* 1 or 2 (SamplingSet::dim)                           */
+  int family_p;            /* 1 = haar, 2..8 = db2..db8 (Family; p vanishing mom.) */
+  int J;                   /* scale, n = 2^J coefficients per axis                 */
+  int64_t M;               /* samples per problem                                  */
+  int batch;               /* number of independent problems (>= 1)                */
+  const double* coords;    /* [batch][M][dim] point-major (x, y) host pointer      */
+  const double* weights;   /* [batch][M] Voronoi mu (NOT sqrt), or NULL            */
+  double bandwidth;        /* |xi| <= bandwidth accepted; NaN = none               */
+  double sigma;            /* NFFT oversampling (default 2)                        */
+  int w;                   /* KB half-width (default 6)                            */
+  int boundary_depth;      /* default 30                                           */
+  int product_terms;       /* default 48                                           */
+  int allow_uniform_fast_path; /* default 1                                        */
+  int allow_tensor_route;  /* default 1: exact tensor route for uniform 2D grids  */
+  int device;              /* CUDA ordinal                                         */
+} gs_op_desc;
+
+typedef struct {
+  int dim, family_p, J, batch, route;
+  int64_t rows;            /* M  (Freq2WaveOp::rows)                               */
+  int64_t cols;            /* N_c = n or n^2 (Freq2WaveOp::cols)                   */
+  int uniform_fast;        /* Freq2WaveOp::uniform_fast (1D)                        */
+  double uniform_epsilon;  /* Freq2WaveOp::uniform_epsilon                         */
+  int weighted;            /* Freq2WaveOp::weighted()                              */
+  int n_over;              /* NFFT oversampled length per axis (0 on exact routes) */
+  int64_t device_bytes;    /* HBM held by the handle                               */
+} gs_op_info_t;
+
+typedef struct {
+  int iterations;          /* SolveStats::iterations (solver.hpp:16-22)            */
+  double residual;         /* SolveStats::residual                                 */
+  int converged;           /* SolveStats::converged                                */
+} gs_solve_stats;
+
+/* gs::freq2wave (freq2wave.cpp:86-193): validates, builds the factors
+ * D, L, R, the KB tables and the sorted sample bins ON THE DEVICE. */
+int gs_op_create(const gs_op_desc* desc, gs_op** out);
+int gs_op_destroy(gs_op* op);
+int gs_op_info(const gs_op* op, gs_op_info_t* info);
+
+/* gs::apply_forward (freq2wave.cpp:215-303): samples[b] = T_b coeffs[b].
+ * coeffs [batch][cols], samples [batch][rows]. `stream` is a cudaStream_t or NULL. */
+int gs_apply_forward(gs_op* op, const double* coeffs, int64_t coeffs_len,
+                     double* samples, void* stream);
+
+/* gs::apply_adjoint (freq2wave.cpp:305-387): coeffs[b] = T_b^* samples[b]. */
+int gs_apply_adjoint(gs_op* op, const double* samples, int64_t samples_len,
+                     double* coeffs, void* stream);
+
+/* gs::solve_least_squares (solver.cpp:19-91), CGNR resident on the GPU.
+ * raw_samples [batch][rows] (weighted ops take RAW data; sqrt(mu) applied here),
+ * x0 [batch][cols] or NULL, max_iterations <= 0 -> 2*cols, tolerance > 0.
+ * x_out [batch][cols]; stats [batch]; history [batch][max_iter+1] or NULL
+ * (entries past stats.iterations are undefined). */
+int gs_solve_least_squares(gs_op* op, const double* raw_samples, int64_t samples_len,
+                           const double* x0, int max_iterations, double tolerance,
+                           double* x_out, gs_solve_stats* stats, double* history,
+                           void* stream);
+
+/* Split CGLS for warm restarts and benchmarking (same algorithm as
+ * gs_solve_least_squares): begin = preamble (solver.cpp:28-68, 2 adjoints +
+ * 1 forward), step = `iterations` loop bodies (solver.cpp:70-88) enqueued on
+ * `stream` with no host synchronisation (converged problems freeze on the
+ * device), active = host poll of the device flags, finish = x / stats / history. */
+typedef struct gs_cgls_session gs_cgls_session;
+int gs_cgls_begin(gs_op* op, const double* raw_samples, int64_t samples_len, const double* x0,
+                  double tolerance, int history_capacity, void* stream, gs_cgls_session** out);
+int gs_cgls_step(gs_cgls_session* s, int iterations, void* stream);
+int gs_cgls_active(gs_cgls_session* s, void* stream, int* any_active);
+int gs_cgls_finish(gs_cgls_session* s, double* x_out, gs_solve_stats* stats, double* history,
+                   void* stream);
+int gs_cgls_destroy(gs_cgls_session* s);
+
+/* Host copies of the per-axis factors of problem `b` in the reference layout
+ * (Freq2WaveOp::Dx/Dy, Lx/Rx/Ly/Ry col-major M x p, freq2wave.hpp:42-43);
+ * axis 0 = x, 1 = y.  L, R may be NULL (haar). */
+int gs_op_export_factors(gs_op* op, int b, int axis, double* D, double* L, double* R);
+
+const char* gs_last_error(void);
+
+/* Build / capability probe: returns the sm version the library was compiled
+ * for (100 for sm_100a) -- loadable without a GPU. */
+int gs_build_arch(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GS_B200_H */

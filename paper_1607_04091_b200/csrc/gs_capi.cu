@@ -1,0 +1,1055 @@
+// gs_capi.cu -- host side of the B200 operator: validation (mirrors
+// freq2wave.cpp:86-193), device-side construction, route dispatch for
+// apply_forward / apply_adjoint, the device-resident CGLS loop and the C-ABI
+// declared in include/gs_b200.h.  No torch types anywhere: plain CUDA runtime.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/gs_b200.h"
+#include "factors.cuh"
+#include "family_data.h"
+#include "gs_common.cuh"
+#include "kernels_nfft.cuh"
+#include "kernels_uniform.cuh"
+#include "kernels_vec.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct GsError {
+  int code;
+  std::string msg;
+};
+[[noreturn]] void fail(int code, const std::string& m) { throw GsError{code, m}; }
+
+#define CK(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess) fail(GS_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+#define CKL()                                                                                 \
+  do {                                                                                        \
+    cudaError_t e_ = cudaGetLastError();                                                      \
+    if (e_ != cudaSuccess) fail(GS_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() {
+    if (p) cudaFree(p);
+  }
+  void alloc(size_t count) {
+    if (count <= n && p) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    if (count == 0) return;
+    CK(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void upload(const T* h, size_t count, cudaStream_t st) {
+    alloc(count);
+    if (count) CK(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, st));
+  }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+inline int ilog2(long long v) {
+  int l = 0;
+  while ((1LL << l) < v) ++l;
+  return l;
+}
+inline bool is_pow2(long long v) { return v > 0 && (v & (v - 1)) == 0; }
+inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
+
+// ------------------------------------------------------------------ host math
+double wrap_half_open(double z) {  // freq2wave.cpp:15-19
+  double w = z - std::floor(z + 0.5);
+  if (w >= 0.5) w -= 1.0;
+  return w;
+}
+
+bool detect_uniform(const double* zeta, size_t M, long long n, double* eps_out) {  // freq2wave.cpp:22-37
+  if (M < 2 || (long long)M < n) return false;
+  double spacing = zeta[1] - zeta[0];
+  if (spacing <= 0.0) return false;
+  double eps = spacing * (double)n;
+  double inv = 1.0 / eps;
+  if (std::abs(inv - std::round(inv)) > 1e-9 || std::round(inv) < 1.0) return false;
+  double half_m = (double)M / 2.0;
+  for (size_t m = 0; m < M; ++m) {
+    double expect = eps / (double)n * ((double)m - half_m);
+    if (std::abs(zeta[m] - expect) > 1e-12) return false;
+  }
+  *eps_out = eps;
+  return true;
+}
+
+double kb_transform(double nu, int w, double beta) {  // nufft.cpp:163-171
+  double t = beta * beta - (GS_TWO_PI * w * nu) * (GS_TWO_PI * w * nu);
+  if (t > 0) {
+    double s = std::sqrt(t);
+    return 2.0 * w * std::sinh(s) / s;
+  }
+  double s = std::sqrt(-t);
+  return 2.0 * w * std::sin(s) / s;
+}
+
+// v_zero = (I - U)^{-1} V 1 by partial-pivot LU (fourier.cpp:60-72)
+bool fixed_point(const double* U, const double* V, int p, double* v) {
+  std::vector<double> A(p * p), b(p, 0.0);
+  for (int i = 0; i < p; ++i)
+    for (int j = 0; j < p; ++j) A[i * p + j] = (i == j ? 1.0 : 0.0) - U[i * p + j];
+  for (int i = 0; i < p; ++i)
+    for (int j = 0; j < 2 * p - 1; ++j) b[i] += V[i * (2 * p - 1) + j];
+  std::vector<double> A0 = A, b0 = b;
+  for (int k = 0; k < p; ++k) {
+    int best = k;
+    for (int i = k + 1; i < p; ++i)
+      if (std::abs(A[i * p + k]) > std::abs(A[best * p + k])) best = i;
+    if (best != k) {
+      for (int j = 0; j < p; ++j) std::swap(A[k * p + j], A[best * p + j]);
+      std::swap(b[k], b[best]);
+    }
+    double d = A[k * p + k];
+    if (d == 0.0) return false;
+    for (int i = k + 1; i < p; ++i) {
+      double f = A[i * p + k] / d;
+      for (int j = k + 1; j < p; ++j) A[i * p + j] -= f * A[k * p + j];
+      b[i] -= f * b[k];
+    }
+  }
+  for (int i = p - 1; i >= 0; --i) {
+    double s = b[i];
+    for (int j = i + 1; j < p; ++j) s -= A[i * p + j] * v[j];
+    v[i] = s / A[i * p + i];
+  }
+  double res = 0, rn = 0;
+  for (int i = 0; i < p; ++i) {
+    double s = -b0[i];
+    for (int j = 0; j < p; ++j) s += A0[i * p + j] * v[j];
+    res += s * s;
+    rn += b0[i] * b0[i];
+  }
+  return std::sqrt(res) <= 1e-10 * (1.0 + std::sqrt(rn));
+}
+
+FamDev make_family(int p) {
+  FamDev f;
+  std::memset(&f, 0, sizeof(f));
+  f.p = p;
+  f.has_edges = p >= 2;
+  const gsdata::FamilyData& src = gsdata::kFamilies[p - 1];
+  for (int i = 0; i < 2 * p; ++i) f.taps[i] = src.taps[i];
+  if (p >= 2) {
+    for (int side = 0; side < 2; ++side) {
+      const double* H = side == 0 ? src.left_H : src.right_H;
+      const double* h = side == 0 ? src.left_h : src.right_h;
+      for (int i = 0; i < p * p; ++i) f.U[side][i] = H[i] / std::sqrt(2.0);  // scaling.cpp:63-70
+      for (int i = 0; i < p * (2 * p - 1); ++i) f.V[side][i] = h[i] / std::sqrt(2.0);
+      if (!fixed_point(f.U[side], f.V[side], p, f.vz[side]))
+        fail(GS_ERR_NUMERICAL, "boundary_fourier_at_zero: singular fixed-point system");
+    }
+  }
+  return f;
+}
+
+struct UniSetup {
+  long long inv_eps, q, n2;
+};
+UniSetup uniform_setup(long long M, double eps, long long N) {  // nufft.cpp:389-400
+  if (eps <= 0.0) fail(GS_ERR_DOMAIN, "epsilon must be positive");
+  double inv = 1.0 / eps;
+  long long inv_eps = std::llround(inv);
+  if (inv_eps < 1 || std::abs(inv - (double)inv_eps) > 1e-9) fail(GS_ERR_DOMAIN, "1/epsilon must be a positive integer");
+  if (M < N) fail(GS_ERR_DOMAIN, "uniform reduction requires M >= N");
+  long long per = N * inv_eps;
+  long long q = (M + per - 1) / per;
+  return {inv_eps, q, q * per};
+}
+
+}  // namespace
+
+// ====================================================================== op
+struct gs_op {
+  gs_op_desc d{};
+  int dim = 1, p = 1, edges = 0, J = 0, B = 1, route = 0, device = 0;
+  long long n = 0;
+  int64_t M = 0, Nc = 0;
+  bool weighted = false;
+  int Rr = 1;  // record length 1 + 2p
+  int depth = 30, terms = 48;
+  FamDev fam;
+  double uniform_eps = 0.0;
+  // FFT twiddles
+  DBuf<cplx> tw;
+  int logLmax = 0;
+  // uniform / tensor
+  UniP up{}, upx{}, upy{};
+  int64_t Ma = 0, Mb = 0;
+  DBuf<cplx> rec_u, rec_ax, rec_ay;
+  // NFFT
+  NfP np{};
+  double beta = 0;
+  DBuf<double> deconv;
+  DBuf<int> perm, base_x, base_y, bins;
+  DBuf<double> wts_x, wts_y;
+  DBuf<cplx> rec_x, rec_y;
+  DBuf<double> sqrtw;  // internal order ([B][M]) or empty
+  // workspace
+  DBuf<cplx> G, lines, TB, TL, TC, W;
+  DBuf<cplx> stage_a, stage_b;
+  std::mutex mu;
+
+  size_t device_bytes() const {
+    return tw.bytes() + rec_u.bytes() + rec_ax.bytes() + rec_ay.bytes() + deconv.bytes() + perm.bytes() +
+           base_x.bytes() + base_y.bytes() + bins.bytes() + wts_x.bytes() + wts_y.bytes() + rec_x.bytes() +
+           rec_y.bytes() + sqrtw.bytes() + G.bytes() + lines.bytes() + TB.bytes() + TL.bytes() + TC.bytes() +
+           W.bytes() + stage_a.bytes() + stage_b.bytes();
+  }
+};
+
+namespace {
+
+const int kSmemMax = 227 * 1024;
+
+void set_smem_attrs() {
+  static bool done = false;
+  if (done) return;
+  CK(cudaFuncSetAttribute(k_uni_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
+  CK(cudaFuncSetAttribute(k_uni_adj, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
+  CK(cudaFuncSetAttribute(k_n1_embed_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
+  CK(cudaFuncSetAttribute(k_n1_ifft_crop, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
+  CK(cudaFuncSetAttribute(k2_rows_embed_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
+  CK(cudaFuncSetAttribute(k2_cols_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
+  CK(cudaFuncSetAttribute(k2_lines_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
+  CK(cudaFuncSetAttribute(k2_spread, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
+  CK(cudaFuncSetAttribute(k2_cols_ifft_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
+  CK(cudaFuncSetAttribute(k2_rows_ifft_crop, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
+  CK(cudaFuncSetAttribute(k2_edges, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
+  done = true;
+}
+
+void make_twiddles(gs_op* op, long long Lmax, cudaStream_t st) {
+  op->logLmax = ilog2(std::max<long long>(Lmax, 2));
+  long long L = 1LL << op->logLmax;
+  std::vector<cplx> h(L / 2);
+  for (long long k = 0; k < L / 2; ++k) {
+    double a = -GS_TWO_PI * (double)k / (double)L;
+    h[k] = mk(std::cos(a), std::sin(a));
+  }
+  op->tw.upload(h.data(), h.size(), st);
+}
+
+// __global__ helpers used only at construction
+__global__ void k_gather_d(const double* __restrict__ src, const int* __restrict__ perm, int64_t M, int64_t total,
+                           double* __restrict__ dst) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  dst[i] = src[(i / M) * M + perm[i]];
+}
+__global__ void k_keys(const int* __restrict__ by, const int* __restrict__ bx, int64_t M, int64_t total, int T, int nt,
+                       unsigned long long* __restrict__ keys, int* __restrict__ vals) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  unsigned long long prob = (unsigned long long)(i / M);
+  unsigned long long bin = by ? (unsigned long long)((by[i] / T) * nt + bx[i] / T) : (unsigned long long)bx[i];
+  keys[i] = (prob << 32) | bin;
+  vals[i] = (int)(i - (int64_t)prob * M);
+}
+__global__ void k_bin_starts(const unsigned long long* __restrict__ keys, int64_t total, int64_t M, int B, int nbins,
+                             int* __restrict__ starts) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t per = nbins + 1;
+  if (i >= (int64_t)B * per) return;
+  unsigned long long prob = (unsigned long long)(i / per), bin = (unsigned long long)(i % per);
+  unsigned long long key = (prob << 32) | bin;
+  int64_t lo = 0, hi = total;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) / 2;
+    if (keys[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  starts[i] = (int)(lo - (int64_t)prob * M);
+}
+
+// sort the samples of every problem by bin; perm[s] = original index
+void sort_bins(gs_op* op, const int* by, const int* bx, int nbins, int T, int nt, cudaStream_t st) {
+  const int64_t total = op->M * op->B;
+  DBuf<unsigned long long> k_in, k_out;
+  DBuf<int> v_in;
+  k_in.alloc(total);
+  k_out.alloc(total);
+  v_in.alloc(total);
+  op->perm.alloc(total);
+  k_keys<<<nblk(total, 256), 256, 0, st>>>(by, bx, op->M, total, T, nt, k_in.p, v_in.p);
+  CKL();
+  size_t tmp = 0;
+  int end_bit = 32 + std::max(1, ilog2(op->B + 1));
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, k_in.p, k_out.p, v_in.p, op->perm.p, (int)total, 0, end_bit, st));
+  DBuf<char> scratch;
+  scratch.alloc(tmp);
+  CK(cub::DeviceRadixSort::SortPairs(scratch.p, tmp, k_in.p, k_out.p, v_in.p, op->perm.p, (int)total, 0, end_bit, st));
+  op->bins.alloc((size_t)op->B * (nbins + 1));
+  k_bin_starts<<<nblk((int64_t)op->B * (nbins + 1), 256), 256, 0, st>>>(k_out.p, total, op->M, op->B, nbins,
+                                                                        op->bins.p);
+  CKL();
+  CK(cudaStreamSynchronize(st));
+}
+
+void build_factors(gs_op* op, const double* d_xi, const double* d_sw, int64_t count, cplx* rec, cudaStream_t st) {
+  k_build_factors<<<nblk(count, 128), 128, 0, st>>>(op->fam, d_xi, d_sw, count, op->J, op->depth, op->terms, rec);
+  CKL();
+}
+
+UniP make_uni(gs_op* op, int64_t M, double eps) {
+  UniSetup s = uniform_setup(M, eps, op->n);
+  if (s.n2 > 8192) fail(GS_ERR_DOMAIN, "uniform route: DFT length " + std::to_string(s.n2) + " exceeds 8192 on this build");
+  UniP P{};
+  P.n = (int)op->n;
+  P.M = (int)M;
+  P.q = (int)s.q;
+  P.N2 = (int)s.n2;
+  P.logN2 = is_pow2(s.n2) ? ilog2(s.n2) : -1;
+  if (P.logN2 < 0 && s.n2 > 4096) fail(GS_ERR_DOMAIN, "uniform route: non power-of-two DFT length > 4096");
+  P.p = op->p;
+  P.edges = op->edges;
+  P.eps = eps;
+  P.phase_step = GS_PI * eps * (double)M / (double)op->n;  // nufft.cpp:412
+  return P;
+}
+size_t uni_smem(const UniP& P) { return (size_t)P.N2 * sizeof(cplx) * (P.logN2 >= 0 ? 1 : 2); }
+
+// ------------------------------------------------------------------ construction
+gs_op* create(const gs_op_desc* dsc) {
+  if (!dsc) fail(GS_ERR_USAGE, "null descriptor");
+  std::unique_ptr<gs_op> op(new gs_op);
+  gs_op_desc d = *dsc;
+  op->d = d;
+  op->dim = d.dim;
+  op->J = d.J;
+  op->B = d.batch <= 0 ? 1 : d.batch;
+  op->M = d.M;
+  op->depth = d.boundary_depth > 0 ? d.boundary_depth : 30;
+  op->terms = d.product_terms > 0 ? d.product_terms : 48;
+  if (d.family_p < 1 || d.family_p > 8) fail(GS_ERR_DOMAIN, "unsupported family");
+  op->p = d.family_p;
+  op->edges = op->p >= 2;
+  op->Rr = 1 + (op->edges ? 2 * op->p : 0);
+  // freq2wave.cpp:93-102
+  if (d.dim != 1 && d.dim != 2) fail(GS_ERR_DOMAIN, "sampling set must be 1D or 2D");
+  if (d.M <= 0 || !d.coords) fail(GS_ERR_SHAPE, "empty sampling set");
+  if (d.J < 0 || d.J > 24) fail(GS_ERR_DOMAIN, "scale J out of range");
+  op->n = 1LL << d.J;
+  if (op->n < 2 * op->p) fail(GS_ERR_DOMAIN, "scale too small: 2^J must be >= 2p");
+  if (d.M > (int64_t)INT32_MAX / 2) fail(GS_ERR_DOMAIN, "too many samples per problem");
+  const int64_t M = d.M, B = op->B, total = M * B;
+  const double* coords = d.coords;
+  for (int64_t i = 0; i < total * d.dim; ++i)
+    if (!std::isfinite(coords[i])) fail(GS_ERR_DOMAIN, "non-finite frequency");
+  std::vector<double> sw;
+  if (d.weights) {  // freq2wave.cpp:105-114
+    op->weighted = true;
+    sw.resize(total);
+    for (int64_t i = 0; i < total; ++i) {
+      if (!(d.weights[i] > 0.0)) fail(GS_ERR_DOMAIN, "weights must be positive");
+      sw[i] = std::sqrt(d.weights[i]);
+    }
+  }
+  const bool has_bw = !std::isnan(d.bandwidth);
+  std::vector<double> xi_x(total), xi_y(d.dim == 2 ? total : 0);
+  for (int64_t i = 0; i < total; ++i) {
+    xi_x[i] = coords[i * d.dim];
+    if (d.dim == 2) xi_y[i] = coords[i * 2 + 1];
+  }
+  auto check_axis = [&](const std::vector<double>& xi) {  // freq2wave.cpp:123-140
+    for (double v : xi) {
+      if (has_bw) {
+        if (std::abs(v) > d.bandwidth) fail(GS_ERR_DOMAIN, "bandwidth exceeded: |xi| > bandwidth");
+      } else {
+        double z = std::ldexp(v, -d.J);
+        if (!(z >= -0.5 && z < 0.5))
+          fail(GS_ERR_DOMAIN,
+               "bandwidth exceeded: scaled point outside [-1/2, 1/2) (pass a bandwidth to allow periodized rows)");
+      }
+    }
+  };
+  check_axis(xi_x);
+  if (d.dim == 2) check_axis(xi_y);
+
+  op->device = d.device;
+  CK(cudaSetDevice(d.device));
+  set_smem_attrs();
+  op->fam = make_family(op->p);
+  op->Nc = d.dim == 1 ? op->n : op->n * op->n;
+  cudaStream_t st = 0;
+
+  // ---- route selection (freq2wave.cpp:170-191, plus the exact tensor route)
+  const bool allow_u = d.allow_uniform_fast_path != 0;
+  std::vector<double> zeta(M);
+  if (d.dim == 1) {
+    bool uni = allow_u;
+    double eps0 = 0;
+    for (int64_t b = 0; uni && b < B; ++b) {
+      for (int64_t m = 0; m < M; ++m) zeta[m] = std::ldexp(xi_x[b * M + m], -d.J);
+      double e = 0;
+      if (!detect_uniform(zeta.data(), M, op->n, &e)) uni = false;
+      else if (b == 0) eps0 = e;
+      else if (e != eps0) uni = false;
+    }
+    op->route = uni ? GS_ROUTE_UNIFORM_1D : GS_ROUTE_NFFT_1D;
+    op->uniform_eps = uni ? eps0 : 0.0;
+  } else {
+    bool ten = allow_u && d.allow_tensor_route != 0;
+    int64_t Mb = 1;
+    if (ten) {
+      while (Mb < M && coords[2 * Mb] == coords[0]) ++Mb;
+      if (M % Mb != 0) ten = false;
+    }
+    int64_t Ma = ten ? M / Mb : 0;
+    double ex = 0, ey = 0;
+    std::vector<double> ax, ay;
+    for (int64_t b = 0; ten && b < B; ++b) {
+      const double* c = coords + b * M * 2;
+      for (int64_t a = 0; ten && a < Ma; ++a)
+        for (int64_t k = 0; k < Mb; ++k)
+          if (c[2 * (a * Mb + k)] != c[2 * a * Mb] || c[2 * (a * Mb + k) + 1] != c[2 * k + 1]) {
+            ten = false;
+            break;
+          }
+      if (!ten) break;
+      std::vector<double> za(Ma), zb(Mb);
+      for (int64_t a = 0; a < Ma; ++a) za[a] = std::ldexp(c[2 * a * Mb], -d.J);
+      for (int64_t k = 0; k < Mb; ++k) zb[k] = std::ldexp(c[2 * k + 1], -d.J);
+      double e1 = 0, e2 = 0;
+      if (!detect_uniform(za.data(), Ma, op->n, &e1) || !detect_uniform(zb.data(), Mb, op->n, &e2)) ten = false;
+      else if (b == 0) {
+        ex = e1;
+        ey = e2;
+      } else if (e1 != ex || e2 != ey) ten = false;
+    }
+    if (ten) {
+      try {
+        op->upx = make_uni(op.get(), Ma, ex);
+        op->upy = make_uni(op.get(), Mb, ey);
+      } catch (const GsError&) {
+        ten = false;
+      }
+    }
+    op->route = ten ? GS_ROUTE_TENSOR_2D : GS_ROUTE_NFFT_2D;
+    op->Ma = Ma;
+    op->Mb = Mb;
+  }
+
+  // ---- per-route construction, all per-point work on the device
+  DBuf<double> d_xi_x, d_xi_y, d_sw;
+  if (op->route == GS_ROUTE_UNIFORM_1D) {
+    op->up = make_uni(op.get(), M, op->uniform_eps);
+    make_twiddles(op.get(), op->up.N2, st);
+    d_xi_x.upload(xi_x.data(), total, st);
+    if (op->weighted) op->sqrtw.upload(sw.data(), total, st);
+    op->rec_u.alloc(total * op->Rr);
+    build_factors(op.get(), d_xi_x.p, op->weighted ? op->sqrtw.p : nullptr, total, op->rec_u.p, st);
+  } else if (op->route == GS_ROUTE_TENSOR_2D) {
+    const int64_t Ma = op->Ma, Mb = op->Mb;
+    std::vector<double> ax(B * Ma), ay(B * Mb);
+    for (int64_t b = 0; b < B; ++b) {
+      for (int64_t a = 0; a < Ma; ++a) ax[b * Ma + a] = coords[(b * M + a * Mb) * 2];
+      for (int64_t k = 0; k < Mb; ++k) ay[b * Mb + k] = coords[(b * M + k) * 2 + 1];
+    }
+    make_twiddles(op.get(), std::max(op->upx.N2, op->upy.N2), st);
+    DBuf<double> dax, day;
+    dax.upload(ax.data(), ax.size(), st);
+    day.upload(ay.data(), ay.size(), st);
+    op->rec_ax.alloc(B * Ma * op->Rr);
+    op->rec_ay.alloc(B * Mb * op->Rr);
+    build_factors(op.get(), dax.p, nullptr, B * Ma, op->rec_ax.p, st);
+    build_factors(op.get(), day.p, nullptr, B * Mb, op->rec_ay.p, st);
+    if (op->weighted) op->sqrtw.upload(sw.data(), total, st);
+    op->W.alloc(B * Ma * op->n);
+    CK(cudaStreamSynchronize(st));
+  } else {
+    // NfftPlan constants (nufft.cpp:190-230)
+    const double sigma = d.sigma > 0 ? d.sigma : 2.0;
+    const int w = d.w > 0 ? d.w : 6;
+    if (sigma < 1.25) fail(GS_ERR_DOMAIN, "oversampling factor must be >= 1.25");
+    if (w < 2) fail(GS_ERR_DOMAIN, "kernel half-width must be >= 2");
+    if (2 * w + 1 > 16) fail(GS_ERR_DOMAIN, "kernel half-width > 7 unsupported on this build");
+    const int n_ov = (int)std::ceil(sigma * (double)op->n / 2.0) * 2;
+    if (!is_pow2(n_ov)) fail(GS_ERR_DOMAIN, "oversampled length must be a power of two on this build");
+    if (n_ov > 4096) fail(GS_ERR_DOMAIN, "oversampled length > 4096 unsupported on this build");
+    {
+      double width = 2.0 * w;
+      double t = (width / sigma) * (width / sigma) * (sigma - 0.5) * (sigma - 0.5) - 0.8;
+      op->beta = GS_PI * std::sqrt(std::max(t, 1.0));
+    }
+    std::vector<double> dec(op->n);
+    for (long long k = -op->n / 2; k < op->n / 2; ++k)
+      dec[k + op->n / 2] = 1.0 / kb_transform((double)k / (double)n_ov, w, op->beta);
+    op->deconv.upload(dec.data(), dec.size(), st);
+    make_twiddles(op.get(), n_ov, st);
+    NfP& P = op->np;
+    P.n = (int)op->n;
+    P.n_ov = n_ov;
+    P.log_nov = ilog2(n_ov);
+    P.p = op->p;
+    P.edges = op->edges;
+    P.S = 2 * w + 1;
+    P.M = M;
+    P.T = std::min(16, n_ov);
+    P.R = P.T + P.S - 1;
+    P.nt = n_ov / P.T;
+    P.CW = std::max(1, std::min(8, (int)((120 * 1024) / ((n_ov + 1) * (int)sizeof(cplx)))));
+    while (n_ov % P.CW) --P.CW;
+    d_xi_x.upload(xi_x.data(), total, st);
+    if (d.dim == 2) d_xi_y.upload(xi_y.data(), total, st);
+    // 1. windows in the caller's order -> bin keys -> sort
+    DBuf<int> bx0, by0;
+    DBuf<double> wdummy;
+    bx0.alloc(total);
+    wdummy.alloc(total * P.S);
+    k_kb_window<<<nblk(total, 256), 256, 0, st>>>(d_xi_x.p, total, d.J, n_ov, w, op->beta, bx0.p, wdummy.p);
+    CKL();
+    if (d.dim == 2) {
+      by0.alloc(total);
+      k_kb_window<<<nblk(total, 256), 256, 0, st>>>(d_xi_y.p, total, d.J, n_ov, w, op->beta, by0.p, wdummy.p);
+      CKL();
+      sort_bins(op.get(), by0.p, bx0.p, P.nt * P.nt, P.T, P.nt, st);
+    } else {
+      sort_bins(op.get(), nullptr, bx0.p, n_ov, 1, 1, st);
+    }
+    // 2. sorted coordinates -> windows and factors in sorted order
+    DBuf<double> sx, sy, ssw;
+    sx.alloc(total);
+    k_gather_d<<<nblk(total, 256), 256, 0, st>>>(d_xi_x.p, op->perm.p, M, total, sx.p);
+    op->base_x.alloc(total);
+    op->wts_x.alloc(total * P.S);
+    k_kb_window<<<nblk(total, 256), 256, 0, st>>>(sx.p, total, d.J, n_ov, w, op->beta, op->base_x.p, op->wts_x.p);
+    if (op->weighted) {
+      d_sw.upload(sw.data(), total, st);
+      op->sqrtw.alloc(total);
+      k_gather_d<<<nblk(total, 256), 256, 0, st>>>(d_sw.p, op->perm.p, M, total, op->sqrtw.p);
+    }
+    op->rec_x.alloc(total * op->Rr);
+    build_factors(op.get(), sx.p, op->weighted ? op->sqrtw.p : nullptr, total, op->rec_x.p, st);
+    if (d.dim == 2) {
+      sy.alloc(total);
+      k_gather_d<<<nblk(total, 256), 256, 0, st>>>(d_xi_y.p, op->perm.p, M, total, sy.p);
+      op->base_y.alloc(total);
+      op->wts_y.alloc(total * P.S);
+      k_kb_window<<<nblk(total, 256), 256, 0, st>>>(sy.p, total, d.J, n_ov, w, op->beta, op->base_y.p, op->wts_y.p);
+      op->rec_y.alloc(total * op->Rr);
+      build_factors(op.get(), sy.p, nullptr, total, op->rec_y.p, st);
+      const int64_t ntiles = (int64_t)P.nt * P.nt;
+      op->G.alloc((size_t)B * n_ov * n_ov);
+      op->TB.alloc((size_t)B * ntiles * P.R * P.R);
+      if (op->edges) {
+        op->lines.alloc((size_t)B * 4 * op->p * n_ov);
+        op->TL.alloc((size_t)B * ntiles * 2 * 2 * op->p * P.R);
+        op->TC.alloc((size_t)B * ntiles * 4 * op->p * op->p);
+      }
+    } else {
+      op->G.alloc((size_t)B * n_ov);
+    }
+    CKL();
+    CK(cudaStreamSynchronize(st));
+  }
+  CK(cudaStreamSynchronize(st));
+  CKL();
+  return op.release();
+}
+
+// ------------------------------------------------------------------ applies
+// x, y are device pointers; perm_io: samples in the caller's order (true) or
+// the internal bin-sorted order (false, used inside CGLS).
+void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t st) {
+  const int B = op->B;
+  switch (op->route) {
+    case GS_ROUTE_UNIFORM_1D: {
+      const UniP& P = op->up;
+      k_uni_fwd<<<dim3(1, B), 256, uni_smem(P), st>>>(P, x, Strided{op->n, 0, 1}, op->rec_u.p, op->M * op->Rr, y,
+                                                     Strided{op->M, 0, 1}, nullptr, 0, op->tw.p, op->logLmax);
+      break;
+    }
+    case GS_ROUTE_TENSOR_2D: {
+      const int64_t n = op->n, Ma = op->Ma, Mb = op->Mb;
+      // W(a, j) = sum_i ax_a(i) X(i, j): one vector per column j
+      k_uni_fwd<<<dim3((unsigned)n, B), 256, uni_smem(op->upx), st>>>(
+          op->upx, x, Strided{n * n, n, 1}, op->rec_ax.p, Ma * op->Rr, op->W.p, Strided{Ma * n, 1, n}, nullptr, 0,
+          op->tw.p, op->logLmax);
+      // Y(a, b) = sum_j ay_b(j) W(a, j): one vector per row a
+      k_uni_fwd<<<dim3((unsigned)Ma, B), 256, uni_smem(op->upy), st>>>(
+          op->upy, op->W.p, Strided{Ma * n, n, 1}, op->rec_ay.p, Mb * op->Rr, y, Strided{op->M, Mb, 1},
+          op->weighted ? op->sqrtw.p : nullptr, op->M, op->tw.p, op->logLmax);
+      break;
+    }
+    case GS_ROUTE_NFFT_1D: {
+      const NfP& P = op->np;
+      k_n1_embed_fft<<<B, 256, P.n_ov * sizeof(cplx), st>>>(P, x, op->deconv.p, op->G.p, op->tw.p, op->logLmax);
+      k_n1_interp<<<dim3(nblk(op->M, 128), B), 128, 0, st>>>(P, op->base_x.p, op->wts_x.p, op->rec_x.p, op->G.p, x,
+                                                              perm_io ? op->perm.p : nullptr, y);
+      break;
+    }
+    case GS_ROUTE_NFFT_2D: {
+      const NfP& P = op->np;
+      k2_rows_embed_fft<<<dim3(P.n, B), 256, P.n_ov * sizeof(cplx), st>>>(P, x, op->deconv.p, op->G.p, op->tw.p,
+                                                                          op->logLmax);
+      k2_cols_fft<<<dim3(P.n_ov / P.CW, B), 256, (size_t)P.CW * (P.n_ov + 1) * sizeof(cplx), st>>>(P, op->G.p, op->tw.p,
+                                                                                                   op->logLmax);
+      if (P.edges)
+        k2_lines_fft<<<dim3(4 * P.p, B), 256, P.n_ov * sizeof(cplx), st>>>(P, x, op->deconv.p, op->lines.p, op->tw.p,
+                                                                           op->logLmax);
+      k2_interp<<<dim3(nblk(op->M, 128), B), 128, 0, st>>>(P, op->base_x.p, op->base_y.p, op->wts_x.p, op->wts_y.p,
+                                                            op->rec_x.p, op->rec_y.p, op->G.p, op->lines.p, x,
+                                                            perm_io ? op->perm.p : nullptr, y);
+      break;
+    }
+  }
+  CKL();
+}
+
+void adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t st) {
+  const int B = op->B;
+  switch (op->route) {
+    case GS_ROUTE_UNIFORM_1D: {
+      const UniP& P = op->up;
+      k_uni_adj<<<dim3(1, B), 256, uni_smem(P), st>>>(P, y, Strided{op->M, 0, 1}, nullptr, 0, op->rec_u.p,
+                                                     op->M * op->Rr, z, Strided{op->n, 0, 1}, op->tw.p, op->logLmax);
+      break;
+    }
+    case GS_ROUTE_TENSOR_2D: {
+      const int64_t n = op->n, Ma = op->Ma, Mb = op->Mb;
+      // V(a, j) = sum_b conj(ay_b(j)) (sqrt(mu) y)(a, b): one vector per row a
+      k_uni_adj<<<dim3((unsigned)Ma, B), 256, uni_smem(op->upy), st>>>(
+          op->upy, y, Strided{op->M, Mb, 1}, op->weighted ? op->sqrtw.p : nullptr, op->M, op->rec_ay.p, Mb * op->Rr,
+          op->W.p, Strided{Ma * n, n, 1}, op->tw.p, op->logLmax);
+      // X(i, j) = sum_a conj(ax_a(i)) V(a, j): one vector per column j
+      k_uni_adj<<<dim3((unsigned)n, B), 256, uni_smem(op->upx), st>>>(
+          op->upx, op->W.p, Strided{Ma * n, 1, n}, nullptr, 0, op->rec_ax.p, Ma * op->Rr, z, Strided{n * n, n, 1},
+          op->tw.p, op->logLmax);
+      break;
+    }
+    case GS_ROUTE_NFFT_1D: {
+      const NfP& P = op->np;
+      k_n1_spread<<<dim3(nblk(P.n_ov, 128), B), 128, 0, st>>>(P, op->bins.p, op->wts_x.p, op->rec_x.p, y,
+                                                               perm_io ? op->perm.p : nullptr, op->G.p);
+      k_n1_ifft_crop<<<B, 256, P.n_ov * sizeof(cplx), st>>>(P, op->G.p, op->deconv.p, op->rec_x.p, y,
+                                                            perm_io ? op->perm.p : nullptr, z, op->tw.p, op->logLmax);
+      break;
+    }
+    case GS_ROUTE_NFFT_2D: {
+      const NfP& P = op->np;
+      const int ntiles = P.nt * P.nt;
+      const size_t per_warp = (size_t)P.R * P.R + (P.edges ? 2 * 2 * P.p * P.R : 0);
+      k2_spread<<<dim3(ntiles, B), 32 * K2_WARPS, per_warp * K2_WARPS * sizeof(cplx), st>>>(
+          P, op->bins.p, op->base_x.p, op->base_y.p, op->wts_x.p, op->wts_y.p, op->rec_x.p, op->rec_y.p, y,
+          perm_io ? op->perm.p : nullptr, op->TB.p, op->TL.p, op->TC.p);
+      k2_cols_ifft_gather<<<dim3(P.n_ov / P.CW, B), 256, (size_t)P.CW * (P.n_ov + 1) * sizeof(cplx), st>>>(
+          P, op->TB.p, op->G.p, op->tw.p, op->logLmax);
+      k2_rows_ifft_crop<<<dim3(P.n, B), 256, P.n_ov * sizeof(cplx), st>>>(P, op->G.p, op->deconv.p, z, op->tw.p,
+                                                                          op->logLmax);
+      if (P.edges)
+        k2_edges<<<dim3(4 * P.p + 1, B), 256, P.n_ov * sizeof(cplx), st>>>(P, op->TL.p, op->TC.p, op->deconv.p, z,
+                                                                           op->tw.p, op->logLmax);
+      break;
+    }
+  }
+  CKL();
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int guard_call(const std::function<void()>& f) {
+  try {
+    f();
+    return GS_OK;
+  } catch (const GsError& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host out of memory";
+    return GS_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return GS_ERR_CUDA;
+  }
+}
+
+// ------------------------------------------------------------------ CGLS
+struct Session {
+  gs_op* op = nullptr;
+  int B = 1;
+  int64_t M = 0, Nc = 0;
+  double tol = 1e-10;
+  int hist_cap = 0;
+  int it = 0;
+  DBuf<cplx> b, r, q, x, p, s;
+  DBuf<CgState> st;
+  DBuf<double> n2, part, hist;
+  DBuf<int> flag;
+  int chunks_M = 1, chunks_N = 1;
+};
+
+void norm2(Session& S, const cplx* v, int64_t len, int chunks, cudaStream_t st) {
+  if (chunks <= 1) {
+    k_norm2<<<S.B, 1024, 0, st>>>(v, len, S.n2.p);
+  } else {
+    k_norm2_part<<<dim3(chunks, S.B), 512, 0, st>>>(v, len, chunks, S.part.p);
+    k_norm2_fold<<<nblk(S.B, 128), 128, 0, st>>>(S.part.p, chunks, S.B, S.n2.p);
+  }
+  CKL();
+}
+
+int pick_chunks(int B, int64_t len) {
+  int c = (int)std::max<int64_t>(1, std::min<int64_t>(64, (296 + B - 1) / B));
+  c = (int)std::min<int64_t>(c, std::max<int64_t>(1, len / 4096));
+  return c;
+}
+
+void session_begin(Session& S, gs_op* op, const cplx* b_raw, bool b_perm, const cplx* x0, double tol, int hist_cap,
+                   cudaStream_t st) {
+  S.op = op;
+  S.B = op->B;
+  S.M = op->M;
+  S.Nc = op->Nc;
+  S.tol = tol;
+  S.hist_cap = hist_cap;
+  S.it = 0;
+  const int64_t TM = S.M * S.B, TN = S.Nc * S.B;
+  S.b.alloc(TM);
+  S.r.alloc(TM);
+  S.q.alloc(TM);
+  S.x.alloc(TN);
+  S.p.alloc(TN);
+  S.s.alloc(TN);
+  S.st.alloc(S.B);
+  S.n2.alloc(S.B);
+  S.chunks_M = pick_chunks(S.B, S.M);
+  S.chunks_N = pick_chunks(S.B, S.Nc);
+  S.part.alloc((size_t)S.B * std::max(S.chunks_M, S.chunks_N));
+  S.hist.alloc((size_t)S.B * hist_cap);
+  S.flag.alloc(1);
+  const bool sorted = op->route == GS_ROUTE_NFFT_1D || op->route == GS_ROUTE_NFFT_2D;
+  // b = sqrt(mu) o b_raw in internal order (solver.cpp:30-33); the tensor route
+  // applies sqrt(mu) inside T, so it takes the raw data scaled here as well.
+  k_gather_scale<<<nblk(TM, 256), 256, 0, st>>>(b_raw, (sorted && b_perm) ? op->perm.p : nullptr,
+                                                op->weighted ? op->sqrtw.p : nullptr, S.M, S.B, S.b.p);
+  CKL();
+  // ref = ||T* b||   (solver.cpp:42)
+  adjoint_dev(op, S.b.p, S.s.p, false, st);
+  norm2(S, S.s.p, S.Nc, S.chunks_N, st);
+  k_cg_ref<<<nblk(S.B, 128), 128, 0, st>>>(S.st.p, S.n2.p, S.B);
+  // x = x0 or 0; r = b - T x; s = T* r; gamma; p = s   (solver.cpp:35-68)
+  if (x0) CK(cudaMemcpyAsync(S.x.p, x0, TN * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+  else CK(cudaMemsetAsync(S.x.p, 0, TN * sizeof(cplx), st));
+  forward_dev(op, S.x.p, S.q.p, false, st);
+  k_sub<<<nblk(TM, 256), 256, 0, st>>>(S.b.p, S.q.p, TM, S.r.p);
+  adjoint_dev(op, S.r.p, S.s.p, false, st);
+  norm2(S, S.s.p, S.Nc, S.chunks_N, st);
+  k_cg_gamma0<<<nblk(S.B, 128), 128, 0, st>>>(S.st.p, S.n2.p, tol, S.hist.p, hist_cap, S.B);
+  CK(cudaMemcpyAsync(S.p.p, S.s.p, TN * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+  CKL();
+}
+
+// one CGLS iteration for every still-active problem (solver.cpp:70-88)
+void session_iterate(Session& S, cudaStream_t st) {
+  gs_op* op = S.op;
+  const int64_t TM = S.M * S.B, TN = S.Nc * S.B;
+  const int it = ++S.it;
+  forward_dev(op, S.p.p, S.q.p, false, st);                          // q = T p
+  norm2(S, S.q.p, S.M, S.chunks_M, st);                              // qq
+  k_cg_alpha<<<nblk(S.B, 128), 128, 0, st>>>(S.st.p, S.n2.p, S.B);   // alpha (or stop)
+  k_axpy_alpha<<<nblk(TN, 256), 256, 0, st>>>(S.x.p, S.p.p, S.Nc, S.B, S.st.p, 1.0);   // x += alpha p
+  k_axpy_alpha<<<nblk(TM, 256), 256, 0, st>>>(S.r.p, S.q.p, S.M, S.B, S.st.p, -1.0);   // r -= alpha q
+  adjoint_dev(op, S.r.p, S.s.p, false, st);                          // s = T* r
+  norm2(S, S.s.p, S.Nc, S.chunks_N, st);                             // gamma'
+  k_cg_beta<<<nblk(S.B, 128), 128, 0, st>>>(S.st.p, S.n2.p, S.tol, it < S.hist_cap ? it : S.hist_cap - 1, S.hist.p,
+                                            S.hist_cap, S.B);
+  k_pupdate<<<nblk(TN, 256), 256, 0, st>>>(S.p.p, S.s.p, S.Nc, S.B, S.st.p);           // p = s + beta p
+  CKL();
+}
+
+bool session_any_active(Session& S, cudaStream_t st) {
+  k_any_active<<<1, 256, 0, st>>>(S.st.p, S.B, S.flag.p);
+  int h = 0;
+  CK(cudaMemcpyAsync(&h, S.flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return h != 0;
+}
+
+}  // namespace
+
+// ====================================================================== C-ABI
+struct gs_cgls_session {
+  Session s;
+};
+
+extern "C" {
+
+const char* gs_last_error(void) { return g_err.c_str(); }
+int gs_build_arch(void) { return 100; }
+
+int gs_op_create(const gs_op_desc* desc, gs_op** out) {
+  return guard_call([&] {
+    if (!out) fail(GS_ERR_USAGE, "null output handle");
+    *out = create(desc);
+  });
+}
+
+int gs_op_destroy(gs_op* op) {
+  if (!op) return GS_OK;
+  cudaSetDevice(op->device);
+  cudaDeviceSynchronize();
+  delete op;
+  return GS_OK;
+}
+
+int gs_op_info(const gs_op* op, gs_op_info_t* info) {
+  if (!op || !info) {
+    g_err = "null argument";
+    return GS_ERR_USAGE;
+  }
+  info->dim = op->dim;
+  info->family_p = op->p;
+  info->J = op->J;
+  info->batch = op->B;
+  info->route = op->route;
+  info->rows = op->M;
+  info->cols = op->Nc;
+  info->uniform_fast = op->route == GS_ROUTE_UNIFORM_1D;
+  info->uniform_epsilon = op->uniform_eps;
+  info->weighted = op->weighted;
+  info->n_over = (op->route == GS_ROUTE_NFFT_1D || op->route == GS_ROUTE_NFFT_2D) ? op->np.n_ov : 0;
+  info->device_bytes = (int64_t)op->device_bytes();
+  return GS_OK;
+}
+
+static void apply_common(gs_op* op, const double* in, int64_t in_len, int64_t want_in, double* out, int64_t out_len,
+                         void* stream, bool fwd) {
+  if (!op || !in || !out) fail(GS_ERR_USAGE, "null argument");
+  if (in_len != want_in)
+    fail(GS_ERR_SHAPE, fwd ? "coefficient vector length mismatch" : "sample vector length mismatch");
+  std::lock_guard<std::mutex> lk(op->mu);
+  CK(cudaSetDevice(op->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool din = is_device_ptr(in), dout = is_device_ptr(out);
+  const cplx* src = (const cplx*)in;
+  cplx* dst = (cplx*)out;
+  if (!din) {
+    op->stage_a.alloc(in_len);
+    CK(cudaMemcpyAsync(op->stage_a.p, in, in_len * sizeof(cplx), cudaMemcpyHostToDevice, st));
+    src = op->stage_a.p;
+  }
+  if (!dout) {
+    op->stage_b.alloc(out_len);
+    dst = op->stage_b.p;
+  }
+  if (fwd) forward_dev(op, src, dst, true, st);
+  else adjoint_dev(op, src, dst, true, st);
+  if (!dout) {
+    CK(cudaMemcpyAsync(out, dst, out_len * sizeof(cplx), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  } else if (!din) {
+    CK(cudaStreamSynchronize(st));  // staging buffer reuse
+  }
+}
+
+int gs_apply_forward(gs_op* op, const double* coeffs, int64_t coeffs_len, double* samples, void* stream) {
+  return guard_call([&] {
+    if (!op) fail(GS_ERR_USAGE, "null handle");
+    apply_common(op, coeffs, coeffs_len, op->Nc * op->B, samples, op->M * op->B, stream, true);
+  });
+}
+
+int gs_apply_adjoint(gs_op* op, const double* samples, int64_t samples_len, double* coeffs, void* stream) {
+  return guard_call([&] {
+    if (!op) fail(GS_ERR_USAGE, "null handle");
+    apply_common(op, samples, samples_len, op->M * op->B, coeffs, op->Nc * op->B, stream, false);
+  });
+}
+
+// ---- CGLS sessions: begin (preamble), step (n iterations, no host sync), finish
+int gs_cgls_begin(gs_op* op, const double* raw_samples, int64_t samples_len, const double* x0, double tolerance,
+                  int history_capacity, void* stream, gs_cgls_session** out) {
+  return guard_call([&] {
+    if (!op || !raw_samples || !out) fail(GS_ERR_USAGE, "null argument");
+    if (samples_len != op->M * op->B) fail(GS_ERR_SHAPE, "sample vector length mismatch");
+    if (!(tolerance > 0)) fail(GS_ERR_DOMAIN, "tolerance must be positive");
+    std::lock_guard<std::mutex> lk(op->mu);
+    CK(cudaSetDevice(op->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    std::unique_ptr<gs_cgls_session> S(new gs_cgls_session);
+    const int64_t TM = op->M * op->B, TN = op->Nc * op->B;
+    const cplx* b = (const cplx*)raw_samples;
+    DBuf<cplx> sb, sx;
+    if (!is_device_ptr(raw_samples)) {
+      sb.upload((const cplx*)raw_samples, TM, st);
+      b = sb.p;
+    }
+    const cplx* xx = (const cplx*)x0;
+    if (x0 && !is_device_ptr(x0)) {
+      sx.upload((const cplx*)x0, TN, st);
+      xx = sx.p;
+    }
+    session_begin(S->s, op, b, true, xx, tolerance, std::max(2, history_capacity), st);
+    CK(cudaStreamSynchronize(st));
+    *out = S.release();
+  });
+}
+
+int gs_cgls_step(gs_cgls_session* s, int iterations, void* stream) {
+  return guard_call([&] {
+    if (!s) fail(GS_ERR_USAGE, "null session");
+    std::lock_guard<std::mutex> lk(s->s.op->mu);
+    CK(cudaSetDevice(s->s.op->device));
+    for (int i = 0; i < iterations; ++i) session_iterate(s->s, (cudaStream_t)stream);
+  });
+}
+
+int gs_cgls_active(gs_cgls_session* s, void* stream, int* any_active) {
+  return guard_call([&] {
+    if (!s || !any_active) fail(GS_ERR_USAGE, "null argument");
+    std::lock_guard<std::mutex> lk(s->s.op->mu);
+    *any_active = session_any_active(s->s, (cudaStream_t)stream) ? 1 : 0;
+  });
+}
+
+int gs_cgls_finish(gs_cgls_session* s, double* x_out, gs_solve_stats* stats, double* history, void* stream) {
+  return guard_call([&] {
+    if (!s) fail(GS_ERR_USAGE, "null session");
+    Session& S = s->s;
+    std::lock_guard<std::mutex> lk(S.op->mu);
+    CK(cudaSetDevice(S.op->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t TN = S.Nc * S.B;
+    k_zero_if_ref0<<<nblk(TN, 256), 256, 0, st>>>(S.x.p, S.Nc, S.B, S.st.p);
+    CKL();
+    if (x_out) CK(cudaMemcpyAsync(x_out, S.x.p, TN * sizeof(cplx), cudaMemcpyDefault, st));
+    std::vector<CgState> hs(S.B);
+    CK(cudaMemcpyAsync(hs.data(), S.st.p, S.B * sizeof(CgState), cudaMemcpyDeviceToHost, st));
+    std::vector<double> hh((size_t)S.B * S.hist_cap);
+    CK(cudaMemcpyAsync(hh.data(), S.hist.p, hh.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int b = 0; b < S.B; ++b) {
+      const CgState& c = hs[b];
+      int hl = std::max(1, std::min(c.hist_len, S.hist_cap));
+      if (stats) {
+        stats[b].iterations = c.iterations;
+        stats[b].converged = c.converged;
+        stats[b].residual = c.ref == 0.0 ? 0.0 : hh[(size_t)b * S.hist_cap + hl - 1];
+      }
+      if (history)
+        for (int i = 0; i < hl; ++i) history[(size_t)b * S.hist_cap + i] = hh[(size_t)b * S.hist_cap + i];
+    }
+  });
+}
+
+int gs_cgls_destroy(gs_cgls_session* s) {
+  delete s;
+  return GS_OK;
+}
+
+int gs_solve_least_squares(gs_op* op, const double* raw_samples, int64_t samples_len, const double* x0,
+                           int max_iterations, double tolerance, double* x_out, gs_solve_stats* stats,
+                           double* history, void* stream) {
+  gs_cgls_session* s = nullptr;
+  if (!op) {
+    g_err = "null handle";
+    return GS_ERR_USAGE;
+  }
+  const int max_iter = max_iterations > 0 ? max_iterations : (int)std::min<int64_t>(INT32_MAX / 2, 2 * op->Nc);
+  int rc = gs_cgls_begin(op, raw_samples, samples_len, x0, tolerance, max_iter + 1, stream, &s);
+  if (rc) return rc;
+  int done = 0;
+  int active = 1;
+  rc = gs_cgls_active(s, stream, &active);
+  int chunk = 4;
+  while (rc == 0 && active && done < max_iter) {
+    int k = std::min(chunk, max_iter - done);
+    rc = gs_cgls_step(s, k, stream);
+    done += k;
+    if (rc == 0) rc = gs_cgls_active(s, stream, &active);
+    chunk = std::min(chunk * 2, 64);
+  }
+  if (rc == 0) rc = gs_cgls_finish(s, x_out, stats, history, stream);
+  gs_cgls_destroy(s);
+  return rc;
+}
+
+int gs_op_export_factors(gs_op* op, int b, int axis, double* D, double* L, double* R) {
+  return guard_call([&] {
+    if (!op || !D) fail(GS_ERR_USAGE, "null argument");
+    if (b < 0 || b >= op->B) fail(GS_ERR_USAGE, "problem index out of range");
+    if (axis < 0 || axis >= op->dim) fail(GS_ERR_USAGE, "axis out of range");
+    std::lock_guard<std::mutex> lk(op->mu);
+    CK(cudaSetDevice(op->device));
+    const int64_t M = op->M;
+    const int Rr = op->Rr, p = op->p;
+    std::vector<cplx> recs(M * Rr);  // per point in the caller's order
+    if (op->route == GS_ROUTE_UNIFORM_1D) {
+      CK(cudaMemcpy(recs.data(), op->rec_u.p + b * M * Rr, M * Rr * sizeof(cplx), cudaMemcpyDeviceToHost));
+    } else if (op->route == GS_ROUTE_TENSOR_2D) {
+      const int64_t Ma = op->Ma, Mb = op->Mb;
+      const int64_t Ml = axis == 0 ? Ma : Mb;
+      std::vector<cplx> ax(Ml * Rr);
+      CK(cudaMemcpy(ax.data(), (axis == 0 ? op->rec_ax.p + b * Ma * Rr : op->rec_ay.p + b * Mb * Rr),
+                    Ml * Rr * sizeof(cplx), cudaMemcpyDeviceToHost));
+      std::vector<double> sw;
+      if (op->weighted && axis == 0) {
+        sw.resize(M);
+        CK(cudaMemcpy(sw.data(), op->sqrtw.p + b * M, M * sizeof(double), cudaMemcpyDeviceToHost));
+      }
+      for (int64_t m = 0; m < M; ++m) {
+        const int64_t k = axis == 0 ? m / Mb : m % Mb;
+        for (int c = 0; c < Rr; ++c) recs[m * Rr + c] = sw.empty() ? ax[k * Rr + c] : cscale(ax[k * Rr + c], sw[m]);
+      }
+    } else {
+      std::vector<cplx> srt(M * Rr);
+      std::vector<int> pm(M);
+      CK(cudaMemcpy(srt.data(), (axis == 0 ? op->rec_x.p : op->rec_y.p) + b * M * Rr, M * Rr * sizeof(cplx),
+                    cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(pm.data(), op->perm.p + b * M, M * sizeof(int), cudaMemcpyDeviceToHost));
+      for (int64_t s = 0; s < M; ++s)
+        for (int c = 0; c < Rr; ++c) recs[(int64_t)pm[s] * Rr + c] = srt[s * Rr + c];
+    }
+    for (int64_t m = 0; m < M; ++m) {
+      D[2 * m] = recs[m * Rr].x;
+      D[2 * m + 1] = recs[m * Rr].y;
+      if (op->edges) {
+        for (int c = 0; c < p; ++c) {  // Eigen col-major M x p: (m, c) at c*M + m
+          if (L) {
+            L[2 * (c * M + m)] = recs[m * Rr + 1 + c].x;
+            L[2 * (c * M + m) + 1] = recs[m * Rr + 1 + c].y;
+          }
+          if (R) {
+            R[2 * (c * M + m)] = recs[m * Rr + 1 + p + c].x;
+            R[2 * (c * M + m) + 1] = recs[m * Rr + 1 + p + c].y;
+          }
+        }
+      }
+    }
+  });
+}
+
+}  // extern "C"

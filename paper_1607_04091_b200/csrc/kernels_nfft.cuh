@@ -1,0 +1,515 @@
+// kernels_nfft.cuh -- Kaiser-Bessel gridding routes (K-N1 / K-N2 / K-F / K-DC /
+// K-D / K-S of SURVEY 2.3), restating NfftPlan::forward / ::adjoint
+// (nufft.cpp:244-365) fused with the 1D and 9-block 2D operator algebra of
+// apply_forward / apply_adjoint (freq2wave.cpp:215-387).
+//
+// Sample-space data (base cell, 13 window weights, D/L/R record) is held in
+// bin-sorted order ("s" index); perm[s] maps back to the caller's order.
+// Spreading (the adjoint) is output-owned, never a global atomic:
+//   1D  -- one thread per oversampled cell gathers from the sorted bins;
+//   2D  -- one CTA per 16x16 grid tile accumulates its points into
+//          per-warp shared-memory copies of the tile+halo, writes the region
+//          once, and the inverse column FFT gathers the <= 4 overlapping
+//          tile regions that cover each cell while loading.
+#pragma once
+#include "gs_common.cuh"
+
+struct NfP {
+  int n;        // modes per axis (2^J)
+  int n_ov;     // oversampled length per axis (power of two)
+  int log_nov;
+  int p, edges; // family, edges = p >= 2
+  int S;        // 2w+1 taps
+  int64_t M;    // samples per problem
+  // 2D tiling
+  int T, R, nt; // tile edge, region edge = T + S - 1, tiles per axis
+  int CW;       // columns per CTA in the column-FFT kernels
+};
+
+// ============================================================== 1D route
+// deconvolve + embed + FFT_{-}  (nufft.cpp:247-269), edge slots zeroed (freq2wave.cpp:224-230)
+__global__ void k_n1_embed_fft(NfP P, const cplx* __restrict__ x, const double* __restrict__ deconv,
+                               cplx* __restrict__ G, const cplx* __restrict__ tw, int logLmax) {
+  extern __shared__ cplx sm[];
+  const int prob = blockIdx.x;
+  x += (int64_t)prob * P.n;
+  G += (int64_t)prob * P.n_ov;
+  for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) sm[i] = mk(0, 0);
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < P.n; idx += blockDim.x) {
+    int k = idx - P.n / 2;
+    cplx v = x[idx];
+    if (P.edges && (idx < P.p || idx >= P.n - P.p)) v = mk(0, 0);
+    int pos = (k + P.n_ov) & (P.n_ov - 1);
+    sm[bitrev(pos, P.log_nov)] = cscale(v, deconv[idx]);
+  }
+  __syncthreads();
+  block_fft_bitrev(sm, P.log_nov, 1, 0, tw, logLmax, -1);
+  for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) G[i] = sm[i];
+}
+
+// interpolation + D + L/R  (nufft.cpp:273-284, freq2wave.cpp:232-236)
+__global__ void k_n1_interp(NfP P, const int* __restrict__ base, const double* __restrict__ wts,
+                            const cplx* __restrict__ rec, const cplx* __restrict__ G, const cplx* __restrict__ x,
+                            const int* __restrict__ out_perm, cplx* __restrict__ y) {
+  const int prob = blockIdx.y;
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= P.M) return;
+  const int64_t gs = prob * P.M + s;
+  const int Rr = 1 + (P.edges ? 2 * P.p : 0);
+  const cplx* g = G + (int64_t)prob * P.n_ov;
+  const int b = base[gs];
+  const double* w = wts + gs * P.S;
+  cplx acc = mk(0, 0);
+  for (int t = 0; t < P.S; ++t) acc = caxpy(acc, w[t], ldg2(g + ((b + t) & (P.n_ov - 1))));
+  const cplx* r = rec + gs * Rr;
+  cplx ym = cmul(r[0], acc);
+  if (P.edges) {
+    const cplx* xp = x + (int64_t)prob * P.n;
+    cplx a = mk(0, 0), c2 = mk(0, 0);
+    for (int c = 0; c < P.p; ++c) a = cadd(a, cmul(r[1 + c], ldg2(xp + c)));
+    for (int c = 0; c < P.p; ++c) c2 = cadd(c2, cmul(r[1 + P.p + c], ldg2(xp + P.n - P.p + c)));
+    ym = cadd(ym, cadd(a, c2));
+  }
+  const int64_t o = out_perm ? (int64_t)out_perm[gs] : s;
+  y[prob * P.M + o] = ym;
+}
+
+// spreading, owner-computes: cell j sums w_s[t] conj(D_s) y_s over the points
+// whose window base is (j - t) mod n_ov  (transpose of nufft.cpp:313-322)
+__global__ void k_n1_spread(NfP P, const int* __restrict__ cell_start, const double* __restrict__ wts,
+                            const cplx* __restrict__ rec, const cplx* __restrict__ yin, const int* __restrict__ in_perm,
+                            cplx* __restrict__ line) {
+  const int prob = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= P.n_ov) return;
+  const int Rr = 1 + (P.edges ? 2 * P.p : 0);
+  const int* cs = cell_start + (int64_t)prob * (P.n_ov + 1);
+  const cplx* yp = yin + (int64_t)prob * P.M;
+  cplx acc = mk(0, 0);
+  for (int t = 0; t < P.S; ++t) {
+    const int cell = (j - t + P.n_ov) & (P.n_ov - 1);
+    for (int s = cs[cell]; s < cs[cell + 1]; ++s) {
+      const int64_t gs = prob * P.M + s;
+      const cplx yv = ldg2(yp + (in_perm ? (int64_t)in_perm[gs] : s));
+      const cplx v = cmul(conj_(ldg2(rec + gs * Rr)), yv);
+      acc = caxpy(acc, __ldg(wts + gs * P.S + t), v);
+    }
+  }
+  line[(int64_t)prob * P.n_ov + j] = acc;
+}
+
+// FFT_{+}, crop, deconvolve (nufft.cpp:340-350); edge slots <- L^H y, R^H y
+// (freq2wave.cpp:317-325)
+__global__ void k_n1_ifft_crop(NfP P, const cplx* __restrict__ line, const double* __restrict__ deconv,
+                               const cplx* __restrict__ rec, const cplx* __restrict__ yin,
+                               const int* __restrict__ in_perm, cplx* __restrict__ z, const cplx* __restrict__ tw,
+                               int logLmax) {
+  extern __shared__ cplx sm[];
+  __shared__ double red[32];
+  const int prob = blockIdx.x;
+  line += (int64_t)prob * P.n_ov;
+  z += (int64_t)prob * P.n;
+  for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) sm[bitrev(i, P.log_nov)] = line[i];
+  __syncthreads();
+  block_fft_bitrev(sm, P.log_nov, 1, 0, tw, logLmax, +1);
+  for (int idx = threadIdx.x; idx < P.n; idx += blockDim.x) {
+    int k = idx - P.n / 2;
+    cplx v = cscale(sm[(k + P.n_ov) & (P.n_ov - 1)], deconv[idx]);
+    if (P.edges && (idx < P.p || idx >= P.n - P.p)) v = mk(0, 0);
+    z[idx] = v;
+  }
+  if (!P.edges) return;
+  const int Rr = 1 + 2 * P.p;
+  cplx eh[8], et[8];
+  for (int c = 0; c < 8; ++c) eh[c] = et[c] = mk(0, 0);
+  for (int64_t s = threadIdx.x; s < P.M; s += blockDim.x) {
+    const int64_t gs = prob * P.M + s;
+    const cplx u = yin[prob * P.M + (in_perm ? (int64_t)in_perm[gs] : s)];
+    const cplx* r = rec + gs * Rr;
+    for (int c = 0; c < P.p; ++c) {
+      eh[c] = cadd(eh[c], cmul(conj_(r[1 + c]), u));
+      et[c] = cadd(et[c], cmul(conj_(r[1 + P.p + c]), u));
+    }
+  }
+  __syncthreads();
+  for (int c = 0; c < P.p; ++c) {
+    double hr = block_sum(eh[c].x, red), hi = block_sum(eh[c].y, red);
+    double tr = block_sum(et[c].x, red), ti = block_sum(et[c].y, red);
+    if (threadIdx.x == 0) {
+      z[c] = mk(hr, hi);
+      z[P.n - P.p + c] = mk(tr, ti);
+    }
+  }
+}
+
+// ============================================================== 2D route
+// Grid layout: G[prob][r][c], axis0 (rows) = y, axis1 (cols) = x, last axis
+// fastest (freq2wave.cpp:183-190).  Coefficients X(i, j) = x[j*n + i], i = x.
+
+// rows of the embedded interior block, deconvolved, FFT_{-} along x
+// (nufft.cpp:253-266 row part + freq2wave.cpp:246-254)
+__global__ void k2_rows_embed_fft(NfP P, const cplx* __restrict__ x, const double* __restrict__ deconv,
+                                  cplx* __restrict__ G, const cplx* __restrict__ tw, int logLmax) {
+  extern __shared__ cplx sm[];
+  const int j = blockIdx.x, prob = blockIdx.y;
+  const int r = (j - P.n / 2 + P.n_ov) & (P.n_ov - 1);
+  cplx* grow = G + ((int64_t)prob * P.n_ov + r) * P.n_ov;
+  if (P.edges && (j < P.p || j >= P.n - P.p)) {
+    for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) grow[i] = mk(0, 0);
+    return;
+  }
+  const cplx* xr = x + (int64_t)prob * P.n * P.n + (int64_t)j * P.n;
+  for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) sm[i] = mk(0, 0);
+  __syncthreads();
+  const double d0 = deconv[j];
+  for (int i = threadIdx.x; i < P.n; i += blockDim.x) {
+    cplx v = xr[i];
+    if (P.edges && (i < P.p || i >= P.n - P.p)) v = mk(0, 0);
+    int pos = (i - P.n / 2 + P.n_ov) & (P.n_ov - 1);
+    sm[bitrev(pos, P.log_nov)] = cscale(v, d0 * deconv[i]);
+  }
+  __syncthreads();
+  block_fft_bitrev(sm, P.log_nov, 1, 0, tw, logLmax, -1);
+  for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) grow[i] = sm[i];
+}
+
+// FFT_{-} along y of CW columns; only the n rows carrying data are loaded
+__global__ void k2_cols_fft(NfP P, cplx* __restrict__ G, const cplx* __restrict__ tw, int logLmax) {
+  extern __shared__ cplx sm[];
+  const int c0 = blockIdx.x * P.CW, prob = blockIdx.y;
+  const int ls = P.n_ov + 1;
+  cplx* g = G + (int64_t)prob * P.n_ov * P.n_ov;
+  for (int i = threadIdx.x; i < P.CW * ls; i += blockDim.x) sm[i] = mk(0, 0);
+  __syncthreads();
+  for (int t = threadIdx.x; t < P.n * P.CW; t += blockDim.x) {
+    const int jj = t / P.CW, cc = t - jj * P.CW;
+    const int r = (jj - P.n / 2 + P.n_ov) & (P.n_ov - 1);
+    sm[cc * ls + bitrev(r, P.log_nov)] = g[(int64_t)r * P.n_ov + c0 + cc];
+  }
+  __syncthreads();
+  block_fft_bitrev(sm, P.log_nov, P.CW, ls, tw, logLmax, -1);
+  for (int t = threadIdx.x; t < P.n_ov * P.CW; t += blockDim.x) {
+    const int r = t / P.CW, cc = t - r * P.CW;
+    g[(int64_t)r * P.n_ov + c0 + cc] = sm[cc * ls + r];
+  }
+}
+
+// The 4p side lines (freq2wave.cpp:272-301): line e < 2p runs along y at the
+// x-edge index i_e (rows 0..p-1, n-p..n-1 of X), e >= 2p along x at the
+// y-edge index j_e.  Interior entries only, deconvolved, FFT_{-}.
+__device__ __forceinline__ int edge_index(int e, int n, int p) { return e < p ? e : n - 2 * p + e; }
+
+__global__ void k2_lines_fft(NfP P, const cplx* __restrict__ x, const double* __restrict__ deconv,
+                             cplx* __restrict__ lines, const cplx* __restrict__ tw, int logLmax) {
+  extern __shared__ cplx sm[];
+  const int L = blockIdx.x, prob = blockIdx.y;
+  const int twop = 2 * P.p;
+  const bool yline = L < twop;
+  const int e = yline ? L : L - twop;
+  const int fixed = edge_index(e, P.n, P.p);
+  const cplx* X = x + (int64_t)prob * P.n * P.n;
+  for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) sm[i] = mk(0, 0);
+  __syncthreads();
+  for (int v = P.p + threadIdx.x; v < P.n - P.p; v += blockDim.x) {
+    cplx val = yline ? X[(int64_t)v * P.n + fixed] : X[(int64_t)fixed * P.n + v];
+    int pos = (v - P.n / 2 + P.n_ov) & (P.n_ov - 1);
+    sm[bitrev(pos, P.log_nov)] = cscale(val, deconv[v]);
+  }
+  __syncthreads();
+  block_fft_bitrev(sm, P.log_nov, 1, 0, tw, logLmax, -1);
+  cplx* out = lines + ((int64_t)prob * 2 * twop + L) * P.n_ov;
+  for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) out[i] = sm[i];
+}
+
+// Per-point forward: 2D interpolation (nufft.cpp:287-303) scaled by Dx Dy,
+// 4 corner blocks (freq2wave.cpp:260-270), 4p side interpolations
+// (freq2wave.cpp:272-301).  axis 0 = x, 1 = y in the sorted arrays.
+__global__ void k2_interp(NfP P, const int* __restrict__ base_x, const int* __restrict__ base_y,
+                          const double* __restrict__ wx_all, const double* __restrict__ wy_all,
+                          const cplx* __restrict__ recx_all, const cplx* __restrict__ recy_all,
+                          const cplx* __restrict__ G, const cplx* __restrict__ lines, const cplx* __restrict__ x,
+                          const int* __restrict__ out_perm, cplx* __restrict__ y) {
+  const int prob = blockIdx.y;
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= P.M) return;
+  const int64_t gs = prob * P.M + s;
+  const int S = P.S, mask = P.n_ov - 1, p = P.p;
+  const int Rr = 1 + (P.edges ? 2 * p : 0);
+  const int by = base_y[gs], bx = base_x[gs];
+  const double* wy = wy_all + gs * S;
+  const double* wx = wx_all + gs * S;
+  double wyr[16], wxr[16];
+  for (int t = 0; t < S; ++t) {
+    wyr[t] = wy[t];
+    wxr[t] = wx[t];
+  }
+  const cplx* g = G + (int64_t)prob * P.n_ov * P.n_ov;
+  cplx acc = mk(0, 0);
+  for (int t0 = 0; t0 < S; ++t0) {
+    const cplx* row = g + (int64_t)((by + t0) & mask) * P.n_ov;
+    cplx ra = mk(0, 0);
+    for (int t1 = 0; t1 < S; ++t1) ra = caxpy(ra, wxr[t1], ldg2(row + ((bx + t1) & mask)));
+    acc = caxpy(acc, wyr[t0], ra);
+  }
+  const cplx* rx = recx_all + gs * Rr;
+  const cplx* ry = recy_all + gs * Rr;
+  const cplx Dx = rx[0], Dy = ry[0];
+  cplx out = cmul(cmul(Dx, Dy), acc);
+  if (P.edges) {
+    const cplx* X = x + (int64_t)prob * P.n * P.n;
+    const int n = P.n, np = n - p;
+    // corners: (Lx,Ly) (Lx,Ry) (Rx,Ly) (Rx,Ry)
+    for (int k = 0; k < 4; ++k) {
+      const int ax = (k < 2) ? 1 : 1 + p;        // record offset of Ax columns
+      const int by_ = (k % 2 == 0) ? 1 : 1 + p;  // record offset of By columns
+      const int row0 = (k < 2) ? 0 : np, col0 = (k % 2 == 0) ? 0 : np;
+      cplx sum = mk(0, 0);
+      for (int j = 0; j < p; ++j) {
+        cplx t = mk(0, 0);
+        for (int i = 0; i < p; ++i) t = cadd(t, cmul(rx[ax + i], ldg2(X + (int64_t)(col0 + j) * n + row0 + i)));
+        sum = cadd(sum, cmul(t, ry[by_ + j]));
+      }
+      out = cadd(out, sum);
+    }
+    const cplx* LY = lines + (int64_t)prob * 4 * p * P.n_ov;
+    const cplx* LX = LY + (int64_t)2 * p * P.n_ov;
+    // side_x_edge (Lx then Rx): y-lines, weights along y
+    for (int e = 0; e < 2 * p; ++e) {
+      const cplx* ln = LY + (int64_t)e * P.n_ov;
+      cplx u = mk(0, 0);
+      for (int t = 0; t < S; ++t) u = caxpy(u, wyr[t], ldg2(ln + ((by + t) & mask)));
+      out = cadd(out, cmul(cmul(rx[1 + e], Dy), u));
+    }
+    // side_y_edge (Ly then Ry): x-lines, weights along x
+    for (int e = 0; e < 2 * p; ++e) {
+      const cplx* ln = LX + (int64_t)e * P.n_ov;
+      cplx u = mk(0, 0);
+      for (int t = 0; t < S; ++t) u = caxpy(u, wxr[t], ldg2(ln + ((bx + t) & mask)));
+      out = cadd(out, cmul(cmul(ry[1 + e], Dx), u));
+    }
+  }
+  const int64_t o = out_perm ? (int64_t)out_perm[gs] : s;
+  y[prob * P.M + o] = out;
+}
+
+// Adjoint spreading of one tile: 4 warps, each with a private shared-memory
+// copy of the (T+S-1)^2 region and of the 2 x 2p line segments; one point per
+// warp at a time, lanes over the window cells (no two lanes share a cell).
+// Output: the region (TB), the line segments (TL) and the corner partial sums
+// (TC) of this tile -- each written exactly once.
+#define K2_WARPS 4
+__global__ void __launch_bounds__(32 * K2_WARPS)
+k2_spread(NfP P, const int* __restrict__ tile_start, const int* __restrict__ base_x, const int* __restrict__ base_y,
+          const double* __restrict__ wx_all, const double* __restrict__ wy_all, const cplx* __restrict__ recx_all,
+          const cplx* __restrict__ recy_all, const cplx* __restrict__ yin, const int* __restrict__ in_perm,
+          cplx* __restrict__ TB, cplx* __restrict__ TL, cplx* __restrict__ TC) {
+  extern __shared__ cplx sm[];
+  const int tile = blockIdx.x, prob = blockIdx.y;
+  const int ntiles = P.nt * P.nt;
+  const int ty = tile / P.nt, tx = tile - ty * P.nt;
+  const int R = P.R, S = P.S, p = P.p, twop = 2 * p;
+  const int nreg = R * R;
+  const int nlin = P.edges ? 2 * twop * R : 0;
+  const int per_warp = nreg + nlin;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < per_warp * K2_WARPS; i += blockDim.x) sm[i] = mk(0, 0);
+  __syncthreads();
+  cplx* reg = sm + warp * per_warp;
+  cplx* lin = reg + nreg;  // [2][2p][R]: y-lines then x-lines
+  const int Rr = 1 + (P.edges ? twop : 0);
+  const int ncorner = P.edges ? 4 * p * p : 0;
+  cplx cacc[8];
+  for (int u = 0; u < 8; ++u) cacc[u] = mk(0, 0);
+  const int* ts = tile_start + (int64_t)prob * (ntiles + 1);
+  const int s0 = ts[tile], s1 = ts[tile + 1];
+  const cplx* yp = yin + (int64_t)prob * P.M;
+  for (int s = s0 + warp; s < s1; s += K2_WARPS) {
+    const int64_t gs = prob * P.M + s;
+    const int oy = base_y[gs] - ty * P.T, ox = base_x[gs] - tx * P.T;
+    const double wyl = lane < S ? wy_all[gs * S + lane] : 0.0;
+    const double wxl = lane < S ? wx_all[gs * S + lane] : 0.0;
+    const cplx ys = ldg2(yp + (in_perm ? (int64_t)in_perm[gs] : s));
+    const cplx* rx = recx_all + gs * Rr;
+    const cplx* ry = recy_all + gs * Rr;
+    const cplx Dx = ldg2(rx), Dy = ldg2(ry);
+    const cplx v2 = cmul(conj_(cmul(Dx, Dy)), ys);  // freq2wave.cpp:335
+    for (int base = 0; base < S * S; base += 32) {
+      const int idx = base + lane;
+      const int t0 = idx / S, t1 = idx - t0 * S;
+      const double w0 = __shfl_sync(0xffffffffu, wyl, t0 < S ? t0 : 0);
+      const double w1 = __shfl_sync(0xffffffffu, wxl, t1);
+      if (idx < S * S) {
+        cplx* cell = reg + (oy + t0) * R + (ox + t1);
+        const cplx v0 = cscale(v2, w0);  // v0 = w0[t0] * y (nufft.cpp:328)
+        *cell = caxpy(*cell, w1, v0);
+      }
+    }
+    if (P.edges) {
+      for (int base = 0; base < twop * S; base += 32) {
+        const int idx = base + lane;
+        const int e = idx / S, t = idx - e * S;
+        const double wyt = __shfl_sync(0xffffffffu, wyl, t);
+        const double wxt = __shfl_sync(0xffffffffu, wxl, t);
+        if (idx < twop * S) {
+          // side_x_edge: v = conj(Ax(m,e) Dy) y along y; side_y_edge: conj(By(m,e) Dx) y along x
+          const cplx vy = cmul(conj_(cmul(ldg2(rx + 1 + e), Dy)), ys);
+          const cplx vx = cmul(conj_(cmul(ldg2(ry + 1 + e), Dx)), ys);
+          cplx* ly = lin + e * R + oy + t;
+          cplx* lx = lin + (twop + e) * R + ox + t;
+          *ly = caxpy(*ly, wyt, vy);
+          *lx = caxpy(*lx, wxt, vx);
+        }
+      }
+      // corners: Z(row0+i, col0+j) += conj(Ax(m,i)) (y conj(By(m,j)))  (freq2wave.cpp:349-353)
+      for (int u = 0; u < 8; ++u) {
+        const int q = lane + 32 * u;
+        if (q < ncorner) {
+          const int k = q / (p * p), rem = q - k * p * p, i = rem / p, j = rem - i * p;
+          const int ax = (k < 2) ? 1 : 1 + p, byo = (k % 2 == 0) ? 1 : 1 + p;
+          cacc[u] = cadd(cacc[u], cmul(conj_(ldg2(rx + ax + i)), cmul(ys, conj_(ldg2(ry + byo + j)))));
+        }
+      }
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  // fold the warp copies and write the tile's region / lines once
+  cplx* tb = TB + ((int64_t)prob * ntiles + tile) * nreg;
+  for (int i = threadIdx.x; i < nreg; i += blockDim.x) {
+    cplx a = sm[i];
+    for (int w = 1; w < K2_WARPS; ++w) a = cadd(a, sm[w * per_warp + i]);
+    tb[i] = a;
+  }
+  if (P.edges) {
+    cplx* tl = TL + ((int64_t)prob * ntiles + tile) * nlin;
+    for (int i = threadIdx.x; i < nlin; i += blockDim.x) {
+      cplx a = sm[nreg + i];
+      for (int w = 1; w < K2_WARPS; ++w) a = cadd(a, sm[w * per_warp + nreg + i]);
+      tl[i] = a;
+    }
+    __syncthreads();
+    // corner partials: reuse the region smem of warp 0 as [K2_WARPS][ncorner]
+    for (int u = 0; u < 8; ++u) {
+      const int q = lane + 32 * u;
+      if (q < ncorner) sm[warp * ncorner + q] = cacc[u];
+    }
+    __syncthreads();
+    cplx* tc = TC + ((int64_t)prob * ntiles + tile) * ncorner;
+    for (int q = threadIdx.x; q < ncorner; q += blockDim.x) {
+      cplx a = sm[q];
+      for (int w = 1; w < K2_WARPS; ++w) a = cadd(a, sm[w * ncorner + q]);
+      tc[q] = a;
+    }
+  }
+}
+
+// Sum of the tile-region entries that land on global cell r along one axis:
+// (tile, local) pairs with local = r%T + d*T < R (2D adjoint).
+__device__ __forceinline__ cplx gather_cell(const NfP& P, const cplx* __restrict__ TBp, int r, int c) {
+  cplx a = mk(0, 0);
+  const int T = P.T, R = P.R, nt = P.nt;
+  for (int dy = 0; dy * T + (r % T) < R; ++dy) {
+    const int ty = ((r / T - dy) % nt + nt) % nt, ly = (r % T) + dy * T;
+    for (int dx = 0; dx * T + (c % T) < R; ++dx) {
+      const int tx = ((c / T - dx) % nt + nt) % nt, lx = (c % T) + dx * T;
+      a = cadd(a, ldg2(TBp + ((int64_t)(ty * nt + tx) * R + ly) * R + lx));
+    }
+  }
+  return a;
+}
+
+// gather tile regions -> FFT_{+} along y for CW columns -> G (rows that the
+// crop keeps only)
+__global__ void k2_cols_ifft_gather(NfP P, const cplx* __restrict__ TB, cplx* __restrict__ G,
+                                    const cplx* __restrict__ tw, int logLmax) {
+  extern __shared__ cplx sm[];
+  const int c0 = blockIdx.x * P.CW, prob = blockIdx.y;
+  const int ls = P.n_ov + 1;
+  const int ntiles = P.nt * P.nt;
+  const cplx* TBp = TB + (int64_t)prob * ntiles * P.R * P.R;
+  for (int t = threadIdx.x; t < P.n_ov * P.CW; t += blockDim.x) {
+    const int r = t / P.CW, cc = t - r * P.CW;
+    sm[cc * ls + bitrev(r, P.log_nov)] = gather_cell(P, TBp, r, c0 + cc);
+  }
+  __syncthreads();
+  block_fft_bitrev(sm, P.log_nov, P.CW, ls, tw, logLmax, +1);
+  cplx* g = G + (int64_t)prob * P.n_ov * P.n_ov;
+  for (int t = threadIdx.x; t < P.n * P.CW; t += blockDim.x) {
+    const int jj = t / P.CW, cc = t - jj * P.CW;
+    const int r = (jj - P.n / 2 + P.n_ov) & (P.n_ov - 1);
+    g[(int64_t)r * P.n_ov + c0 + cc] = sm[cc * ls + r];
+  }
+}
+
+// FFT_{+} along x of the kept rows, crop, deconvolve -> interior block of Z;
+// every edge entry of Z is zeroed here (filled by k2_edges).
+__global__ void k2_rows_ifft_crop(NfP P, const cplx* __restrict__ G, const double* __restrict__ deconv,
+                                  cplx* __restrict__ z, const cplx* __restrict__ tw, int logLmax) {
+  extern __shared__ cplx sm[];
+  const int j = blockIdx.x, prob = blockIdx.y;
+  cplx* zr = z + (int64_t)prob * P.n * P.n + (int64_t)j * P.n;
+  if (P.edges && (j < P.p || j >= P.n - P.p)) {
+    for (int i = threadIdx.x; i < P.n; i += blockDim.x) zr[i] = mk(0, 0);
+    return;
+  }
+  const int r = (j - P.n / 2 + P.n_ov) & (P.n_ov - 1);
+  const cplx* grow = G + ((int64_t)prob * P.n_ov + r) * P.n_ov;
+  for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) sm[bitrev(i, P.log_nov)] = grow[i];
+  __syncthreads();
+  block_fft_bitrev(sm, P.log_nov, 1, 0, tw, logLmax, +1);
+  const double d0 = deconv[j];
+  for (int i = threadIdx.x; i < P.n; i += blockDim.x) {
+    cplx v = cscale(sm[(i - P.n / 2 + P.n_ov) & (P.n_ov - 1)], d0 * deconv[i]);
+    if (P.edges && (i < P.p || i >= P.n - P.p)) v = mk(0, 0);
+    zr[i] = v;
+  }
+}
+
+// Side lines (gather of the tile line segments, FFT_{+}, crop, deconvolve,
+// add into the edge rows / columns of Z, freq2wave.cpp:359-385) and, in the
+// extra block per problem, the corner sums (freq2wave.cpp:349-357).
+__global__ void k2_edges(NfP P, const cplx* __restrict__ TL, const cplx* __restrict__ TC,
+                         const double* __restrict__ deconv, cplx* __restrict__ z, const cplx* __restrict__ tw,
+                         int logLmax) {
+  extern __shared__ cplx sm[];
+  const int L = blockIdx.x, prob = blockIdx.y;
+  const int p = P.p, twop = 2 * p, n = P.n, T = P.T, R = P.R, nt = P.nt;
+  const int ntiles = nt * nt;
+  const int nlin = 2 * twop * R;
+  cplx* Z = z + (int64_t)prob * n * n;
+  if (L == 2 * twop) {  // corners
+    const int ncorner = 4 * p * p;
+    const cplx* tc = TC + (int64_t)prob * ntiles * ncorner;
+    for (int q = threadIdx.x; q < ncorner; q += blockDim.x) {
+      cplx a = mk(0, 0);
+      for (int t = 0; t < ntiles; ++t) a = cadd(a, tc[(int64_t)t * ncorner + q]);
+      const int k = q / (p * p), rem = q - k * p * p, i = rem / p, j = rem - i * p;
+      const int row0 = (k < 2) ? 0 : n - p, col0 = (k % 2 == 0) ? 0 : n - p;
+      Z[(int64_t)(col0 + j) * n + row0 + i] = a;
+    }
+    return;
+  }
+  const bool yline = L < twop;
+  const int e = yline ? L : L - twop;
+  const cplx* TLp = TL + (int64_t)prob * ntiles * nlin;
+  for (int pos = threadIdx.x; pos < P.n_ov; pos += blockDim.x) {
+    cplx a = mk(0, 0);
+    for (int d = 0; d * T + (pos % T) < R; ++d) {
+      const int tk = ((pos / T - d) % nt + nt) % nt, l = (pos % T) + d * T;
+      for (int o = 0; o < nt; ++o) {
+        const int tile = yline ? tk * nt + o : o * nt + tk;
+        a = cadd(a, TLp[(int64_t)tile * nlin + (yline ? 0 : twop * R) + e * R + l]);
+      }
+    }
+    sm[bitrev(pos, P.log_nov)] = a;
+  }
+  __syncthreads();
+  block_fft_bitrev(sm, P.log_nov, 1, 0, tw, logLmax, +1);
+  const int fixed = edge_index(e, n, p);
+  for (int v = p + threadIdx.x; v < n - p; v += blockDim.x) {
+    cplx val = cscale(sm[(v - n / 2 + P.n_ov) & (P.n_ov - 1)], deconv[v]);
+    if (yline) Z[(int64_t)v * n + fixed] = val;  // Z(i_e, j)
+    else Z[(int64_t)fixed * n + v] = val;        // Z(i, j_e)
+  }
+}

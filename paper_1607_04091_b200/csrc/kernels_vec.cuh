@@ -1,0 +1,190 @@
+// kernels_vec.cuh -- CGLS vector algebra kept on the device (solver.cpp:19-91):
+// per-problem norms (deterministic block reductions), the alpha / beta scalar
+// steps, and the fused axpys.  Every kernel is batched over independent
+// problems and honours the per-problem `active` flag, so converged problems
+// freeze while the rest of the batch keeps iterating with no host round trip.
+#pragma once
+#include "gs_common.cuh"
+
+struct CgState {
+  double ref;      // ||T* b||
+  double gamma;    // ||s||^2 of the current residual
+  double gamma_new;
+  double qq;
+  double alpha, beta;
+  int active;      // 1 while iterating
+  int iterations;
+  int converged;
+  int hist_len;
+};
+
+// out[prob] = sum |v|^2 over len entries (one block per problem; fixed order)
+__global__ void k_norm2(const cplx* __restrict__ v, int64_t len, double* __restrict__ out) {
+  __shared__ double red[32];
+  const int prob = blockIdx.x;
+  v += prob * len;
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
+    cplx a = v[i];
+    acc = fma(a.x, a.x, fma(a.y, a.y, acc));
+  }
+  double s = block_sum(acc, red);
+  if (threadIdx.x == 0) out[prob] = s;
+}
+
+// two-level variant for long vectors: partial sums per (prob, chunk)
+__global__ void k_norm2_part(const cplx* __restrict__ v, int64_t len, int chunks, double* __restrict__ part) {
+  __shared__ double red[32];
+  const int prob = blockIdx.y, ch = blockIdx.x;
+  const int64_t per = (len + chunks - 1) / chunks;
+  const int64_t lo = ch * per, hi = min(len, lo + per);
+  v += prob * len;
+  double acc = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    cplx a = v[i];
+    acc = fma(a.x, a.x, fma(a.y, a.y, acc));
+  }
+  double s = block_sum(acc, red);
+  if (threadIdx.x == 0) part[(int64_t)prob * chunks + ch] = s;
+}
+__global__ void k_norm2_fold(const double* __restrict__ part, int chunks, int B, double* __restrict__ out) {
+  const int prob = blockIdx.x * blockDim.x + threadIdx.x;
+  if (prob >= B) return;
+  double a = 0.0;  // sequential fold keeps the order fixed
+  for (int c = 0; c < chunks; ++c) a += part[(int64_t)prob * chunks + c];
+  out[prob] = a;
+}
+
+// b_s[prob][s] = sqrtw_s * b_raw[prob][perm[s]]  (solver.cpp:30-33, sorted order)
+__global__ void k_gather_scale(const cplx* __restrict__ b, const int* __restrict__ perm, const double* __restrict__ sw,
+                               int64_t M, int B, cplx* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= M * B) return;
+  const int64_t prob = i / M;
+  const int64_t src = perm ? prob * M + perm[i] : i;
+  cplx v = b[src];
+  if (sw) v = cscale(v, sw[i]);
+  out[i] = v;
+}
+
+// r = b - tx
+__global__ void k_sub(const cplx* __restrict__ b, const cplx* __restrict__ tx, int64_t n, cplx* __restrict__ r) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) r[i] = csub(b[i], tx[i]);
+}
+
+// preamble: ref = sqrt(n2[0]); state init   (solver.cpp:42-48)
+__global__ void k_cg_ref(CgState* st, const double* __restrict__ n2, int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  CgState s;
+  s.ref = sqrt(n2[b]);
+  s.gamma = s.gamma_new = s.qq = s.alpha = s.beta = 0.0;
+  s.iterations = 0;
+  s.converged = 0;
+  s.hist_len = 0;
+  s.active = 1;
+  if (s.ref == 0.0) {  // zero data -> zero solution, converged, history {0}
+    s.active = 0;
+    s.converged = 1;
+    s.hist_len = 1;
+  }
+  st[b] = s;
+}
+
+// gamma = ||s||^2; history[0]; tolerance test  (solver.cpp:55-62)
+__global__ void k_cg_gamma0(CgState* st, const double* __restrict__ n2, double tol, double* hist, int hist_stride, int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  CgState s = st[b];
+  if (!s.active) {
+    if (s.ref == 0.0 && hist) hist[(int64_t)b * hist_stride] = 0.0;
+    return;
+  }
+  s.gamma = n2[b];
+  double h = sqrt(s.gamma) / s.ref;
+  if (hist) hist[(int64_t)b * hist_stride] = h;
+  s.hist_len = 1;
+  if (h <= tol) {
+    s.converged = 1;
+    s.active = 0;
+  }
+  st[b] = s;
+}
+
+// qq = ||q||^2; break on qq == 0; alpha = gamma / qq  (solver.cpp:71-74)
+__global__ void k_cg_alpha(CgState* st, const double* __restrict__ n2, int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  CgState s = st[b];
+  if (!s.active) return;
+  s.qq = n2[b];
+  if (s.qq == 0.0) {
+    s.active = 0;  // search direction in the numerical null space
+    s.alpha = 0.0;
+  } else {
+    s.alpha = s.gamma / s.qq;
+  }
+  st[b] = s;
+}
+
+// gamma' = ||s||^2; history; tolerance; beta  (solver.cpp:77-87)
+__global__ void k_cg_beta(CgState* st, const double* __restrict__ n2, double tol, int it, double* hist, int hist_stride,
+                          int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  CgState s = st[b];
+  if (!s.active) return;
+  double gn = n2[b];
+  s.iterations = it;
+  double h = sqrt(gn) / s.ref;
+  if (hist) hist[(int64_t)b * hist_stride + it] = h;
+  s.hist_len = it + 1;
+  if (h <= tol) {
+    s.converged = 1;
+    s.active = 0;
+    s.beta = 0.0;
+  } else {
+    s.beta = gn / s.gamma;
+    s.gamma = gn;
+  }
+  st[b] = s;
+}
+
+// v += alpha w   (x += alpha p,  solver.cpp:75)  -- only while the problem is active
+// and its alpha was set this iteration (flag snapshot taken before k_cg_alpha)
+__global__ void k_axpy_alpha(cplx* __restrict__ v, const cplx* __restrict__ w, int64_t len, int B, const CgState* st,
+                             double sign) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= len * B) return;
+  const CgState& s = st[i / len];
+  if (!s.active) return;
+  const double a = sign * s.alpha;
+  cplx a0 = v[i], b0 = w[i];
+  v[i] = mk(fma(a, b0.x, a0.x), fma(a, b0.y, a0.y));
+}
+
+// p = s + beta p  (solver.cpp:87)
+__global__ void k_pupdate(cplx* __restrict__ p, const cplx* __restrict__ s, int64_t len, int B, const CgState* st) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= len * B) return;
+  const CgState& c = st[i / len];
+  if (!c.active) return;
+  cplx pv = p[i], sv = s[i];
+  p[i] = mk(fma(c.beta, pv.x, sv.x), fma(c.beta, pv.y, sv.y));
+}
+
+// any problem still active?  (host polls this every chunk of iterations)
+__global__ void k_any_active(const CgState* st, int B, int* flag) {
+  int a = 0;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) a |= st[b].active;
+  a = __syncthreads_or(a);
+  if (threadIdx.x == 0) *flag = a;
+}
+
+// zero the solution of zero-data problems (ref == 0): x = 0 (solver.cpp:43-47)
+__global__ void k_zero_if_ref0(cplx* __restrict__ x, int64_t len, int B, const CgState* st) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= len * B) return;
+  if (st[i / len].ref == 0.0) x[i] = mk(0, 0);
+}
