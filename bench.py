@@ -1,0 +1,515 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 T / T* / CGLS hot path (BASELINE.json metric:
+"T.x+T*.y pairs/sec and CGLS iters/sec; % of HBM/FP64 roofline at 1/2/4/8 GPU").
+
+Default workload = C5 (BASELINE.json configs[4]): 256 independent 2D
+non-uniform problems, each 2^18 jittered-grid samples (spacing 0.5 on
+[-128,128)^2, U(-0.2,0.2) jitter, seed 20160613+b), db4 at J=8 (256x256
+coefficients), Voronoi density weights, complex128 coefficients and noise
+sigma=1e-3.  It is the configuration the metric's 1/2/4/8-GPU scaling is
+quoted on and the largest that fits one GPU.  Problems shard across ranks
+(no data-path collective; total work fixed -> "strong" scaling).
+
+A step = one CGLS iteration (solver.cpp:70-88: one T, one T*, the norms and
+axpys) over every problem of the rank.  `value` = problem-iterations/s over
+all ranks, device-timed with CUDA events (max over ranks).  Inputs (per-point
+factor tables, 35 GB at N=1) exceed L2, so no flush is needed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c1..c5]
+  python bench.py --impl reference ...   # CPU restatement of the reference
+                                          # on the host cores (oracle/)
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SEED = 20160613
+WORKLOADS = {
+    # name: (dim, family p, J, builder, iterations in the config, noise sigma, description)
+    "c1": "1D uniform: M=1024 integer frequencies -512..511, Haar J=9 (N=512), sigma=1e-3",
+    "c2": "1D jittered: M=4096 (spacing 0.5, U(-0.2,0.2)), Voronoi weights, db4 J=10 (N=1024), sigma=1e-3",
+    "c3": "2D uniform tensor: 512x512 integer grid on [-256,256)^2, db2 J=8 (N=256^2), sigma=1e-4",
+    "c4": "2D spiral: 2^20 samples, R=512, 64 turns, Voronoi weights, db4 J=9 (N=512^2), sigma=1e-4",
+    "c5": "Batched 2D jittered: 256 problems x 2^18 samples (spacing 0.5 on [-128,128)^2, U(-0.2,0.2)), "
+          "Voronoi weights, db4 J=8 (N=256^2), sigma=1e-3",
+}
+
+
+# ------------------------------------------------------------------ inputs
+def problem_inputs(workload, b, gen):
+    """(dim, p, J, coords, weights, bandwidth, sigma) of problem b, via a generator
+    module exposing gen_grid / gen_jitter / gen_spiral / voronoi."""
+    if workload == "c1":
+        return 1, 1, 9, gen.gen_grid(1024, 1.0), None, 512.0, 1e-3
+    if workload == "c2":
+        c = gen.gen_jitter(4096, 0.5, 0.2, SEED + b)
+        K = float(np.max(np.abs(c)))
+        return 1, 4, 10, c, gen.voronoi(1, c, K), K, 1e-3
+    if workload == "c3":
+        return 2, 2, 8, gen.gen_grid(512, 1.0, 2), None, 256.0, 1e-4
+    if workload == "c4":
+        c = gen.gen_spiral(64, 16384.0, 512.0)
+        return 2, 4, 9, c, gen.voronoi(2, c, 512.0), 512.0, 1e-4
+    if workload == "c5":
+        c = gen.gen_jitter(512, 0.5, 0.2, SEED + b, 2)
+        K = float(np.max(np.abs(c)))
+        return 2, 4, 8, c, gen.voronoi(2, c, K), K, 1e-3
+    raise SystemExit(f"unknown workload {workload}")
+
+
+def problem_count(workload):
+    return 256 if workload == "c5" else 1
+
+
+def coeffs_and_noise(b, ncols, nrows, sigma):
+    rng = np.random.default_rng(SEED + 7919 * b)
+    x = (rng.standard_normal(ncols) + 1j * rng.standard_normal(ncols)) / math.sqrt(2.0)
+    noise = sigma * (rng.standard_normal(nrows) + 1j * rng.standard_normal(nrows)) / math.sqrt(2.0)
+    return x, noise
+
+
+class ProductGen:
+    """Input harness of the product package (csrc/host_inputs.cpp)."""
+
+    def __init__(self):
+        from paper_1607_04091_b200 import inputs
+        self.i = inputs
+
+    def gen_grid(self, M, eps, dim=1):
+        return self.i.gen_grid(M, eps, dim)
+
+    def gen_jitter(self, M, eps, eta, seed, dim=1):
+        return self.i.gen_jitter(M, eps, eta, seed, dim)
+
+    def gen_spiral(self, t, ppt, K):
+        return self.i.gen_spiral(t, ppt, K)
+
+    def voronoi(self, dim, c, K):
+        return self.i.voronoi_weights(dim, c, K)
+
+
+# ------------------------------------------------------------------ roofline bookkeeping
+def algorithmic_bytes(kernel, dim, p, M, Nc):
+    """Compulsory HBM bytes of one launch per problem (SURVEY 8(d) accounting:
+    coordinates 8*dim, D 16*dim, L/R 32*p*dim per sample; x / y 16 B per entry)."""
+    per_pt = 8 * dim + 16 * dim + (32 * p * dim if p >= 2 else 0)
+    if kernel in ("k2_interp", "k_n1_interp"):
+        return M * (per_pt + 16) + 16 * Nc
+    if kernel in ("k2_spread", "k_n1_spread"):
+        return M * (per_pt + 16)
+    return None
+
+
+def iteration_bytes(dim, p, M, Nc, uniform_axis=None):
+    """bytes per CGLS iteration = pair + 16 (6 Nc + 3 M)."""
+    if uniform_axis is not None:
+        pair = 2 * (16 * Nc + 16 * M) + 2 * 16 * dim * uniform_axis * (1 + (2 * p if p >= 2 else 0))
+    else:
+        pair = 2 * (16 * Nc + 16 * M + 8 * dim * M + 16 * dim * M + (32 * p * dim * M if p >= 2 else 0))
+    return pair, pair + 16 * (6 * Nc + 3 * M)
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic(kernel, workload):
+    """dram bytes per launch per problem from the committed ncu capture, if any."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(workload, {}).get(kernel)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = os.path.join("/tmp", f"gs_clocks_{os.getpid()}_{device}.csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.device)], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [s.strip() for s in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ distributed plumbing
+def dist_init(n):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        import torch
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allreduce_max(v, world, device):
+    if world <= 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_gpu(args):
+    import torch
+    import paper_1607_04091_b200 as gs
+
+    rank, world, local = dist_init(args.gpus)
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    gen = ProductGen()
+    P = args.problems or problem_count(args.workload)
+    lo, hi = rank * P // world, (rank + 1) * P // world
+    mine = list(range(lo, hi))
+    B = len(mine)
+    t0 = time.time()
+    inp = [problem_inputs(args.workload, b, gen) for b in mine]
+    dim, p, J = inp[0][0], inp[0][1], inp[0][2]
+    sigma_noise = inp[0][6]
+    bw = max(x[5] for x in inp)
+    sets = [gs.SamplingSet(dim, x[3]) for x in inp]
+    weighted = inp[0][4] is not None
+    mu = np.concatenate([x[4] for x in inp]) if weighted else None
+    # data w = T_unweighted x_true + noise; the unweighted operator
+    # is built, applied and released before the weighted one is built
+    op_u = gs.freq2wave(sets, p, J, bandwidth=bw, device=local)
+    M, Nc = op_u.rows(), op_u.cols()
+    xs, ns = zip(*[coeffs_and_noise(b, Nc, M, sigma_noise) for b in mine])
+    x_true = torch.from_numpy(np.concatenate(xs)).to(dev)
+    data = gs.apply_forward(op_u, x_true) + torch.from_numpy(np.concatenate(ns)).to(dev)
+    op_u.close()
+    del op_u
+    torch.cuda.synchronize()
+    op = gs.freq2wave(sets, p, J, bandwidth=bw, weights=mu, device=local)
+    route = op.route
+    build_s = time.time() - t0
+    stream = torch.cuda.current_stream(dev)
+    L = gs.load_library()
+    import ctypes as C
+    L.gs_launch_count.restype = C.c_longlong
+
+    # -------- value: device-timed CGLS iterations over the resident batch
+    sess = gs.CglsSession(op, data, tolerance=1e-300, history_capacity=args.warmup + args.steps + 2, stream=stream)
+    sess.step(args.warmup, stream=stream)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier(world)
+    torch.cuda.synchronize()
+    n0 = L.gs_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    sess.step(args.steps, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    launches = L.gs_launch_count() - n0
+    clk = clocks.stop()
+    ms = allreduce_max(e0.elapsed_time(e1), world, dev)
+    _, st = sess.result()
+    sess.close()
+    ms_per_step = ms / args.steps
+    value = P * args.steps / (ms / 1e3)
+
+    # -------- pairs/s through the public API on resident device tensors
+    xp = torch.randn(B * Nc, dtype=torch.complex128, device=dev)
+    yp = torch.randn(B * M, dtype=torch.complex128, device=dev)
+    for _ in range(2):
+        gs.apply_adjoint(op, gs.apply_forward(op, xp, stream=stream), stream=stream)
+    torch.cuda.synchronize()
+    npairs = max(2, min(args.steps, 10))
+    e0.record(stream)
+    for _ in range(npairs):
+        gs.apply_forward(op, xp, stream=stream)
+        gs.apply_adjoint(op, yp, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    pair_ms = allreduce_max(e0.elapsed_time(e1), world, dev) / npairs
+    pairs_per_sec = P / (pair_ms / 1e3)
+
+    # -------- per-kernel device times of one pair -> dominant kernel roofline
+    prof = gs_profile(op, stream)
+    peak, peak_kind = load_peaks()
+    dom = max((k for k in prof if algorithmic_bytes(k, dim, p, M, Nc) is not None), key=lambda k: prof[k],
+              default=None)
+    roofline = None
+    if dom is not None:
+        ab = algorithmic_bytes(dom, dim, p, M, Nc) * B
+        ach = ab / (prof[dom] / 1e3) / 1e9
+        tr = load_traffic(dom, args.workload)
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 2), "peak": peak, "unit": "GB/s",
+                    "frac": round(ach / peak, 4), "traffic": (tr * B if tr is not None else None),
+                    "algorithmic_bytes_per_launch": ab, "launch_ms": round(prof[dom], 4),
+                    "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"}
+    uaxis = {"c1": 1024, "c3": 512}.get(args.workload)
+    pair_b, it_b = iteration_bytes(dim, p, M, Nc, uaxis)
+    it_gbs = it_b * P / (ms_per_step / 1e3) / 1e9
+    roof_iter = {"bytes_per_problem_iteration": it_b, "achieved_gbs": round(it_gbs, 2),
+                 "frac": round(it_gbs / peak, 4)}
+
+    # -------- e2e: public API from pinned host buffers (H2D of b, D2H of x inside)
+    b_host = data.cpu().pin_memory()
+    x_host = torch.empty(B * Nc, dtype=torch.complex128).pin_memory()
+    barrier(world)
+    t_e = time.perf_counter()
+    xr, stats = gs_solve_host(op, b_host, x_host, args.steps)
+    t_e = time.perf_counter() - t_e
+    t_e = allreduce_max(t_e, world, dev)
+    e2e_value = P * args.steps / t_e
+    h2d = int(b_host.numel() * 16)
+    d2h = int(x_host.numel() * 16)
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(args.workload)
+        out = {
+            "metric": "CGLS iterations/sec (problem-iterations; T.x + T*.y pairs/sec alongside)",
+            "value": round(value, 3), "unit": "problem-iterations/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64)",
+            "data": "synthetic: reference pattern generators (patterns.cpp) + seeded complex-normal coefficients",
+            "config": {"workload": args.workload.upper(), "description": WORKLOADS[args.workload],
+                       "problems": P, "problems_per_rank": B, "samples_per_problem": M, "coeffs_per_problem": Nc,
+                       "family": f"p={p}", "J": J, "route": route, "cgls_tolerance": "1e-300 (fixed count)",
+                       "l2": "inputs larger than L2 (per-point tables %.1f GB/GPU)" % (op.device_bytes / 1e9)
+                       if op.device_bytes > 126e6 else "L2-resident working set; back-to-back steps",
+                       "parallelism": f"problem-sharded x{world}" if world > 1 else "1 GPU"},
+            "pairs_per_sec": round(pairs_per_sec, 3), "ms_per_pair": round(pair_ms, 4),
+            "gpu_launches": int(launches),
+            "roofline": roofline, "roofline_iteration": roof_iter,
+            "kernel_ms_per_pair": {k: round(v, 4) for k, v in prof.items()},
+            "e2e": {"value": round(e2e_value, 3), "unit": "problem-iterations/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "steps_per_call": args.steps,
+                    "note": "one gs_solve_least_squares call (preamble + steps) from pinned host memory"},
+            "clocks": clk, "cpu_baseline": cpu, "build_seconds": round(build_s, 1),
+            "final_residual_problem0": st[0].residual,
+        }
+        print(json.dumps(out), flush=True)
+    op.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return out
+
+
+def gs_profile(op, stream):
+    import ctypes as C
+    import paper_1607_04091_b200 as gs
+    L = gs.load_library()
+    L.gs_profile_pair.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_double), C.c_char_p,
+                                  C.POINTER(C.c_int)]
+    ms = (C.c_double * 32)()
+    names = C.create_string_buffer(32 * 32)
+    cnt = C.c_int()
+    rc = L.gs_profile_pair(op.handle, 3, C.c_void_p(stream.cuda_stream), 32, ms, names, C.byref(cnt))
+    if rc:
+        return {}
+    out = {}
+    for i in range(cnt.value):
+        nm = names.raw[32 * i:32 * (i + 1)].split(b"\0")[0].decode()
+        out[nm] = out.get(nm, 0.0) + ms[i]
+    return out
+
+
+def gs_solve_host(op, b_host, x_host, iters):
+    import ctypes as C
+    import paper_1607_04091_b200 as gs
+    L = gs.load_library()
+    B = op.batch
+    stats = (gs._Stats * B)()
+    rc = L.gs_solve_least_squares(op.handle, b_host.data_ptr(), b_host.numel(), None, int(iters), 1e-300,
+                                  x_host.data_ptr(), stats, None, None)
+    gs._check(rc)
+    return x_host, stats
+
+
+# ------------------------------------------------------------------ CPU legs (oracle = test infrastructure)
+def _cpu_problem(workload, b):
+    import oracle
+
+    class OracleGen:
+        gen_grid = staticmethod(oracle.gen_grid)
+        gen_jitter = staticmethod(oracle.gen_jitter)
+        gen_spiral = staticmethod(oracle.gen_spiral)
+
+        @staticmethod
+        def voronoi(dim, c, K):
+            if dim == 2 and c.size > 2 * 20000:  # reference O(M^2) clip is infeasible; same weights, fast path
+                from paper_1607_04091_b200 import inputs
+                return inputs.voronoi_weights(dim, c, K)
+            return oracle.voronoi(dim, c, K)
+
+    dim, p, J, c, mu, bw, sig = problem_inputs(workload, b, OracleGen)
+    op_u = oracle.Op(dim, p, J, c, bandwidth=bw)
+    x, nz = coeffs_and_noise(b, op_u.cols, op_u.rows, sig)
+    data = op_u.forward(x) + nz
+    del op_u
+    op = oracle.Op(dim, p, J, c, weights=mu, bandwidth=bw)
+    return op, data
+
+
+def _cpu_iter_seconds(op, data, k):
+    """Seconds per CGLS iteration: (T(solve 1+k) - T(solve 1)) / k (removes the preamble)."""
+    t = time.perf_counter()
+    op.solve(data, max_iterations=1, tolerance=1e-300)
+    t1 = time.perf_counter() - t
+    t = time.perf_counter()
+    op.solve(data, max_iterations=1 + k, tolerance=1e-300)
+    t2 = time.perf_counter() - t
+    return max(1e-9, (t2 - t1) / k), t1, t2
+
+
+def cpu_baseline(workload):
+    """Rank 0, N=1: the oracle (restated reference, single thread like the
+    reference itself) on one problem of the workload."""
+    try:
+        t = time.perf_counter()
+        op, data = _cpu_problem(workload, 0)
+        build = time.perf_counter() - t
+        k = 2 if workload in ("c4", "c5", "c3") else 20
+        per_it, _, _ = _cpu_iter_seconds(op, data, k)
+        return {"value": round(1.0 / per_it, 4), "unit": "problem-iterations/s", "cores": 1, "kind": "port",
+                "sample": f"{workload.upper()} problem 0, {k} CGLS iterations (difference of solves of 1 and "
+                          f"{1 + k} iterations), construction ({build:.1f} s) excluded"}
+    except Exception as e:  # noqa: BLE001
+        return {"value": None, "unit": "problem-iterations/s", "cores": 1, "kind": "port", "sample": f"failed: {e}"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU restatement of the reference path (oracle/) on
+    the host cores, all threads, same workload / metric; rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return None
+    import oracle
+    oracle.lib()
+    ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    P = args.problems or problem_count(args.workload)
+    threads = max(1, min(ncpu, P, 64 if args.workload == "c5" else 1))
+    k = max(1, min(args.steps, 3 if args.workload in ("c4", "c5", "c3") else 20))
+    rates = [0.0] * threads
+    errs = []
+
+    def work(i):
+        try:
+            op, data = _cpu_problem(args.workload, i)
+            per_it, _, _ = _cpu_iter_seconds(op, data, k)
+            rates[i] = 1.0 / per_it
+        except Exception as e:  # noqa: BLE001
+            errs.append(str(e))
+
+    t = time.perf_counter()
+    ths = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    wall = time.perf_counter() - t
+    value = float(sum(rates))
+    out = {"impl": "reference", "metric": "CGLS iterations/sec (problem-iterations; T.x + T*.y pairs/sec alongside)",
+           "value": round(value, 4), "unit": "problem-iterations/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+           "dtype": "c128 (f64)", "data": "synthetic (same generators and seeds as the GPU arm)",
+           "config": {"workload": args.workload.upper(), "description": WORKLOADS[args.workload]},
+           "cpu_baseline": {"value": round(value, 4), "unit": "problem-iterations/s", "cores": threads,
+                            "kind": "port",
+                            "sample": f"{threads} concurrent problems x {k} CGLS iterations each (oracle/gs_oracle.cpp,"
+                                      f" the reference algorithm restated; construction excluded); wall {wall:.0f} s"},
+           "e2e": {"value": round(value, 4), "unit": "problem-iterations/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    if errs:
+        out["errors"] = errs[:3]
+    print(json.dumps(out), flush=True)
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS))
+    ap.add_argument("--problems", type=int, default=0, help="override the problem count (quick runs)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -124,7 +124,25 @@ int gs_cgls_destroy(gs_cgls_session* s);
  * axis 0 = x, 1 = y.  L, R may be NULL (haar). */
 int gs_op_export_factors(gs_op* op, int b, int axis, double* D, double* L, double* R);
 
+/* Per-kernel device time of one T + T* pair (no reference counterpart; the
+ * measurement hook bench.py uses for the roofline): `reps` pairs on zeroed
+ * buffers, CUDA events between consecutive launches on `stream`.  Writes up
+ * to max_kernels average durations (ms) and 32-byte kernel names. */
+int gs_profile_pair(gs_op* op, int reps, void* stream, int max_kernels, double* ms_out,
+                    char* names_out, int* count);
+
+/* Input harness (reference patterns.cpp generators, exact fast Voronoi
+ * weights with weights.cpp semantics); host-only, not on the timed path. */
+int gs_gen_grid(int64_t M, double eps, int dim, double* out);
+int gs_gen_jitter(int64_t M, double eps, double eta, uint64_t seed, int dim, double* out);
+int gs_gen_spiral(int turns, double points_per_turn, double K, double* out);
+int gs_voronoi_weights(int dim, int64_t M, const double* coords, double K, double* mu, int nthreads);
+const char* gs_inputs_last_error(void);
+
 const char* gs_last_error(void);
+
+/* Number of kernels this library has launched so far (process-wide counter). */
+long long gs_launch_count(void);
 
 /* Build / capability probe: returns the sm version the library was compiled
  * for (100 for sm_100a) -- loadable without a GPU. */

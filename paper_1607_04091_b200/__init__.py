@@ -122,6 +122,13 @@ def _check(rc):
         raise _ERRS.get(rc, Error)(msg)
 
 
+def _check_inputs(rc):
+    if rc != 0:
+        L = load_library()
+        L.gs_inputs_last_error.restype = C.c_char_p
+        raise _ERRS.get(rc, Error)(L.gs_inputs_last_error().decode())
+
+
 # ------------------------------------------------------------------ value types
 _FAMILIES = {"haar": 1, "db1": 1, **{f"db{p}": p for p in range(2, 9)}}
 

@@ -5,6 +5,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -227,20 +228,27 @@ namespace {
 
 const int kSmemMax = 227 * 1024;
 
+template <class K>
+void allow_big_smem(K kernel) {
+  cudaFuncAttributes a;
+  CK(cudaFuncGetAttributes(&a, kernel));
+  CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax - (int)a.sharedSizeBytes));
+}
+
 void set_smem_attrs() {
   static bool done = false;
   if (done) return;
-  CK(cudaFuncSetAttribute(k_uni_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
-  CK(cudaFuncSetAttribute(k_uni_adj, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
-  CK(cudaFuncSetAttribute(k_n1_embed_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
-  CK(cudaFuncSetAttribute(k_n1_ifft_crop, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
-  CK(cudaFuncSetAttribute(k2_rows_embed_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
-  CK(cudaFuncSetAttribute(k2_cols_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
-  CK(cudaFuncSetAttribute(k2_lines_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
-  CK(cudaFuncSetAttribute(k2_spread, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
-  CK(cudaFuncSetAttribute(k2_cols_ifft_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
-  CK(cudaFuncSetAttribute(k2_rows_ifft_crop, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
-  CK(cudaFuncSetAttribute(k2_edges, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax));
+  allow_big_smem(k_uni_fwd);
+  allow_big_smem(k_uni_adj);
+  allow_big_smem(k_n1_embed_fft);
+  allow_big_smem(k_n1_ifft_crop);
+  allow_big_smem(k2_rows_embed_fft);
+  allow_big_smem(k2_cols_fft);
+  allow_big_smem(k2_lines_fft);
+  allow_big_smem(k2_spread);
+  allow_big_smem(k2_cols_ifft_gather);
+  allow_big_smem(k2_rows_ifft_crop);
+  allow_big_smem(k2_edges);
   done = true;
 }
 
@@ -573,6 +581,27 @@ gs_op* create(const gs_op_desc* dsc) {
   return op.release();
 }
 
+// ------------------------------------------------------------------ per-kernel timing
+// When armed by gs_profile_pair, every launch in forward_dev / adjoint_dev is
+// followed by an event on the launching stream; consecutive events bracket
+// exactly one kernel.
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;
+  std::vector<std::string> names;
+};
+Prof g_prof;
+std::atomic<long long> g_launches{0};  // kernels this library has launched (gs_launch_count)
+void pmark(const char* name, cudaStream_t st) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (!g_prof.on) return;
+  cudaEvent_t e;
+  CK(cudaEventCreate(&e));
+  CK(cudaEventRecord(e, st));
+  g_prof.ev.push_back(e);
+  g_prof.names.push_back(name);
+}
+
 // ------------------------------------------------------------------ applies
 // x, y are device pointers; perm_io: samples in the caller's order (true) or
 // the internal bin-sorted order (false, used inside CGLS).
@@ -583,6 +612,7 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
       const UniP& P = op->up;
       k_uni_fwd<<<dim3(1, B), 256, uni_smem(P), st>>>(P, x, Strided{op->n, 0, 1}, op->rec_u.p, op->M * op->Rr, y,
                                                      Strided{op->M, 0, 1}, nullptr, 0, op->tw.p, op->logLmax);
+      pmark("k_uni_fwd", st);
       break;
     }
     case GS_ROUTE_TENSOR_2D: {
@@ -591,31 +621,40 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
       k_uni_fwd<<<dim3((unsigned)n, B), 256, uni_smem(op->upx), st>>>(
           op->upx, x, Strided{n * n, n, 1}, op->rec_ax.p, Ma * op->Rr, op->W.p, Strided{Ma * n, 1, n}, nullptr, 0,
           op->tw.p, op->logLmax);
+      pmark("k_uni_fwd[x-pass]", st);
       // Y(a, b) = sum_j ay_b(j) W(a, j): one vector per row a
       k_uni_fwd<<<dim3((unsigned)Ma, B), 256, uni_smem(op->upy), st>>>(
           op->upy, op->W.p, Strided{Ma * n, n, 1}, op->rec_ay.p, Mb * op->Rr, y, Strided{op->M, Mb, 1},
           op->weighted ? op->sqrtw.p : nullptr, op->M, op->tw.p, op->logLmax);
+      pmark("k_uni_fwd[y-pass]", st);
       break;
     }
     case GS_ROUTE_NFFT_1D: {
       const NfP& P = op->np;
       k_n1_embed_fft<<<B, 256, P.n_ov * sizeof(cplx), st>>>(P, x, op->deconv.p, op->G.p, op->tw.p, op->logLmax);
+      pmark("k_n1_embed_fft", st);
       k_n1_interp<<<dim3(nblk(op->M, 128), B), 128, 0, st>>>(P, op->base_x.p, op->wts_x.p, op->rec_x.p, op->G.p, x,
                                                               perm_io ? op->perm.p : nullptr, y);
+      pmark("k_n1_interp", st);
       break;
     }
     case GS_ROUTE_NFFT_2D: {
       const NfP& P = op->np;
       k2_rows_embed_fft<<<dim3(P.n, B), 256, P.n_ov * sizeof(cplx), st>>>(P, x, op->deconv.p, op->G.p, op->tw.p,
                                                                           op->logLmax);
+      pmark("k2_rows_embed_fft", st);
       k2_cols_fft<<<dim3(P.n_ov / P.CW, B), 256, (size_t)P.CW * (P.n_ov + 1) * sizeof(cplx), st>>>(P, op->G.p, op->tw.p,
                                                                                                    op->logLmax);
-      if (P.edges)
+      pmark("k2_cols_fft", st);
+      if (P.edges) {
         k2_lines_fft<<<dim3(4 * P.p, B), 256, P.n_ov * sizeof(cplx), st>>>(P, x, op->deconv.p, op->lines.p, op->tw.p,
                                                                            op->logLmax);
+        pmark("k2_lines_fft", st);
+      }
       k2_interp<<<dim3(nblk(op->M, 128), B), 128, 0, st>>>(P, op->base_x.p, op->base_y.p, op->wts_x.p, op->wts_y.p,
                                                             op->rec_x.p, op->rec_y.p, op->G.p, op->lines.p, x,
                                                             perm_io ? op->perm.p : nullptr, y);
+      pmark("k2_interp", st);
       break;
     }
   }
@@ -629,6 +668,7 @@ void adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
       const UniP& P = op->up;
       k_uni_adj<<<dim3(1, B), 256, uni_smem(P), st>>>(P, y, Strided{op->M, 0, 1}, nullptr, 0, op->rec_u.p,
                                                      op->M * op->Rr, z, Strided{op->n, 0, 1}, op->tw.p, op->logLmax);
+      pmark("k_uni_adj", st);
       break;
     }
     case GS_ROUTE_TENSOR_2D: {
@@ -637,18 +677,22 @@ void adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
       k_uni_adj<<<dim3((unsigned)Ma, B), 256, uni_smem(op->upy), st>>>(
           op->upy, y, Strided{op->M, Mb, 1}, op->weighted ? op->sqrtw.p : nullptr, op->M, op->rec_ay.p, Mb * op->Rr,
           op->W.p, Strided{Ma * n, n, 1}, op->tw.p, op->logLmax);
+      pmark("k_uni_adj[y-pass]", st);
       // X(i, j) = sum_a conj(ax_a(i)) V(a, j): one vector per column j
       k_uni_adj<<<dim3((unsigned)n, B), 256, uni_smem(op->upx), st>>>(
           op->upx, op->W.p, Strided{Ma * n, 1, n}, nullptr, 0, op->rec_ax.p, Ma * op->Rr, z, Strided{n * n, n, 1},
           op->tw.p, op->logLmax);
+      pmark("k_uni_adj[x-pass]", st);
       break;
     }
     case GS_ROUTE_NFFT_1D: {
       const NfP& P = op->np;
       k_n1_spread<<<dim3(nblk(P.n_ov, 128), B), 128, 0, st>>>(P, op->bins.p, op->wts_x.p, op->rec_x.p, y,
                                                                perm_io ? op->perm.p : nullptr, op->G.p);
+      pmark("k_n1_spread", st);
       k_n1_ifft_crop<<<B, 256, P.n_ov * sizeof(cplx), st>>>(P, op->G.p, op->deconv.p, op->rec_x.p, y,
                                                             perm_io ? op->perm.p : nullptr, z, op->tw.p, op->logLmax);
+      pmark("k_n1_ifft_crop", st);
       break;
     }
     case GS_ROUTE_NFFT_2D: {
@@ -658,13 +702,18 @@ void adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
       k2_spread<<<dim3(ntiles, B), 32 * K2_WARPS, per_warp * K2_WARPS * sizeof(cplx), st>>>(
           P, op->bins.p, op->base_x.p, op->base_y.p, op->wts_x.p, op->wts_y.p, op->rec_x.p, op->rec_y.p, y,
           perm_io ? op->perm.p : nullptr, op->TB.p, op->TL.p, op->TC.p);
+      pmark("k2_spread", st);
       k2_cols_ifft_gather<<<dim3(P.n_ov / P.CW, B), 256, (size_t)P.CW * (P.n_ov + 1) * sizeof(cplx), st>>>(
           P, op->TB.p, op->G.p, op->tw.p, op->logLmax);
+      pmark("k2_cols_ifft_gather", st);
       k2_rows_ifft_crop<<<dim3(P.n, B), 256, P.n_ov * sizeof(cplx), st>>>(P, op->G.p, op->deconv.p, z, op->tw.p,
                                                                           op->logLmax);
-      if (P.edges)
+      pmark("k2_rows_ifft_crop", st);
+      if (P.edges) {
         k2_edges<<<dim3(4 * P.p + 1, B), 256, P.n_ov * sizeof(cplx), st>>>(P, op->TL.p, op->TC.p, op->deconv.p, z,
                                                                            op->tw.p, op->logLmax);
+        pmark("k2_edges", st);
+      }
       break;
     }
   }
@@ -713,10 +762,10 @@ struct Session {
 
 void norm2(Session& S, const cplx* v, int64_t len, int chunks, cudaStream_t st) {
   if (chunks <= 1) {
-    k_norm2<<<S.B, 1024, 0, st>>>(v, len, S.n2.p);
+    k_norm2<<<S.B, 1024, 0, st>>>(v, len, S.n2.p); pmark("k_norm2", st);
   } else {
-    k_norm2_part<<<dim3(chunks, S.B), 512, 0, st>>>(v, len, chunks, S.part.p);
-    k_norm2_fold<<<nblk(S.B, 128), 128, 0, st>>>(S.part.p, chunks, S.B, S.n2.p);
+    k_norm2_part<<<dim3(chunks, S.B), 512, 0, st>>>(v, len, chunks, S.part.p); pmark("k_norm2_part", st);
+    k_norm2_fold<<<nblk(S.B, 128), 128, 0, st>>>(S.part.p, chunks, S.B, S.n2.p); pmark("k_norm2_fold", st);
   }
   CKL();
 }
@@ -779,14 +828,19 @@ void session_iterate(Session& S, cudaStream_t st) {
   const int it = ++S.it;
   forward_dev(op, S.p.p, S.q.p, false, st);                          // q = T p
   norm2(S, S.q.p, S.M, S.chunks_M, st);                              // qq
-  k_cg_alpha<<<nblk(S.B, 128), 128, 0, st>>>(S.st.p, S.n2.p, S.B);   // alpha (or stop)
-  k_axpy_alpha<<<nblk(TN, 256), 256, 0, st>>>(S.x.p, S.p.p, S.Nc, S.B, S.st.p, 1.0);   // x += alpha p
-  k_axpy_alpha<<<nblk(TM, 256), 256, 0, st>>>(S.r.p, S.q.p, S.M, S.B, S.st.p, -1.0);   // r -= alpha q
+  k_cg_alpha<<<nblk(S.B, 128), 128, 0, st>>>(S.st.p, S.n2.p, S.B);  // alpha (or stop)
+  pmark("k_cg_alpha", st);
+  k_axpy_alpha<<<nblk(TN, 256), 256, 0, st>>>(S.x.p, S.p.p, S.Nc, S.B, S.st.p, 1.0);  // x += alpha p
+  pmark("k_axpy_x", st);
+  k_axpy_alpha<<<nblk(TM, 256), 256, 0, st>>>(S.r.p, S.q.p, S.M, S.B, S.st.p, -1.0);  // r -= alpha q
+  pmark("k_axpy_r", st);
   adjoint_dev(op, S.r.p, S.s.p, false, st);                          // s = T* r
   norm2(S, S.s.p, S.Nc, S.chunks_N, st);                             // gamma'
   k_cg_beta<<<nblk(S.B, 128), 128, 0, st>>>(S.st.p, S.n2.p, S.tol, it < S.hist_cap ? it : S.hist_cap - 1, S.hist.p,
                                             S.hist_cap, S.B);
-  k_pupdate<<<nblk(TN, 256), 256, 0, st>>>(S.p.p, S.s.p, S.Nc, S.B, S.st.p);           // p = s + beta p
+  pmark("k_cg_beta", st);
+  k_pupdate<<<nblk(TN, 256), 256, 0, st>>>(S.p.p, S.s.p, S.Nc, S.B, S.st.p);  // p = s + beta p
+  pmark("k_pupdate", st);
   CKL();
 }
 
@@ -808,6 +862,7 @@ struct gs_cgls_session {
 extern "C" {
 
 const char* gs_last_error(void) { return g_err.c_str(); }
+long long gs_launch_count(void) { return g_launches.load(); }
 int gs_build_arch(void) { return 100; }
 
 int gs_op_create(const gs_op_desc* desc, gs_op** out) {
@@ -995,6 +1050,57 @@ int gs_solve_least_squares(gs_op* op, const double* raw_samples, int64_t samples
   if (rc == 0) rc = gs_cgls_finish(s, x_out, stats, history, stream);
   gs_cgls_destroy(s);
   return rc;
+}
+
+int gs_profile_pair(gs_op* op, int reps, void* stream, int max_kernels, double* ms_out, char* names_out,
+                    int* count) {
+  return guard_call([&] {
+    if (!op || !ms_out || !count || reps <= 0) fail(GS_ERR_USAGE, "bad argument");
+    std::lock_guard<std::mutex> lk(op->mu);
+    CK(cudaSetDevice(op->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    DBuf<cplx> x, y, z;
+    x.alloc(op->Nc * op->B);
+    y.alloc(op->M * op->B);
+    z.alloc(op->Nc * op->B);
+    CK(cudaMemsetAsync(x.p, 0, x.bytes(), st));
+    CK(cudaMemsetAsync(y.p, 0, y.bytes(), st));
+    forward_dev(op, x.p, y.p, false, st);  // warm
+    adjoint_dev(op, y.p, z.p, false, st);
+    CK(cudaStreamSynchronize(st));
+    std::vector<double> acc;
+    std::vector<std::string> names;
+    for (int r = 0; r < reps; ++r) {
+      g_prof = Prof();
+      g_prof.on = true;
+      pmark("start", st);
+      forward_dev(op, x.p, y.p, false, st);
+      adjoint_dev(op, y.p, z.p, false, st);
+      CK(cudaStreamSynchronize(st));
+      g_prof.on = false;
+      const size_t k = g_prof.ev.size() - 1;
+      if (acc.empty()) {
+        acc.assign(k, 0.0);
+        names.assign(g_prof.names.begin() + 1, g_prof.names.end());
+      }
+      for (size_t i = 0; i < k; ++i) {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, g_prof.ev[i], g_prof.ev[i + 1]));
+        acc[i] += ms;
+      }
+      for (auto e : g_prof.ev) cudaEventDestroy(e);
+    }
+    g_prof = Prof();
+    const int k = (int)std::min<size_t>(acc.size(), (size_t)max_kernels);
+    for (int i = 0; i < k; ++i) {
+      ms_out[i] = acc[i] / reps;
+      if (names_out) {
+        std::strncpy(names_out + 32 * i, names[i].c_str(), 31);
+        names_out[32 * i + 31] = 0;
+      }
+    }
+    *count = k;
+  });
 }
 
 int gs_op_export_factors(gs_op* op, int b, int axis, double* D, double* L, double* R) {

@@ -1,0 +1,225 @@
+// host_inputs.cpp -- input harness for the benchmark configs:
+//   * sampling patterns with the reference's exact generators
+//     (patterns.cpp:14-74: std::mt19937_64 + std::uniform_real_distribution,
+//     so the same libstdc++ yields the same doubles);
+//   * exact Voronoi density-compensation weights in O(M log M): the cell of
+//     point m is clipped (the same half-plane clip as weights.cpp:20-38) only
+//     against neighbours in expanding bucket rings, stopping once every
+//     unprocessed point is farther than twice the cell's farthest vertex --
+//     beyond that no bisector can cut the cell, so the polygon equals the
+//     reference's clip against all M points (weights.cpp:59-70).
+// Multi-threaded with std::thread.  Not on the timed path.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <random>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace {
+
+struct P2 {
+  double x, y;
+};
+
+void clip(std::vector<P2>& poly, std::vector<P2>& tmp, P2 mid, P2 a) {  // weights.cpp:20-38
+  tmp.clear();
+  size_t n = poly.size();
+  for (size_t i = 0; i < n; ++i) {
+    const P2& cur = poly[i];
+    const P2& nxt = poly[(i + 1) % n];
+    double dc = a.x * (cur.x - mid.x) + a.y * (cur.y - mid.y);
+    double dn = a.x * (nxt.x - mid.x) + a.y * (nxt.y - mid.y);
+    if (dc <= 0) tmp.push_back(cur);
+    if ((dc < 0 && dn > 0) || (dc > 0 && dn < 0)) {
+      double t = dc / (dc - dn);
+      tmp.push_back({cur.x + t * (nxt.x - cur.x), cur.y + t * (nxt.y - cur.y)});
+    }
+  }
+  poly.swap(tmp);
+}
+
+double area(const std::vector<P2>& poly) {  // weights.cpp:40-49
+  double acc = 0.0;
+  size_t n = poly.size();
+  for (size_t i = 0; i < n; ++i) acc += poly[i].x * poly[(i + 1) % n].y - poly[(i + 1) % n].x * poly[i].y;
+  return 0.5 * std::abs(acc);
+}
+
+thread_local std::string g_in_err;
+
+}  // namespace
+
+extern "C" {
+
+const char* gs_inputs_last_error(void) { return g_in_err.c_str(); }
+
+// patterns.cpp:25-44
+int gs_gen_grid(int64_t M, double eps, int dim, double* out) {
+  if (M < 1 || !(eps > 0) || (dim != 1 && dim != 2)) {
+    g_in_err = "bad grid parameters";
+    return 5;
+  }
+  std::vector<double> axis(M);
+  double half = (double)M / 2.0;
+  for (int64_t m = 0; m < M; ++m) axis[m] = eps * ((double)m - half);
+  if (dim == 1) {
+    std::memcpy(out, axis.data(), M * sizeof(double));
+    return 0;
+  }
+  int64_t k = 0;
+  for (double x : axis)
+    for (double y : axis) {
+      out[k++] = x;
+      out[k++] = y;
+    }
+  return 0;
+}
+
+// patterns.cpp:46-56
+int gs_gen_jitter(int64_t M, double eps, double eta, uint64_t seed, int dim, double* out) {
+  if (!(eta >= 0) || eta >= eps / 2) {
+    g_in_err = "eta must satisfy 0 <= eta < epsilon/2";
+    return 5;
+  }
+  int rc = gs_gen_grid(M, eps, dim, out);
+  if (rc) return rc;
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> shift(-eta, eta);
+  int64_t n = M * (dim == 2 ? M * 2 : 1);
+  for (int64_t i = 0; i < n; ++i) out[i] += shift(rng);
+  if (dim == 1) std::sort(out, out + M);
+  return 0;
+}
+
+// patterns.cpp:58-74
+int gs_gen_spiral(int turns, double ppt, double K, double* out) {
+  if (turns < 1 || !(ppt > 0) || !(K > 0)) {
+    g_in_err = "bad spiral parameters";
+    return 5;
+  }
+  long long count = std::llround(turns * ppt);
+  for (long long i = 0; i < count; ++i) {
+    double t = (double)i / ppt;
+    double radius = K * t / (double)turns;
+    double angle = 2.0 * 3.14159265358979323846 * t;
+    out[2 * i] = radius * std::cos(angle);
+    out[2 * i + 1] = radius * std::sin(angle);
+  }
+  return 0;
+}
+
+// Voronoi cell measures inside [-K, K]^dim (weights.cpp:95-133), exact, fast.
+int gs_voronoi_weights(int dim, int64_t M, const double* coords, double K, double* mu, int nthreads) {
+  if (!(K > 0)) {
+    g_in_err = "K must be positive";
+    return 5;
+  }
+  if (M <= 0) {
+    g_in_err = "empty point set";
+    return 4;
+  }
+  if (dim == 1) {
+    std::vector<int64_t> order(M);
+    for (int64_t i = 0; i < M; ++i) order[i] = i;
+    std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return coords[a] < coords[b]; });
+    for (int64_t i = 1; i < M; ++i)
+      if (coords[order[i]] == coords[order[i - 1]]) {
+        g_in_err = "degenerate input: duplicate sample points";
+        return 5;
+      }
+    if (coords[order[0]] < -K || coords[order[M - 1]] > K) {
+      g_in_err = "point outside the bandwidth region";
+      return 5;
+    }
+    for (int64_t i = 0; i < M; ++i) {
+      double lo = i == 0 ? -K : 0.5 * (coords[order[i - 1]] + coords[order[i]]);
+      double hi = i + 1 == M ? K : 0.5 * (coords[order[i]] + coords[order[i + 1]]);
+      mu[order[i]] = hi - lo;
+    }
+    return 0;
+  }
+  for (int64_t m = 0; m < M; ++m)
+    if (std::abs(coords[2 * m]) > K || std::abs(coords[2 * m + 1]) > K) {
+      g_in_err = "point outside the bandwidth region";
+      return 5;
+    }
+  // bucket grid, ~2 points per bucket on average
+  const int G = std::max(1, (int)std::sqrt((double)M / 2.0));
+  const double h = 2.0 * K / G;
+  auto cell = [&](double v) { return std::min(G - 1, std::max(0, (int)std::floor((v + K) / h))); };
+  std::vector<int64_t> start((size_t)G * G + 1, 0), idx(M);
+  for (int64_t m = 0; m < M; ++m) start[(size_t)cell(coords[2 * m + 1]) * G + cell(coords[2 * m]) + 1]++;
+  for (size_t i = 1; i < start.size(); ++i) start[i] += start[i - 1];
+  {
+    std::vector<int64_t> fill(start.begin(), start.end() - 1);
+    for (int64_t m = 0; m < M; ++m) idx[fill[(size_t)cell(coords[2 * m + 1]) * G + cell(coords[2 * m])]++] = m;
+  }
+  // duplicates (same bucket) -> reference DomainError
+  for (size_t b = 0; b + 1 < start.size(); ++b)
+    for (int64_t i = start[b]; i < start[b + 1]; ++i)
+      for (int64_t j = i + 1; j < start[b + 1]; ++j)
+        if (coords[2 * idx[i]] == coords[2 * idx[j]] && coords[2 * idx[i] + 1] == coords[2 * idx[j] + 1]) {
+          g_in_err = "degenerate input: duplicate sample points";
+          return 5;
+        }
+  if (nthreads <= 0) nthreads = (int)std::max(1u, std::thread::hardware_concurrency());
+  std::atomic<int64_t> next(0);
+  auto worker = [&]() {
+    std::vector<P2> poly, tmp;
+    std::vector<std::pair<double, int64_t>> cand;
+    const int64_t chunk = 256;
+    for (;;) {
+      int64_t lo = next.fetch_add(chunk);
+      if (lo >= M) break;
+      int64_t hi = std::min(M, lo + chunk);
+      for (int64_t m = lo; m < hi; ++m) {
+        const P2 own{coords[2 * m], coords[2 * m + 1]};
+        const int cx = cell(own.x), cy = cell(own.y);
+        poly = {{-K, -K}, {K, -K}, {K, K}, {-K, K}};
+        for (int ring = 0;; ++ring) {
+          cand.clear();
+          for (int gy = cy - ring; gy <= cy + ring; ++gy) {
+            if (gy < 0 || gy >= G) continue;
+            for (int gx = cx - ring; gx <= cx + ring; ++gx) {
+              if (gx < 0 || gx >= G) continue;
+              if (std::max(std::abs(gx - cx), std::abs(gy - cy)) != ring) continue;
+              const size_t b = (size_t)gy * G + gx;
+              for (int64_t i = start[b]; i < start[b + 1]; ++i) {
+                int64_t j = idx[i];
+                if (j == m) continue;
+                double dx = coords[2 * j] - own.x, dy = coords[2 * j + 1] - own.y;
+                cand.push_back({dx * dx + dy * dy, j});
+              }
+            }
+          }
+          std::sort(cand.begin(), cand.end());
+          for (auto& c : cand) {
+            const P2 q{coords[2 * c.second], coords[2 * c.second + 1]};
+            clip(poly, tmp, P2{(own.x + q.x) / 2, (own.y + q.y) / 2}, P2{q.x - own.x, q.y - own.y});
+            if (poly.empty()) break;
+          }
+          if (poly.empty()) break;
+          // every point outside rings <= ring is at least this far from own
+          double dxm = std::min(own.x - (-K + (cx - ring) * h), (-K + (cx + ring + 1) * h) - own.x);
+          double dym = std::min(own.y - (-K + (cy - ring) * h), (-K + (cy + ring + 1) * h) - own.y);
+          double reach = std::min(dxm, dym);
+          bool covers_all = cx - ring <= 0 && cy - ring <= 0 && cx + ring >= G - 1 && cy + ring >= G - 1;
+          double rmax2 = 0.0;
+          for (const P2& v : poly) rmax2 = std::max(rmax2, (v.x - own.x) * (v.x - own.x) + (v.y - own.y) * (v.y - own.y));
+          if (covers_all || 4.0 * rmax2 <= reach * reach) break;
+        }
+        mu[m] = area(poly);
+      }
+    }
+  };
+  std::vector<std::thread> th;
+  for (int t = 0; t < nthreads; ++t) th.emplace_back(worker);
+  for (auto& t : th) t.join();
+  return 0;
+}
+
+}  // extern "C"

@@ -21,7 +21,7 @@ def _lib():
 
 def declared_functions():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(gs_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|long long|const char\*)\s+(gs_\w+)\s*\(", text, re.M)))
 
 
 def test_library_exports_every_declared_symbol():
