@@ -19,6 +19,7 @@
 #include "family_data.h"
 #include "gs_common.cuh"
 #include "kernels_nfft.cuh"
+#include "kernels_nfft2d_fast.cuh"
 #include "kernels_uniform.cuh"
 #include "kernels_vec.cuh"
 
@@ -208,6 +209,9 @@ struct gs_op {
   double beta = 0;
   DBuf<double> deconv;
   DBuf<int> perm, base_x, base_y, bins;
+  bool fast2d = false;  // kernels_nfft2d_fast.cuh path (w = 6, p <= 4)
+  int cap = 1;          // chunk capacity per problem (2D work list)
+  DBuf<int> ch_tile, ch_s0, ch_s1, ch_count, tcs;
   DBuf<double> wts_x, wts_y;
   DBuf<cplx> rec_x, rec_y;
   DBuf<double> sqrtw;  // internal order ([B][M]) or empty
@@ -249,6 +253,10 @@ void set_smem_attrs() {
   allow_big_smem(k2_cols_ifft_gather);
   allow_big_smem(k2_rows_ifft_crop);
   allow_big_smem(k2_edges);
+  allow_big_smem(k2f_spread<1>);
+  allow_big_smem(k2f_spread<2>);
+  allow_big_smem(k2f_spread<3>);
+  allow_big_smem(k2f_spread<4>);
   done = true;
 }
 
@@ -275,16 +283,19 @@ __global__ void k_keys(const int* __restrict__ by, const int* __restrict__ bx, i
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= total) return;
   unsigned long long prob = (unsigned long long)(i / M);
-  unsigned long long bin = by ? (unsigned long long)((by[i] / T) * nt + bx[i] / T) : (unsigned long long)bx[i];
+  // 2D: tile-major, then cell (row-major) inside the tile; 1D: cell
+  unsigned long long bin =
+      by ? (unsigned long long)(((by[i] / T) * nt + bx[i] / T) * T * T + (by[i] % T) * T + bx[i] % T)
+         : (unsigned long long)bx[i];
   keys[i] = (prob << 32) | bin;
   vals[i] = (int)(i - (int64_t)prob * M);
 }
 __global__ void k_bin_starts(const unsigned long long* __restrict__ keys, int64_t total, int64_t M, int B, int nbins,
-                             int* __restrict__ starts) {
+                             int scale, int* __restrict__ starts) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t per = nbins + 1;
   if (i >= (int64_t)B * per) return;
-  unsigned long long prob = (unsigned long long)(i / per), bin = (unsigned long long)(i % per);
+  unsigned long long prob = (unsigned long long)(i / per), bin = (unsigned long long)(i % per) * scale;
   unsigned long long key = (prob << 32) | bin;
   int64_t lo = 0, hi = total;
   while (lo < hi) {
@@ -314,7 +325,7 @@ void sort_bins(gs_op* op, const int* by, const int* bx, int nbins, int T, int nt
   CK(cub::DeviceRadixSort::SortPairs(scratch.p, tmp, k_in.p, k_out.p, v_in.p, op->perm.p, (int)total, 0, end_bit, st));
   op->bins.alloc((size_t)op->B * (nbins + 1));
   k_bin_starts<<<nblk((int64_t)op->B * (nbins + 1), 256), 256, 0, st>>>(k_out.p, total, op->M, op->B, nbins,
-                                                                        op->bins.p);
+                                                                        by ? T * T : 1, op->bins.p);
   CKL();
   CK(cudaStreamSynchronize(st));
 }
@@ -518,9 +529,10 @@ gs_op* create(const gs_op_desc* dsc) {
     P.edges = op->edges;
     P.S = 2 * w + 1;
     P.M = M;
-    P.T = std::min(16, n_ov);
+    op->fast2d = d.dim == 2 && P.S == F_S && op->p <= 4 && n_ov >= 2 * F_R;
+    P.T = op->fast2d ? F_T : std::min(16, n_ov);
     P.R = P.T + P.S - 1;
-    P.nt = n_ov / P.T;
+    P.nt = (n_ov + P.T - 1) / P.T;
     P.CW = std::max(1, std::min(8, (int)((120 * 1024) / ((n_ov + 1) * (int)sizeof(cplx)))));
     while (n_ov % P.CW) --P.CW;
     d_xi_x.upload(xi_x.data(), total, st);
@@ -545,7 +557,7 @@ gs_op* create(const gs_op_desc* dsc) {
     sx.alloc(total);
     k_gather_d<<<nblk(total, 256), 256, 0, st>>>(d_xi_x.p, op->perm.p, M, total, sx.p);
     op->base_x.alloc(total);
-    op->wts_x.alloc(total * P.S);
+    op->wts_x.alloc(total * P.S + 2);  // +2: 16-B staging reads may round past the end
     k_kb_window<<<nblk(total, 256), 256, 0, st>>>(sx.p, total, d.J, n_ov, w, op->beta, op->base_x.p, op->wts_x.p);
     if (op->weighted) {
       d_sw.upload(sw.data(), total, st);
@@ -558,17 +570,62 @@ gs_op* create(const gs_op_desc* dsc) {
       sy.alloc(total);
       k_gather_d<<<nblk(total, 256), 256, 0, st>>>(d_xi_y.p, op->perm.p, M, total, sy.p);
       op->base_y.alloc(total);
-      op->wts_y.alloc(total * P.S);
+      op->wts_y.alloc(total * P.S + 2);
       k_kb_window<<<nblk(total, 256), 256, 0, st>>>(sy.p, total, d.J, n_ov, w, op->beta, op->base_y.p, op->wts_y.p);
       op->rec_y.alloc(total * op->Rr);
       build_factors(op.get(), sy.p, nullptr, total, op->rec_y.p, st);
       const int64_t ntiles = (int64_t)P.nt * P.nt;
+      // work list: (tile, sample range) chunks; the generic kernels use one
+      // chunk per tile (empty ones included), the fast ones skip empty tiles
+      // and split dense tiles into chunks of <= kChunk samples
+      std::vector<int> starts((size_t)B * (ntiles + 1));
+      CK(cudaMemcpy(starts.data(), op->bins.p, starts.size() * sizeof(int), cudaMemcpyDeviceToHost));
+      const int kChunk = F_CHUNK;
+      std::vector<std::vector<int>> ct(B), c0(B), c1(B);
+      std::vector<int> tcs((size_t)B * (ntiles + 1));
+      int cap = 1;
+      for (int64_t b = 0; b < B; ++b) {
+        const int* sb = starts.data() + b * (ntiles + 1);
+        int* tb = tcs.data() + b * (ntiles + 1);
+        for (int64_t t = 0; t < ntiles; ++t) {
+          tb[t] = (int)ct[b].size();
+          const int a = sb[t], e = sb[t + 1];
+          if (!op->fast2d) {
+            ct[b].push_back((int)t);
+            c0[b].push_back(a);
+            c1[b].push_back(e);
+            continue;
+          }
+          for (int s = a; s < e; s += kChunk) {
+            ct[b].push_back((int)t);
+            c0[b].push_back(s);
+            c1[b].push_back(std::min(e, s + kChunk));
+          }
+        }
+        tb[ntiles] = (int)ct[b].size();
+        cap = std::max(cap, (int)ct[b].size());
+      }
+      std::vector<int> h_t((size_t)B * cap, 0), h_0((size_t)B * cap, 0), h_1((size_t)B * cap, 0), h_n(B);
+      for (int64_t b = 0; b < B; ++b) {
+        h_n[b] = (int)ct[b].size();
+        for (size_t k = 0; k < ct[b].size(); ++k) {
+          h_t[b * cap + k] = ct[b][k];
+          h_0[b * cap + k] = c0[b][k];
+          h_1[b * cap + k] = c1[b][k];
+        }
+      }
+      op->cap = cap;
+      op->ch_tile.upload(h_t.data(), h_t.size(), st);
+      op->ch_s0.upload(h_0.data(), h_0.size(), st);
+      op->ch_s1.upload(h_1.data(), h_1.size(), st);
+      op->ch_count.upload(h_n.data(), h_n.size(), st);
+      op->tcs.upload(tcs.data(), tcs.size(), st);
       op->G.alloc((size_t)B * n_ov * n_ov);
-      op->TB.alloc((size_t)B * ntiles * P.R * P.R);
+      op->TB.alloc((size_t)B * cap * P.R * P.R);
       if (op->edges) {
         op->lines.alloc((size_t)B * 4 * op->p * n_ov);
-        op->TL.alloc((size_t)B * ntiles * 2 * 2 * op->p * P.R);
-        op->TC.alloc((size_t)B * ntiles * 4 * op->p * op->p);
+        op->TL.alloc((size_t)B * cap * 2 * 2 * op->p * P.R);
+        op->TC.alloc((size_t)B * cap * 4 * op->p * op->p);
       }
     } else {
       op->G.alloc((size_t)B * n_ov);
@@ -651,10 +708,27 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
                                                                            op->logLmax);
         pmark("k2_lines_fft", st);
       }
-      k2_interp<<<dim3(nblk(op->M, 128), B), 128, 0, st>>>(P, op->base_x.p, op->base_y.p, op->wts_x.p, op->wts_y.p,
-                                                            op->rec_x.p, op->rec_y.p, op->G.p, op->lines.p, x,
-                                                            perm_io ? op->perm.p : nullptr, y);
-      pmark("k2_interp", st);
+      if (op->fast2d) {
+        const dim3 grid(op->cap, B);
+        const int* pp = perm_io ? op->perm.p : nullptr;
+#define GS_F_INTERP(PP)                                                                                            \
+  k2f_interp<PP><<<grid, 128, 0, st>>>(P, op->ch_tile.p, op->ch_s0.p, op->ch_s1.p, op->ch_count.p, op->cap,         \
+                                       op->base_x.p, op->base_y.p, op->wts_x.p, op->wts_y.p, op->rec_x.p, op->rec_y.p, \
+                                       op->G.p, op->lines.p, x, pp, y)
+        switch (op->p) {
+          case 1: GS_F_INTERP(1); break;
+          case 2: GS_F_INTERP(2); break;
+          case 3: GS_F_INTERP(3); break;
+          default: GS_F_INTERP(4); break;
+        }
+#undef GS_F_INTERP
+        pmark("k2f_interp", st);
+      } else {
+        k2_interp<<<dim3(nblk(op->M, 128), B), 128, 0, st>>>(P, op->base_x.p, op->base_y.p, op->wts_x.p, op->wts_y.p,
+                                                              op->rec_x.p, op->rec_y.p, op->G.p, op->lines.p, x,
+                                                              perm_io ? op->perm.p : nullptr, y);
+        pmark("k2_interp", st);
+      }
       break;
     }
   }
@@ -698,20 +772,37 @@ void adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
     case GS_ROUTE_NFFT_2D: {
       const NfP& P = op->np;
       const int ntiles = P.nt * P.nt;
-      const size_t per_warp = (size_t)P.R * P.R + (P.edges ? 2 * 2 * P.p * P.R : 0);
-      k2_spread<<<dim3(ntiles, B), 32 * K2_WARPS, per_warp * K2_WARPS * sizeof(cplx), st>>>(
-          P, op->bins.p, op->base_x.p, op->base_y.p, op->wts_x.p, op->wts_y.p, op->rec_x.p, op->rec_y.p, y,
-          perm_io ? op->perm.p : nullptr, op->TB.p, op->TL.p, op->TC.p);
-      pmark("k2_spread", st);
+      if (op->fast2d) {
+        const dim3 grid(op->cap, B);
+        const int* pp = perm_io ? op->perm.p : nullptr;
+#define GS_F_SPREAD(PP)                                                                                          \
+  k2f_spread<PP><<<grid, 32 * F_WARPS, FSpread<PP>::bytes(), st>>>(                                          \
+      P, op->ch_tile.p, op->ch_s0.p, op->ch_s1.p, op->ch_count.p, op->cap, op->base_x.p, op->base_y.p, op->wts_x.p, \
+      op->wts_y.p, op->rec_x.p, op->rec_y.p, y, pp, op->TB.p, op->TL.p, op->TC.p)
+        switch (op->p) {
+          case 1: GS_F_SPREAD(1); break;
+          case 2: GS_F_SPREAD(2); break;
+          case 3: GS_F_SPREAD(3); break;
+          default: GS_F_SPREAD(4); break;
+        }
+#undef GS_F_SPREAD
+        pmark("k2f_spread", st);
+      } else {
+        const size_t per_warp = (size_t)P.R * P.R + (P.edges ? 2 * 2 * P.p * P.R : 0);
+        k2_spread<<<dim3(ntiles, B), 32 * K2_WARPS, per_warp * K2_WARPS * sizeof(cplx), st>>>(
+            P, op->bins.p, op->base_x.p, op->base_y.p, op->wts_x.p, op->wts_y.p, op->rec_x.p, op->rec_y.p, y,
+            perm_io ? op->perm.p : nullptr, op->TB.p, op->TL.p, op->TC.p);
+        pmark("k2_spread", st);
+      }
       k2_cols_ifft_gather<<<dim3(P.n_ov / P.CW, B), 256, (size_t)P.CW * (P.n_ov + 1) * sizeof(cplx), st>>>(
-          P, op->TB.p, op->G.p, op->tw.p, op->logLmax);
+          P, op->TB.p, op->tcs.p, op->cap, op->G.p, op->tw.p, op->logLmax);
       pmark("k2_cols_ifft_gather", st);
       k2_rows_ifft_crop<<<dim3(P.n, B), 256, P.n_ov * sizeof(cplx), st>>>(P, op->G.p, op->deconv.p, z, op->tw.p,
                                                                           op->logLmax);
       pmark("k2_rows_ifft_crop", st);
       if (P.edges) {
-        k2_edges<<<dim3(4 * P.p + 1, B), 256, P.n_ov * sizeof(cplx), st>>>(P, op->TL.p, op->TC.p, op->deconv.p, z,
-                                                                           op->tw.p, op->logLmax);
+        k2_edges<<<dim3(4 * P.p + 1, B), 256, P.n_ov * sizeof(cplx), st>>>(
+            P, op->TL.p, op->TC.p, op->tcs.p, op->ch_count.p, op->cap, op->deconv.p, z, op->tw.p, op->logLmax);
         pmark("k2_edges", st);
       }
       break;

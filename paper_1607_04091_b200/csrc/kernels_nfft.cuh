@@ -404,33 +404,53 @@ k2_spread(NfP P, const int* __restrict__ tile_start, const int* __restrict__ bas
   }
 }
 
-// Sum of the tile-region entries that land on global cell r along one axis:
-// (tile, local) pairs with local = r%T + d*T < R (2D adjoint).
-__device__ __forceinline__ cplx gather_cell(const NfP& P, const cplx* __restrict__ TBp, int r, int c) {
-  cplx a = mk(0, 0);
-  const int T = P.T, R = P.R, nt = P.nt;
-  for (int dy = 0; dy * T + (r % T) < R; ++dy) {
-    const int ty = ((r / T - dy) % nt + nt) % nt, ly = (r % T) + dy * T;
-    for (int dx = 0; dx * T + (c % T) < R; ++dx) {
-      const int tx = ((c / T - dx) % nt + nt) % nt, lx = (c % T) + dx * T;
-      a = cadd(a, ldg2(TBp + ((int64_t)(ty * nt + tx) * R + ly) * R + lx));
+// Tiles whose (T+S-1)-wide region covers global index r along one axis, as
+// (tile, local offset) pairs: region of tile t spans [t*T, t*T + R) mod n_ov;
+// the last tile may be partial (n_ov need not be a multiple of T).
+#define MAX_COVER 8
+__device__ __forceinline__ int cover(int r, int T, int R, int nt, int n_ov, int* tl, int* ll) {
+  int k = 0;
+  const int dmax = (R + T - 1) / T;
+  for (int d = 0; d <= dmax && d < nt; ++d) {
+    const int t = ((r / T - d) % nt + nt) % nt;
+    for (int l = ((r - t * T) % n_ov + n_ov) % n_ov; l < R && k < MAX_COVER; l += n_ov) {
+      tl[k] = t;
+      ll[k] = l;
+      ++k;
     }
   }
+  return k;
+}
+
+// Sum over every chunk of every covering tile of its region entry at cell (r, c)
+// (chunks of a tile: tcs[tile] .. tcs[tile+1]; TBp already offset to the problem)
+__device__ __forceinline__ cplx gather_cell(const NfP& P, const cplx* __restrict__ TBp, const int* __restrict__ tcs,
+                                            int r, int c) {
+  cplx a = mk(0, 0);
+  int ty[MAX_COVER], ly[MAX_COVER], tx[MAX_COVER], lx[MAX_COVER];
+  const int ny = cover(r, P.T, P.R, P.nt, P.n_ov, ty, ly);
+  const int nx = cover(c, P.T, P.R, P.nt, P.n_ov, tx, lx);
+  for (int i = 0; i < ny; ++i)
+    for (int j = 0; j < nx; ++j) {
+      const int tile = ty[i] * P.nt + tx[j];
+      for (int ch = tcs[tile]; ch < tcs[tile + 1]; ++ch)
+        a = cadd(a, ldg2(TBp + ((int64_t)ch * P.R + ly[i]) * P.R + lx[j]));
+    }
   return a;
 }
 
 // gather tile regions -> FFT_{+} along y for CW columns -> G (rows that the
 // crop keeps only)
-__global__ void k2_cols_ifft_gather(NfP P, const cplx* __restrict__ TB, cplx* __restrict__ G,
-                                    const cplx* __restrict__ tw, int logLmax) {
+__global__ void k2_cols_ifft_gather(NfP P, const cplx* __restrict__ TB, const int* __restrict__ tcs_all, int cap,
+                                    cplx* __restrict__ G, const cplx* __restrict__ tw, int logLmax) {
   extern __shared__ cplx sm[];
   const int c0 = blockIdx.x * P.CW, prob = blockIdx.y;
   const int ls = P.n_ov + 1;
-  const int ntiles = P.nt * P.nt;
-  const cplx* TBp = TB + (int64_t)prob * ntiles * P.R * P.R;
+  const cplx* TBp = TB + (int64_t)prob * cap * P.R * P.R;
+  const int* tcs = tcs_all + (int64_t)prob * (P.nt * P.nt + 1);
   for (int t = threadIdx.x; t < P.n_ov * P.CW; t += blockDim.x) {
     const int r = t / P.CW, cc = t - r * P.CW;
-    sm[cc * ls + bitrev(r, P.log_nov)] = gather_cell(P, TBp, r, c0 + cc);
+    sm[cc * ls + bitrev(r, P.log_nov)] = gather_cell(P, TBp, tcs, r, c0 + cc);
   }
   __syncthreads();
   block_fft_bitrev(sm, P.log_nov, P.CW, ls, tw, logLmax, +1);
@@ -470,20 +490,22 @@ __global__ void k2_rows_ifft_crop(NfP P, const cplx* __restrict__ G, const doubl
 // add into the edge rows / columns of Z, freq2wave.cpp:359-385) and, in the
 // extra block per problem, the corner sums (freq2wave.cpp:349-357).
 __global__ void k2_edges(NfP P, const cplx* __restrict__ TL, const cplx* __restrict__ TC,
+                         const int* __restrict__ tcs_all, const int* __restrict__ ch_count, int cap,
                          const double* __restrict__ deconv, cplx* __restrict__ z, const cplx* __restrict__ tw,
                          int logLmax) {
   extern __shared__ cplx sm[];
   const int L = blockIdx.x, prob = blockIdx.y;
   const int p = P.p, twop = 2 * p, n = P.n, T = P.T, R = P.R, nt = P.nt;
-  const int ntiles = nt * nt;
   const int nlin = 2 * twop * R;
+  const int* tcs = tcs_all + (int64_t)prob * (nt * nt + 1);
   cplx* Z = z + (int64_t)prob * n * n;
-  if (L == 2 * twop) {  // corners
+  if (L == 2 * twop) {  // corners: fixed-order sum of the chunk partials
     const int ncorner = 4 * p * p;
-    const cplx* tc = TC + (int64_t)prob * ntiles * ncorner;
+    const cplx* tc = TC + (int64_t)prob * cap * ncorner;
+    const int nch = ch_count[prob];
     for (int q = threadIdx.x; q < ncorner; q += blockDim.x) {
       cplx a = mk(0, 0);
-      for (int t = 0; t < ntiles; ++t) a = cadd(a, tc[(int64_t)t * ncorner + q]);
+      for (int t = 0; t < nch; ++t) a = cadd(a, tc[(int64_t)t * ncorner + q]);
       const int k = q / (p * p), rem = q - k * p * p, i = rem / p, j = rem - i * p;
       const int row0 = (k < 2) ? 0 : n - p, col0 = (k % 2 == 0) ? 0 : n - p;
       Z[(int64_t)(col0 + j) * n + row0 + i] = a;
@@ -492,16 +514,17 @@ __global__ void k2_edges(NfP P, const cplx* __restrict__ TL, const cplx* __restr
   }
   const bool yline = L < twop;
   const int e = yline ? L : L - twop;
-  const cplx* TLp = TL + (int64_t)prob * ntiles * nlin;
+  const cplx* TLp = TL + (int64_t)prob * cap * nlin;
   for (int pos = threadIdx.x; pos < P.n_ov; pos += blockDim.x) {
     cplx a = mk(0, 0);
-    for (int d = 0; d * T + (pos % T) < R; ++d) {
-      const int tk = ((pos / T - d) % nt + nt) % nt, l = (pos % T) + d * T;
+    int tk[MAX_COVER], lk[MAX_COVER];
+    const int nc = cover(pos, T, R, nt, P.n_ov, tk, lk);
+    for (int i = 0; i < nc; ++i)
       for (int o = 0; o < nt; ++o) {
-        const int tile = yline ? tk * nt + o : o * nt + tk;
-        a = cadd(a, TLp[(int64_t)tile * nlin + (yline ? 0 : twop * R) + e * R + l]);
+        const int tile = yline ? tk[i] * nt + o : o * nt + tk[i];
+        for (int ch = tcs[tile]; ch < tcs[tile + 1]; ++ch)
+          a = cadd(a, TLp[(int64_t)ch * nlin + (yline ? 0 : twop * R) + e * R + lk[i]]);
       }
-    }
     sm[bitrev(pos, P.log_nov)] = a;
   }
   __syncthreads();
