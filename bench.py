@@ -103,10 +103,12 @@ def algorithmic_bytes(kernel, dim, p, M, Nc):
     """Compulsory HBM bytes of one launch per problem (SURVEY 8(d) accounting:
     coordinates 8*dim, D 16*dim, L/R 32*p*dim per sample; x / y 16 B per entry)."""
     per_pt = 8 * dim + 16 * dim + (32 * p * dim if p >= 2 else 0)
-    if kernel in ("k2_interp", "k_n1_interp"):
+    if kernel in ("k2_interp", "k2f_interp", "k_n1_interp"):
         return M * (per_pt + 16) + 16 * Nc
-    if kernel in ("k2_spread", "k_n1_spread"):
+    if kernel in ("k2_spread", "k2f_spread", "k_n1_spread"):
         return M * (per_pt + 16)
+    if kernel in ("k_uni_fwd", "k_uni_adj"):  # whole 1D uniform apply in one CTA
+        return 16 * (Nc + M) + M * (16 + (32 * p if p >= 2 else 0))
     return None
 
 

@@ -253,6 +253,10 @@ void set_smem_attrs() {
   allow_big_smem(k2_cols_ifft_gather);
   allow_big_smem(k2_rows_ifft_crop);
   allow_big_smem(k2_edges);
+  allow_big_smem(k2f_interp<1>);
+  allow_big_smem(k2f_interp<2>);
+  allow_big_smem(k2f_interp<3>);
+  allow_big_smem(k2f_interp<4>);
   allow_big_smem(k2f_spread<1>);
   allow_big_smem(k2f_spread<2>);
   allow_big_smem(k2f_spread<3>);
@@ -712,7 +716,8 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
         const dim3 grid(op->cap, B);
         const int* pp = perm_io ? op->perm.p : nullptr;
 #define GS_F_INTERP(PP)                                                                                            \
-  k2f_interp<PP><<<grid, 128, 0, st>>>(P, op->ch_tile.p, op->ch_s0.p, op->ch_s1.p, op->ch_count.p, op->cap,         \
+  k2f_interp<PP><<<grid, 128, 2 * (F_CHUNK * F_S + 2) * sizeof(double), st>>>(                                    \
+      P, op->ch_tile.p, op->ch_s0.p, op->ch_s1.p, op->ch_count.p, op->cap,                                           \
                                        op->base_x.p, op->base_y.p, op->wts_x.p, op->wts_y.p, op->rec_x.p, op->rec_y.p, \
                                        op->G.p, op->lines.p, x, pp, y)
         switch (op->p) {

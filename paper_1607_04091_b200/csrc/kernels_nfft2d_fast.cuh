@@ -22,6 +22,7 @@
 #define F_S 13
 #define F_T 12
 #define F_R 24
+#define F_CHUNK 160  // samples per work item (chunks of a tile are staged in shared memory)
 
 // ------------------------------------------------------------------ interpolation
 template <int P>
@@ -48,31 +49,57 @@ __global__ void __launch_bounds__(128, 3) k2f_interp(NfP Pp, const int* __restri
   const int ty = tile / Pp.nt, tx = tile - ty * Pp.nt;
   const int n_ov = Pp.n_ov, mask = n_ov - 1, n = Pp.n;
   const cplx* g = G + (int64_t)prob * n_ov * n_ov;
+  // asynchronous 16-B copies (cp.async): all of the tile's staging is in flight at once
+  auto cp16 = [](cplx* dst, const cplx* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
+                     static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+  };
   for (int i = threadIdx.x; i < R * R; i += blockDim.x) {
     const int r = i / R, cc = i - r * R;
-    reg[i] = ldg2(g + (int64_t)((ty * T + r) & mask) * n_ov + ((tx * T + cc) & mask));
+    cp16(reg + i, g + (int64_t)((ty * T + r) & mask) * n_ov + ((tx * T + cc) & mask));
   }
   if (E > 0) {
     const cplx* LY = lines + (int64_t)prob * 2 * E * n_ov;
     const cplx* LX = LY + (int64_t)E * n_ov;
     for (int i = threadIdx.x; i < E * R; i += blockDim.x) {
       const int e = i / R, r = i - e * R;
-      ly[e][r] = ldg2(LY + (int64_t)e * n_ov + ((ty * T + r) & mask));
-      lx[e][r] = ldg2(LX + (int64_t)e * n_ov + ((tx * T + r) & mask));
+      cp16(&ly[e][r], LY + (int64_t)e * n_ov + ((ty * T + r) & mask));
+      cp16(&lx[e][r], LX + (int64_t)e * n_ov + ((tx * T + r) & mask));
     }
     const cplx* X = x + (int64_t)prob * n * n;
     for (int q = threadIdx.x; q < 4 * P * P; q += blockDim.x) {
       const int k = q / (P * P), rem = q - k * P * P, i = rem / P, j = rem - i * P;
       const int row0 = (k < 2) ? 0 : n - P, col0 = (k % 2 == 0) ? 0 : n - P;
-      cx[q] = ldg2(X + (int64_t)(col0 + j) * n + row0 + i);
+      cp16(cx + q, X + (int64_t)(col0 + j) * n + row0 + i);
     }
   }
+  // the chunk's window weights (contiguous ranges, staged 16-B aligned-down)
+  const int64_t g0 = (int64_t)prob * Pp.M + s0;
+  const int nn = s1 - s0;
+  auto stage = [&](double* dst, const double* src, int count) -> const double* {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(src), al = a & ~uintptr_t(15);
+    const int off = (int)(a - al), nv = (off + count * 8 + 15) / 16;
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    for (int i = threadIdx.x; i < nv; i += blockDim.x)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d + 16u * i),
+                   "l"(reinterpret_cast<const char*>(al) + 16 * i)
+                   : "memory");
+    return reinterpret_cast<const double*>(reinterpret_cast<const char*>(dst) + off);
+  };
+  extern __shared__ __align__(16) double fi_dyn[];  // [2][F_CHUNK * S + 2]
+  double* swy = fi_dyn;
+  double* swx = fi_dyn + F_CHUNK * S + 2;
+  const double* wys = stage(swy, wy_all + g0 * S, nn * S);
+  const double* wxs = stage(swx, wx_all + g0 * S, nn * S);
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
   for (int s = s0 + threadIdx.x; s < s1; s += blockDim.x) {
     const int64_t gs = (int64_t)prob * Pp.M + s;
     const int oy = base_y[gs] - ty * T, ox = base_x[gs] - tx * T;
-    const double* wyp = wy_all + gs * S;
-    const double* wxp = wx_all + gs * S;
+    const double* wyp = wys + (s - s0) * S;
+    const double* wxp = wxs + (s - s0) * S;
     const cplx* rx = recx_all + gs * RR;
     const cplx* ry = recy_all + gs * RR;
     const cplx Dx = ldg2(rx), Dy = ldg2(ry);
@@ -86,7 +113,7 @@ __global__ void __launch_bounds__(128, 3) k2f_interp(NfP Pp, const int* __restri
     {
       double wx[S];
 #pragma unroll
-      for (int t = 0; t < S; ++t) wx[t] = __ldg(wxp + t);
+      for (int t = 0; t < S; ++t) wx[t] = wxp[t];
       cplx acc = mk(0, 0);
 #pragma unroll
       for (int t0 = 0; t0 < S; ++t0) {
@@ -94,7 +121,7 @@ __global__ void __launch_bounds__(128, 3) k2f_interp(NfP Pp, const int* __restri
         cplx ra = mk(0, 0);
 #pragma unroll
         for (int t1 = 0; t1 < S; ++t1) ra = caxpy(ra, wx[t1], row[t1]);
-        acc = caxpy(acc, __ldg(wyp + t0), ra);
+        acc = caxpy(acc, wyp[t0], ra);
       }
       out = cmul(cmul(Dx, Dy), acc);
       if (E > 0) {
@@ -112,7 +139,7 @@ __global__ void __launch_bounds__(128, 3) k2f_interp(NfP Pp, const int* __restri
     if (E > 0) {
       double wy[S];
 #pragma unroll
-      for (int t = 0; t < S; ++t) wy[t] = __ldg(wyp + t);
+      for (int t = 0; t < S; ++t) wy[t] = wyp[t];
 #pragma unroll
       for (int i = 0; i < E; ++i) {
         const int hi = i < P ? 0 : 1, ii = i - hi * P;
@@ -135,7 +162,6 @@ __global__ void __launch_bounds__(128, 3) k2f_interp(NfP Pp, const int* __restri
 
 // ------------------------------------------------------------------ spreading
 #define F_WARPS 4
-#define F_CHUNK 160  // samples per spreading work item (staged in shared memory)
 
 template <int P>
 struct FSpread {
