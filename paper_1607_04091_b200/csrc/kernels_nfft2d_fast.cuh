@@ -39,7 +39,8 @@ __global__ void __launch_bounds__(128, 3) k2f_interp(NfP Pp, const int* __restri
   constexpr int EE = E > 0 ? E : 1;
   constexpr int RR = 1 + E;
   constexpr int NC = P >= 2 ? 4 * P * P : 1;
-  __shared__ cplx reg[R * R];
+  constexpr int RS = R + 1;  // padded row stride: rows 384 B apart would alias the same banks
+  __shared__ cplx reg[R * RS];
   __shared__ cplx ly[EE][R];
   __shared__ cplx lx[EE][R];
   __shared__ cplx cx[NC];
@@ -58,7 +59,7 @@ __global__ void __launch_bounds__(128, 3) k2f_interp(NfP Pp, const int* __restri
   };
   for (int i = threadIdx.x; i < R * R; i += blockDim.x) {
     const int r = i / R, cc = i - r * R;
-    cp16(reg + i, g + (int64_t)((ty * T + r) & mask) * n_ov + ((tx * T + cc) & mask));
+    cp16(reg + r * RS + cc, g + (int64_t)((ty * T + r) & mask) * n_ov + ((tx * T + cc) & mask));
   }
   if (E > 0) {
     const cplx* LY = lines + (int64_t)prob * 2 * E * n_ov;
@@ -117,7 +118,7 @@ __global__ void __launch_bounds__(128, 3) k2f_interp(NfP Pp, const int* __restri
       cplx acc = mk(0, 0);
 #pragma unroll
       for (int t0 = 0; t0 < S; ++t0) {
-        const cplx* row = reg + (oy + t0) * R + ox;
+        const cplx* row = reg + (oy + t0) * RS + ox;
         cplx ra = mk(0, 0);
 #pragma unroll
         for (int t1 = 0; t1 < S; ++t1) ra = caxpy(ra, wx[t1], row[t1]);
