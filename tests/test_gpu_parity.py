@@ -268,3 +268,33 @@ def test_device_tensors_roundtrip():
     yd = g.apply_forward(op, torch.from_numpy(x).cuda())
     assert yd.is_cuda
     assert rel_error(yd.cpu().numpy(), g.apply_forward(op, x)) == 0.0
+
+
+# ------------------------------------------------------------------ full-size C4 / C5 problems
+def _voronoi_fast(dim, c, K):
+    from paper_1607_04091_b200 import inputs
+    return inputs.voronoi_weights(dim, c, K)
+
+
+def test_c5_problem_full_size():
+    """One C5 problem at full size (2^18 jittered samples, db4 J=8, Voronoi
+    weights): T x / T* y parity and a short fixed-count CGLS."""
+    rng = np.random.default_rng(20160613)
+    c = oracle.gen_jitter(512, 0.5, 0.2, 20160613, 2)
+    K = float(np.max(np.abs(c)))
+    mu = _voronoi_fast(2, c, K)
+    ref, op = build_pair(2, 4, 8, c, weights=mu, bandwidth=K)
+    assert op.route == "nfft_2d"
+    check_apply(ref, op, rng)
+    b = rc(ref.rows, rng)
+    check_cgls(ref, op, b, 3)
+
+
+def test_c4_spiral_full_size_apply():
+    """C4 at full size (2^20 spiral samples, R=512, 64 turns, db4 J=9)."""
+    rng = np.random.default_rng(20160613)
+    c = oracle.gen_spiral(64, 16384.0, 512.0)
+    mu = _voronoi_fast(2, c, 512.0)
+    ref, op = build_pair(2, 4, 9, c, weights=mu, bandwidth=512.0)
+    assert op.route == "nfft_2d"
+    check_apply(ref, op, rng)
