@@ -32,7 +32,7 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB = os.path.join(_HERE, "libgs_b200.so")
+_LIB = os.environ.get("GS_B200_LIB") or os.path.join(_HERE, "libgs_b200.so")  # env: A/B builds only
 _lib = None
 
 

@@ -138,6 +138,7 @@ __global__ void k_kb_window(const double* __restrict__ xi, int64_t count, int J,
   long long j0 = llround(pos);
   long long b = j0 - w;
   base[i] = (int)(((b % n_ov) + n_ov) % n_ov);
+  if (!wts) return;  // base only (bin keys)
   for (int t = 0; t < S; ++t) {
     double u = pos - (double)(j0 - w + t);
     double q = 1.0 - (u / w) * (u / w);

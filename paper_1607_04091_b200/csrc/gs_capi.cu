@@ -216,14 +216,14 @@ struct gs_op {
   DBuf<cplx> rec_x, rec_y;
   DBuf<double> sqrtw;  // internal order ([B][M]) or empty
   // workspace
-  DBuf<cplx> G, lines, TB, TL, TC, W;
+  DBuf<cplx> G, lines, TB, TL, TLF, TC, TCF, W;
   DBuf<cplx> stage_a, stage_b;
   std::mutex mu;
 
   size_t device_bytes() const {
     return tw.bytes() + rec_u.bytes() + rec_ax.bytes() + rec_ay.bytes() + deconv.bytes() + perm.bytes() +
            base_x.bytes() + base_y.bytes() + bins.bytes() + wts_x.bytes() + wts_y.bytes() + rec_x.bytes() +
-           rec_y.bytes() + sqrtw.bytes() + G.bytes() + lines.bytes() + TB.bytes() + TL.bytes() + TC.bytes() +
+           rec_y.bytes() + sqrtw.bytes() + G.bytes() + lines.bytes() + TB.bytes() + TL.bytes() + TLF.bytes() + TC.bytes() + TCF.bytes() +
            W.bytes() + stage_a.bytes() + stage_b.bytes();
   }
 };
@@ -543,14 +543,12 @@ gs_op* create(const gs_op_desc* dsc) {
     if (d.dim == 2) d_xi_y.upload(xi_y.data(), total, st);
     // 1. windows in the caller's order -> bin keys -> sort
     DBuf<int> bx0, by0;
-    DBuf<double> wdummy;
     bx0.alloc(total);
-    wdummy.alloc(total * P.S);
-    k_kb_window<<<nblk(total, 256), 256, 0, st>>>(d_xi_x.p, total, d.J, n_ov, w, op->beta, bx0.p, wdummy.p);
+    k_kb_window<<<nblk(total, 256), 256, 0, st>>>(d_xi_x.p, total, d.J, n_ov, w, op->beta, bx0.p, nullptr);
     CKL();
     if (d.dim == 2) {
       by0.alloc(total);
-      k_kb_window<<<nblk(total, 256), 256, 0, st>>>(d_xi_y.p, total, d.J, n_ov, w, op->beta, by0.p, wdummy.p);
+      k_kb_window<<<nblk(total, 256), 256, 0, st>>>(d_xi_y.p, total, d.J, n_ov, w, op->beta, by0.p, nullptr);
       CKL();
       sort_bins(op.get(), by0.p, bx0.p, P.nt * P.nt, P.T, P.nt, st);
     } else {
@@ -630,6 +628,8 @@ gs_op* create(const gs_op_desc* dsc) {
         op->lines.alloc((size_t)B * 4 * op->p * n_ov);
         op->TL.alloc((size_t)B * cap * 2 * 2 * op->p * P.R);
         op->TC.alloc((size_t)B * cap * 4 * op->p * op->p);
+        op->TLF.alloc((size_t)B * 2 * P.nt * 2 * op->p * P.R);
+        op->TCF.alloc((size_t)B * ((cap + K2_CGROUP - 1) / K2_CGROUP) * 4 * op->p * op->p);
       }
     } else {
       op->G.alloc((size_t)B * n_ov);
@@ -717,9 +717,8 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
         const int* pp = perm_io ? op->perm.p : nullptr;
 #define GS_F_INTERP(PP)                                                                                            \
   k2f_interp<PP><<<grid, 128, 2 * (F_CHUNK * F_S + 2) * sizeof(double), st>>>(                                    \
-      P, op->ch_tile.p, op->ch_s0.p, op->ch_s1.p, op->ch_count.p, op->cap,                                           \
-                                       op->base_x.p, op->base_y.p, op->wts_x.p, op->wts_y.p, op->rec_x.p, op->rec_y.p, \
-                                       op->G.p, op->lines.p, x, pp, y)
+      P, op->ch_tile.p, op->ch_s0.p, op->ch_s1.p, op->ch_count.p, op->cap, op->base_x.p, op->base_y.p, op->wts_x.p,  \
+      op->wts_y.p, op->rec_x.p, op->rec_y.p, op->G.p, op->lines.p, x, pp, y)
         switch (op->p) {
           case 1: GS_F_INTERP(1); break;
           case 2: GS_F_INTERP(2); break;
@@ -782,8 +781,8 @@ void adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
         const int* pp = perm_io ? op->perm.p : nullptr;
 #define GS_F_SPREAD(PP)                                                                                          \
   k2f_spread<PP><<<grid, 32 * F_WARPS, FSpread<PP>::bytes(), st>>>(                                          \
-      P, op->ch_tile.p, op->ch_s0.p, op->ch_s1.p, op->ch_count.p, op->cap, op->base_x.p, op->base_y.p, op->wts_x.p, \
-      op->wts_y.p, op->rec_x.p, op->rec_y.p, y, pp, op->TB.p, op->TL.p, op->TC.p)
+      P, op->ch_tile.p, op->ch_s0.p, op->ch_s1.p, op->ch_count.p, op->cap, op->base_x.p, op->base_y.p,            \
+      op->wts_x.p, op->wts_y.p, op->rec_x.p, op->rec_y.p, y, pp, op->TB.p, op->TL.p, op->TC.p)
         switch (op->p) {
           case 1: GS_F_SPREAD(1); break;
           case 2: GS_F_SPREAD(2); break;
@@ -806,8 +805,15 @@ void adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
                                                                           op->logLmax);
       pmark("k2_rows_ifft_crop", st);
       if (P.edges) {
+        const int per = P.nt * 2 * P.p * P.R;
+        k2_fold_lines<<<dim3(nblk(per, 128), 2, B), 128, 0, st>>>(P, op->TL.p, op->tcs.p, op->cap, op->TLF.p);
+        pmark("k2_fold_lines", st);
+        const int ngroups = (op->cap + K2_CGROUP - 1) / K2_CGROUP;
+        k2_fold_corners<<<dim3(nblk(ngroups * 4 * P.p * P.p, 128), B), 128, 0, st>>>(
+            P, op->TC.p, op->ch_count.p, op->cap, ngroups, op->TCF.p);
+        pmark("k2_fold_corners", st);
         k2_edges<<<dim3(4 * P.p + 1, B), 256, P.n_ov * sizeof(cplx), st>>>(
-            P, op->TL.p, op->TC.p, op->tcs.p, op->ch_count.p, op->cap, op->deconv.p, z, op->tw.p, op->logLmax);
+            P, op->TLF.p, op->TCF.p, op->tcs.p, op->ch_count.p, op->cap, op->deconv.p, z, op->tw.p, op->logLmax);
         pmark("k2_edges", st);
       }
       break;

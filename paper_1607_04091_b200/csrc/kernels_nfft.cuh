@@ -489,7 +489,46 @@ __global__ void k2_rows_ifft_crop(NfP P, const cplx* __restrict__ G, const doubl
 // Side lines (gather of the tile line segments, FFT_{+}, crop, deconvolve,
 // add into the edge rows / columns of Z, freq2wave.cpp:359-385) and, in the
 // extra block per problem, the corner sums (freq2wave.cpp:349-357).
-__global__ void k2_edges(NfP P, const cplx* __restrict__ TL, const cplx* __restrict__ TC,
+// Fold the side-line partials of every chunk along the tile row (y-lines) or
+// tile column (x-lines) they belong to: TLF[prob][axis][t][e][l], one thread
+// per (t, e, l) -- a fully parallel first level of the line gather.
+__global__ void k2_fold_lines(NfP P, const cplx* __restrict__ TL, const int* __restrict__ tcs_all, int cap,
+                              cplx* __restrict__ TLF) {
+  const int prob = blockIdx.z, axis = blockIdx.y;
+  const int twop = 2 * P.p, R = P.R, nt = P.nt;
+  const int per = nt * twop * R;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= per) return;
+  const int t = i / (twop * R), rem = i - t * twop * R;  // rem = e * R + l
+  const int nlin = 2 * twop * R;
+  const int* tcs = tcs_all + (int64_t)prob * (nt * nt + 1);
+  const cplx* TLp = TL + (int64_t)prob * cap * nlin + (axis ? twop * R : 0) + rem;
+  cplx a = mk(0, 0);
+  for (int o = 0; o < nt; ++o) {
+    const int tile = axis == 0 ? t * nt + o : o * nt + t;
+    for (int ch = tcs[tile]; ch < tcs[tile + 1]; ++ch) a = cadd(a, ldg2(TLp + (int64_t)ch * nlin));
+  }
+  TLF[(((int64_t)prob * 2 + axis) * nt + t) * twop * R + rem] = a;
+}
+
+// First level of the corner reduction: TCF[prob][g][q] = sum of the corner
+// partials of chunks g*64 .. g*64+63 (fixed order).
+#define K2_CGROUP 64
+__global__ void k2_fold_corners(NfP P, const cplx* __restrict__ TC, const int* __restrict__ ch_count, int cap,
+                                int ngroups, cplx* __restrict__ TCF) {
+  const int prob = blockIdx.y;
+  const int ncorner = 4 * P.p * P.p;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ngroups * ncorner) return;
+  const int g = i / ncorner, q = i - g * ncorner;
+  const int nch = ch_count[prob];
+  const cplx* tc = TC + (int64_t)prob * cap * ncorner + q;
+  cplx a = mk(0, 0);
+  for (int c = g * K2_CGROUP; c < min(nch, (g + 1) * K2_CGROUP); ++c) a = cadd(a, ldg2(tc + (int64_t)c * ncorner));
+  TCF[((int64_t)prob * ngroups + g) * ncorner + q] = a;
+}
+
+__global__ void k2_edges(NfP P, const cplx* __restrict__ TLF, const cplx* __restrict__ TC,
                          const int* __restrict__ tcs_all, const int* __restrict__ ch_count, int cap,
                          const double* __restrict__ deconv, cplx* __restrict__ z, const cplx* __restrict__ tw,
                          int logLmax) {
@@ -499,10 +538,11 @@ __global__ void k2_edges(NfP P, const cplx* __restrict__ TL, const cplx* __restr
   const int nlin = 2 * twop * R;
   const int* tcs = tcs_all + (int64_t)prob * (nt * nt + 1);
   cplx* Z = z + (int64_t)prob * n * n;
-  if (L == 2 * twop) {  // corners: fixed-order sum of the chunk partials
+  if (L == 2 * twop) {  // corners: fixed-order sum of the chunk-group partials (TC = TCF here)
     const int ncorner = 4 * p * p;
-    const cplx* tc = TC + (int64_t)prob * cap * ncorner;
-    const int nch = ch_count[prob];
+    const int ngroups = (cap + K2_CGROUP - 1) / K2_CGROUP;
+    const cplx* tc = TC + (int64_t)prob * ngroups * ncorner;
+    const int nch = (ch_count[prob] + K2_CGROUP - 1) / K2_CGROUP;
     for (int q = threadIdx.x; q < ncorner; q += blockDim.x) {
       cplx a = mk(0, 0);
       for (int t = 0; t < nch; ++t) a = cadd(a, tc[(int64_t)t * ncorner + q]);
@@ -514,17 +554,14 @@ __global__ void k2_edges(NfP P, const cplx* __restrict__ TL, const cplx* __restr
   }
   const bool yline = L < twop;
   const int e = yline ? L : L - twop;
-  const cplx* TLp = TL + (int64_t)prob * cap * nlin;
+  const cplx* TLFp = TLF + ((int64_t)prob * 2 + (yline ? 0 : 1)) * nt * twop * R;
+  (void)nlin;
+  (void)tcs;
   for (int pos = threadIdx.x; pos < P.n_ov; pos += blockDim.x) {
     cplx a = mk(0, 0);
     int tk[MAX_COVER], lk[MAX_COVER];
     const int nc = cover(pos, T, R, nt, P.n_ov, tk, lk);
-    for (int i = 0; i < nc; ++i)
-      for (int o = 0; o < nt; ++o) {
-        const int tile = yline ? tk[i] * nt + o : o * nt + tk[i];
-        for (int ch = tcs[tile]; ch < tcs[tile + 1]; ++ch)
-          a = cadd(a, TLp[(int64_t)ch * nlin + (yline ? 0 : twop * R) + e * R + lk[i]]);
-      }
+    for (int i = 0; i < nc; ++i) a = cadd(a, TLFp[((int64_t)tk[i] * twop + e) * R + lk[i]]);
     sm[bitrev(pos, P.log_nov)] = a;
   }
   __syncthreads();
