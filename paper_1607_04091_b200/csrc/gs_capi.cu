@@ -218,6 +218,7 @@ struct gs_op {
   // workspace
   DBuf<cplx> G, lines, TB, TL, TLF, TC, TCF, W;
   DBuf<cplx> stage_a, stage_b;
+  gs_cgls_session* solve_cache = nullptr;  // workspace of the last gs_solve_least_squares
   std::mutex mu;
 
   size_t device_bytes() const {
@@ -978,6 +979,7 @@ int gs_op_destroy(gs_op* op) {
   if (!op) return GS_OK;
   cudaSetDevice(op->device);
   cudaDeviceSynchronize();
+  gs_cgls_destroy(op->solve_cache);
   delete op;
   return GS_OK;
 }
@@ -1056,21 +1058,21 @@ int gs_cgls_begin(gs_op* op, const double* raw_samples, int64_t samples_len, con
     std::lock_guard<std::mutex> lk(op->mu);
     CK(cudaSetDevice(op->device));
     cudaStream_t st = (cudaStream_t)stream;
-    std::unique_ptr<gs_cgls_session> S(new gs_cgls_session);
+    // *out may carry an earlier session of this op: its device buffers are reused
+    std::unique_ptr<gs_cgls_session> S((*out && (*out)->s.op == op) ? *out : new gs_cgls_session);
+    *out = nullptr;
     const int64_t TM = op->M * op->B, TN = op->Nc * op->B;
     const cplx* b = (const cplx*)raw_samples;
-    DBuf<cplx> sb, sx;
     if (!is_device_ptr(raw_samples)) {
-      sb.upload((const cplx*)raw_samples, TM, st);
-      b = sb.p;
+      op->stage_a.upload((const cplx*)raw_samples, TM, st);
+      b = op->stage_a.p;
     }
     const cplx* xx = (const cplx*)x0;
     if (x0 && !is_device_ptr(x0)) {
-      sx.upload((const cplx*)x0, TN, st);
-      xx = sx.p;
+      op->stage_b.upload((const cplx*)x0, TN, st);
+      xx = op->stage_b.p;
     }
     session_begin(S->s, op, b, true, xx, tolerance, std::max(2, history_capacity), st);
-    CK(cudaStreamSynchronize(st));
     *out = S.release();
   });
 }
@@ -1130,14 +1132,19 @@ int gs_cgls_destroy(gs_cgls_session* s) {
 int gs_solve_least_squares(gs_op* op, const double* raw_samples, int64_t samples_len, const double* x0,
                            int max_iterations, double tolerance, double* x_out, gs_solve_stats* stats,
                            double* history, void* stream) {
-  gs_cgls_session* s = nullptr;
   if (!op) {
     g_err = "null handle";
     return GS_ERR_USAGE;
   }
+  // the op keeps its last solve workspace, so repeated solves allocate nothing
+  gs_cgls_session* s = op->solve_cache;
+  op->solve_cache = nullptr;
   const int max_iter = max_iterations > 0 ? max_iterations : (int)std::min<int64_t>(INT32_MAX / 2, 2 * op->Nc);
   int rc = gs_cgls_begin(op, raw_samples, samples_len, x0, tolerance, max_iter + 1, stream, &s);
-  if (rc) return rc;
+  if (rc) {
+    gs_cgls_destroy(s);
+    return rc;
+  }
   int done = 0;
   int active = 1;
   rc = gs_cgls_active(s, stream, &active);
@@ -1150,7 +1157,7 @@ int gs_solve_least_squares(gs_op* op, const double* raw_samples, int64_t samples
     chunk = std::min(chunk * 2, 64);
   }
   if (rc == 0) rc = gs_cgls_finish(s, x_out, stats, history, stream);
-  gs_cgls_destroy(s);
+  op->solve_cache = s;
   return rc;
 }
 
