@@ -185,35 +185,36 @@ struct FSpread {
   static constexpr size_t MAIN = (STG_END > FOLD ? STG_END : FOLD);  // fold buffer aliases the staging
   struct Scratch {  // derived per-sample values shared inside a warp (two samples in flight)
     cplx d[2][32];
+    double2 wy[16];  // row taps of the two samples, packed (wy_a[t], wy_b[t])
   };
   static constexpr size_t bytes() { return (MAIN + 15) / 16 * 16 + sizeof(Scratch) * F_WARPS; }
 };
 
-// acc[OY + t] += wa[t] u0 + wb[t] u1, t < 13, with OY a compile-time row offset
+// acc[OY + t] += w[t].x u0 + w[t].y u1, t < 13 (w = the two samples' row taps,
+// packed pairwise), with OY a compile-time row offset
 template <int OY>
-__device__ __forceinline__ void f_upd(cplx (&acc)[F_R], cplx u0, cplx u1, const double* wa, const double* wb) {
+__device__ __forceinline__ void f_upd(cplx (&acc)[F_R], cplx u0, cplx u1, const double2* w) {
 #pragma unroll
   for (int t = 0; t < F_S; ++t) {
-    const double x = wa[t], z = wb[t];
-    acc[OY + t].x = fma(z, u1.x, fma(x, u0.x, acc[OY + t].x));
-    acc[OY + t].y = fma(z, u1.y, fma(x, u0.y, acc[OY + t].y));
+    const double2 ww = w[t];
+    acc[OY + t].x = fma(ww.y, u1.x, fma(ww.x, u0.x, acc[OY + t].x));
+    acc[OY + t].y = fma(ww.y, u1.y, fma(ww.x, u0.y, acc[OY + t].y));
   }
 }
-__device__ __forceinline__ void f_upd_dispatch(int oy, cplx (&acc)[F_R], cplx u0, cplx u1, const double* wa,
-                                               const double* wb) {
+__device__ __forceinline__ void f_upd_dispatch(int oy, cplx (&acc)[F_R], cplx u0, cplx u1, const double2* w) {
   switch (oy) {
-    case 0: f_upd<0>(acc, u0, u1, wa, wb); break;
-    case 1: f_upd<1>(acc, u0, u1, wa, wb); break;
-    case 2: f_upd<2>(acc, u0, u1, wa, wb); break;
-    case 3: f_upd<3>(acc, u0, u1, wa, wb); break;
-    case 4: f_upd<4>(acc, u0, u1, wa, wb); break;
-    case 5: f_upd<5>(acc, u0, u1, wa, wb); break;
-    case 6: f_upd<6>(acc, u0, u1, wa, wb); break;
-    case 7: f_upd<7>(acc, u0, u1, wa, wb); break;
-    case 8: f_upd<8>(acc, u0, u1, wa, wb); break;
-    case 9: f_upd<9>(acc, u0, u1, wa, wb); break;
-    case 10: f_upd<10>(acc, u0, u1, wa, wb); break;
-    case 11: f_upd<11>(acc, u0, u1, wa, wb); break;
+    case 0: f_upd<0>(acc, u0, u1, w); break;
+    case 1: f_upd<1>(acc, u0, u1, w); break;
+    case 2: f_upd<2>(acc, u0, u1, w); break;
+    case 3: f_upd<3>(acc, u0, u1, w); break;
+    case 4: f_upd<4>(acc, u0, u1, w); break;
+    case 5: f_upd<5>(acc, u0, u1, w); break;
+    case 6: f_upd<6>(acc, u0, u1, w); break;
+    case 7: f_upd<7>(acc, u0, u1, w); break;
+    case 8: f_upd<8>(acc, u0, u1, w); break;
+    case 9: f_upd<9>(acc, u0, u1, w); break;
+    case 10: f_upd<10>(acc, u0, u1, w); break;
+    case 11: f_upd<11>(acc, u0, u1, w); break;
     default: __builtin_unreachable();
   }
 }
@@ -323,6 +324,7 @@ k2f_spread(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ ch_s
         const cplx Bv = role_b == 0 ? rx[0] : (role_b == 1 ? mk(1.0, 0.0) : ry[0]);
         scr.d[k][lane] = cmul(conj_(cmul(Av, Bv)), ys);
       }
+      if (lane < S) scr.wy[lane] = make_double2(s_wy[s * S + lane], s_wy[sb * S + lane]);
       __syncwarp();
       cplx u[2];
       double w1[2];
@@ -335,7 +337,7 @@ k2f_spread(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ ch_s
         const cplx ug = cscale(scr.d[k][24], w1[k]);
         u[k] = lane < R ? ug : ((E > 0 && lane - R < E) ? scr.d[k][16 + ly] : mk(0, 0));
       }
-      f_upd_dispatch(oy, acc, u[0], u[1], s_wy + s * S, s_wy + sb * S);
+      f_upd_dispatch(oy, acc, u[0], u[1], scr.wy);
       if (E > 0) {
 #pragma unroll
         for (int e = 0; e < E; ++e) accx[e] = caxpy(caxpy(accx[e], w1[0], scr.d[0][e]), w1[1], scr.d[1][e]);
