@@ -203,7 +203,7 @@ struct gs_op {
   // uniform / tensor
   UniP up{}, upx{}, upy{};
   int64_t Ma = 0, Mb = 0;
-  DBuf<cplx> rec_u, rec_ax, rec_ay;
+  DBuf<cplx> rec_u, rec_ax, rec_ay, ph_u, ph_x, ph_y;
   // NFFT
   NfP np{};
   double beta = 0;
@@ -356,6 +356,22 @@ UniP make_uni(gs_op* op, int64_t M, double eps) {
   P.phase_step = GS_PI * eps * (double)M / (double)op->n;  // nufft.cpp:412
   return P;
 }
+// phase tables of a uniform setup (see UniP), computed with the reference's formulas
+void attach_phases(UniP& P, DBuf<cplx>& buf, cudaStream_t st) {
+  std::vector<cplx> h((size_t)P.n + P.M);
+  for (int l = 0; l < P.n; ++l) {
+    const double a = P.phase_step * (double)l;
+    h[l] = mk(std::cos(a), std::sin(a));
+  }
+  for (int m = 0; m < P.M; ++m) {
+    const double xi = P.eps / (double)P.n * ((double)m - (double)P.M / 2.0);
+    const double a = GS_PI * (double)P.n * xi;
+    h[(size_t)P.n + m] = mk(std::cos(a), std::sin(a));
+  }
+  buf.upload(h.data(), h.size(), st);
+  P.ph_in = buf.p;
+  P.ph_out = buf.p + P.n;
+}
 size_t uni_smem(const UniP& P) { return (size_t)P.N2 * sizeof(cplx) * (P.logN2 >= 0 ? 1 : 2); }
 
 // ------------------------------------------------------------------ construction
@@ -483,6 +499,7 @@ gs_op* create(const gs_op_desc* dsc) {
   DBuf<double> d_xi_x, d_xi_y, d_sw;
   if (op->route == GS_ROUTE_UNIFORM_1D) {
     op->up = make_uni(op.get(), M, op->uniform_eps);
+    attach_phases(op->up, op->ph_u, st);
     make_twiddles(op.get(), op->up.N2, st);
     d_xi_x.upload(xi_x.data(), total, st);
     if (op->weighted) op->sqrtw.upload(sw.data(), total, st);
@@ -496,6 +513,8 @@ gs_op* create(const gs_op_desc* dsc) {
       for (int64_t k = 0; k < Mb; ++k) ay[b * Mb + k] = coords[(b * M + k) * 2 + 1];
     }
     make_twiddles(op.get(), std::max(op->upx.N2, op->upy.N2), st);
+    attach_phases(op->upx, op->ph_x, st);
+    attach_phases(op->upy, op->ph_y, st);
     DBuf<double> dax, day;
     dax.upload(ax.data(), ax.size(), st);
     day.upload(ay.data(), ay.size(), st);
@@ -861,6 +880,22 @@ struct Session {
   DBuf<double> n2, part, hist;
   DBuf<int> flag;
   int chunks_M = 1, chunks_N = 1;
+  // one CGLS iteration captured as a CUDA graph (replayed on a private stream
+  // that is event-chained to the caller's stream); rebuilt if a buffer moved
+  cudaStream_t gst = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  long long graph_kernels = 0;
+  std::vector<const void*> graph_sig;
+  Session() = default;
+  Session(const Session&) = delete;
+  Session& operator=(const Session&) = delete;
+  ~Session() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (ev_in) cudaEventDestroy(ev_in);
+    if (ev_out) cudaEventDestroy(ev_out);
+    if (gst) cudaStreamDestroy(gst);
+  }
 };
 
 void norm2(Session& S, const cplx* v, int64_t len, int chunks, cudaStream_t st) {
@@ -925,10 +960,9 @@ void session_begin(Session& S, gs_op* op, const cplx* b_raw, bool b_perm, const 
 }
 
 // one CGLS iteration for every still-active problem (solver.cpp:70-88)
-void session_iterate(Session& S, cudaStream_t st) {
+void session_iterate_body(Session& S, cudaStream_t st) {
   gs_op* op = S.op;
   const int64_t TM = S.M * S.B, TN = S.Nc * S.B;
-  const int it = ++S.it;
   forward_dev(op, S.p.p, S.q.p, false, st);                          // q = T p
   norm2(S, S.q.p, S.M, S.chunks_M, st);                              // qq
   k_cg_alpha<<<nblk(S.B, 128), 128, 0, st>>>(S.st.p, S.n2.p, S.B);  // alpha (or stop)
@@ -939,12 +973,61 @@ void session_iterate(Session& S, cudaStream_t st) {
   pmark("k_axpy_r", st);
   adjoint_dev(op, S.r.p, S.s.p, false, st);                          // s = T* r
   norm2(S, S.s.p, S.Nc, S.chunks_N, st);                             // gamma'
-  k_cg_beta<<<nblk(S.B, 128), 128, 0, st>>>(S.st.p, S.n2.p, S.tol, it < S.hist_cap ? it : S.hist_cap - 1, S.hist.p,
-                                            S.hist_cap, S.B);
+  k_cg_beta<<<nblk(S.B, 128), 128, 0, st>>>(S.st.p, S.n2.p, S.tol, S.hist.p, S.hist_cap, S.B);
   pmark("k_cg_beta", st);
   k_pupdate<<<nblk(TN, 256), 256, 0, st>>>(S.p.p, S.s.p, S.Nc, S.B, S.st.p);  // p = s + beta p
   pmark("k_pupdate", st);
   CKL();
+}
+
+bool graphs_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("GS_B200_NO_GRAPHS");
+    return !(e && *e && *e != '0');
+  }();
+  return on;
+}
+
+// k iterations of solver.cpp:70-88 for every active problem, no host sync
+void session_iterate(Session& S, cudaStream_t st, int k) {
+  if (k <= 0) return;
+  S.it += k;
+  if (!graphs_enabled() || g_prof.on) {
+    for (int i = 0; i < k; ++i) session_iterate_body(S, st);
+    return;
+  }
+  uint64_t tol_bits = 0;
+  std::memcpy(&tol_bits, &S.tol, sizeof(tol_bits));
+  const std::vector<const void*> sig = {S.p.p, S.q.p, S.r.p, S.s.p, S.x.p, S.st.p, S.n2.p, S.hist.p, S.part.p,
+                                        reinterpret_cast<const void*>((intptr_t)S.hist_cap),
+                                        reinterpret_cast<const void*>((uintptr_t)tol_bits)};
+  if (S.gexec && (sig != S.graph_sig)) {
+    cudaGraphExecDestroy(S.gexec);
+    S.gexec = nullptr;
+  }
+  if (!S.gst) {
+    CK(cudaStreamCreateWithFlags(&S.gst, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&S.ev_in, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&S.ev_out, cudaEventDisableTiming));
+  }
+  if (!S.gexec) {
+    cudaGraph_t g = nullptr;
+    const long long n0 = g_launches.load();
+    CK(cudaStreamBeginCapture(S.gst, cudaStreamCaptureModeThreadLocal));
+    session_iterate_body(S, S.gst);
+    CK(cudaStreamEndCapture(S.gst, &g));
+    S.graph_kernels = g_launches.load() - n0;
+    g_launches.fetch_sub(S.graph_kernels);  // counted when replayed
+    CK(cudaGraphInstantiate(&S.gexec, g, 0));
+    CK(cudaGraphDestroy(g));
+    S.graph_sig = sig;
+  }
+  CK(cudaEventRecord(S.ev_in, st));
+  CK(cudaStreamWaitEvent(S.gst, S.ev_in, 0));
+  for (int i = 0; i < k; ++i) CK(cudaGraphLaunch(S.gexec, S.gst));
+  g_launches.fetch_add(S.graph_kernels * k);
+  CK(cudaEventRecord(S.ev_out, S.gst));
+  CK(cudaStreamWaitEvent(st, S.ev_out, 0));
 }
 
 bool session_any_active(Session& S, cudaStream_t st) {
@@ -1082,7 +1165,7 @@ int gs_cgls_step(gs_cgls_session* s, int iterations, void* stream) {
     if (!s) fail(GS_ERR_USAGE, "null session");
     std::lock_guard<std::mutex> lk(s->s.op->mu);
     CK(cudaSetDevice(s->s.op->device));
-    for (int i = 0; i < iterations; ++i) session_iterate(s->s, (cudaStream_t)stream);
+    session_iterate(s->s, (cudaStream_t)stream, iterations);
   });
 }
 

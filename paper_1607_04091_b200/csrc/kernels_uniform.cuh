@@ -15,6 +15,10 @@ struct UniP {
   int p, edges;   // family p, edges = p >= 2
   double eps;     // uniform_epsilon
   double phase_step;  // pi * eps * M / N  (nufft.cpp:412)
+  // phase tables built at construction (host libm, same arguments as the reference):
+  // ph_in[l] = e^{i phase_step l} (nufft.cpp:414), ph_out[m] = e^{i pi N xi_m} (nufft.cpp:427)
+  const cplx* ph_in;
+  const cplx* ph_out;
 };
 
 struct Strided {
@@ -38,7 +42,7 @@ __global__ void k_uni_fwd(UniP P, const cplx* __restrict__ x, Strided xs, const 
   for (int l = threadIdx.x; l < P.n; l += blockDim.x) {
     cplx v = x[l * xs.elem];
     if (P.edges && (l < P.p || l >= P.n - P.p)) v = mk(0, 0);  // freq2wave.cpp:224-230
-    cplx z = cmul(v, polar1(P.phase_step * (double)l));
+    cplx z = cmul(v, ldg2(P.ph_in + l));
     int pos = P.q * l;
     sm[pow2 ? bitrev(pos, P.logN2) : pos] = z;
   }
@@ -57,8 +61,7 @@ __global__ void k_uni_fwd(UniP P, const cplx* __restrict__ x, Strided xs, const 
       xt[c] = x[(P.n - P.p + c) * xs.elem];
     }
   for (int m = threadIdx.x; m < P.M; m += blockDim.x) {
-    double xi = P.eps / (double)P.n * ((double)m - (double)P.M / 2.0);
-    cplx o = cmul(polar1(GS_PI * (double)P.n * xi), Z[m]);
+    cplx o = cmul(ldg2(P.ph_out + m), Z[m]);
     const cplx* r = rec + (int64_t)m * R;
     cplx ym = cmul(r[0], o);
     if (P.edges) {
@@ -95,8 +98,7 @@ __global__ void k_uni_adj(UniP P, const cplx* __restrict__ y, Strided ys, const 
     if (pre) u = cscale(u, pre[m * ys.elem]);
     const cplx* r = rec + (int64_t)m * R;
     cplx v = cmul(conj_(r[0]), u);  // freq2wave.cpp:315
-    double xi = P.eps / (double)P.n * ((double)m - (double)P.M / 2.0);
-    cplx val = cmul(v, polar1(-GS_PI * (double)P.n * xi));  // nufft.cpp:443-445
+    cplx val = cmul(v, conj_(ldg2(P.ph_out + m)));  // e^{-i pi N xi_m}, nufft.cpp:443-445
     sm[pow2 ? bitrev(m, P.logN2) : m] = val;
     if (P.edges)
       for (int c = 0; c < P.p; ++c) {
@@ -113,7 +115,7 @@ __global__ void k_uni_adj(UniP P, const cplx* __restrict__ y, Strided ys, const 
     Z = sm + P.N2;
   }
   for (int l = threadIdx.x; l < P.n; l += blockDim.x) {
-    cplx v = cmul(Z[P.q * l], polar1(-P.phase_step * (double)l));
+    cplx v = cmul(Z[P.q * l], conj_(ldg2(P.ph_in + l)));
     if (P.edges && (l < P.p || l >= P.n - P.p)) v = mk(0, 0);  // freq2wave.cpp:318-321
     z[l * zs.elem] = v;
   }

@@ -129,17 +129,20 @@ __global__ void k_cg_alpha(CgState* st, const double* __restrict__ n2, int B) {
 }
 
 // gamma' = ||s||^2; history; tolerance; beta  (solver.cpp:77-87)
-__global__ void k_cg_beta(CgState* st, const double* __restrict__ n2, double tol, int it, double* hist, int hist_stride,
+// (the iteration number lives on the device, so one captured CUDA graph replays
+// every iteration)
+__global__ void k_cg_beta(CgState* st, const double* __restrict__ n2, double tol, double* hist, int hist_stride,
                           int B) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   CgState s = st[b];
   if (!s.active) return;
   double gn = n2[b];
+  const int it = s.iterations + 1;
   s.iterations = it;
   double h = sqrt(gn) / s.ref;
-  if (hist) hist[(int64_t)b * hist_stride + it] = h;
-  s.hist_len = it + 1;
+  if (hist) hist[(int64_t)b * hist_stride + (it < hist_stride ? it : hist_stride - 1)] = h;
+  s.hist_len = (it < hist_stride ? it : hist_stride - 1) + 1;
   if (h <= tol) {
     s.converged = 1;
     s.active = 0;
