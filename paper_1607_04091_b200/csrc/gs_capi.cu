@@ -212,6 +212,8 @@ struct gs_op {
   bool fast2d = false;  // kernels_nfft2d_fast.cuh path (w = 6, p <= 4)
   int cap = 1;          // chunk capacity per problem (2D work list)
   DBuf<int> ch_tile, ch_s0, ch_s1, ch_count, tcs;
+  DBuf<unsigned> units;  // fast 2D interpolation work units (k2f_build_units)
+  DBuf<int> ucount;
   DBuf<double> wts_x, wts_y;
   DBuf<cplx> rec_x, rec_y;
   DBuf<double> sqrtw;  // internal order ([B][M]) or empty
@@ -642,6 +644,15 @@ gs_op* create(const gs_op_desc* dsc) {
       op->ch_s1.upload(h_1.data(), h_1.size(), st);
       op->ch_count.upload(h_n.data(), h_n.size(), st);
       op->tcs.upload(tcs.data(), tcs.size(), st);
+      if (op->fast2d) {
+        op->units.alloc(total);
+        op->ucount.alloc((size_t)B * cap);
+        k2f_build_units<<<nblk((int64_t)B * cap, 128), 128, 0, st>>>(op->ch_tile.p, op->ch_s0.p, op->ch_s1.p,
+                                                                     op->ch_count.p, cap, (int)B, (int)M, P.nt,
+                                                                     op->base_x.p, op->base_y.p,
+                                                                     op->units.p, op->ucount.p);
+        CKL();
+      }
       op->G.alloc((size_t)B * n_ov * n_ov);
       op->TB.alloc((size_t)B * cap * P.R * P.R);
       if (op->edges) {
@@ -736,9 +747,9 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
         const dim3 grid(op->cap, B);
         const int* pp = perm_io ? op->perm.p : nullptr;
 #define GS_F_INTERP(PP)                                                                                            \
-  k2f_interp<PP><<<grid, 128, 2 * (F_CHUNK * F_S + 2) * sizeof(double), st>>>(                                    \
-      P, op->ch_tile.p, op->ch_s0.p, op->ch_s1.p, op->ch_count.p, op->cap, op->base_x.p, op->base_y.p, op->wts_x.p,  \
-      op->wts_y.p, op->rec_x.p, op->rec_y.p, op->G.p, op->lines.p, x, pp, y)
+  k2f_interp<PP><<<grid, F_ITHREADS, FInterp<PP>::bytes(), st>>>(                                    \
+      P, op->ch_tile.p, op->ch_s0.p, op->ch_s1.p, op->ch_count.p, op->cap, op->units.p, op->ucount.p, op->base_x.p, \
+      op->base_y.p, op->wts_x.p, op->wts_y.p, op->rec_x.p, op->rec_y.p, op->G.p, op->lines.p, x, pp, y)
         switch (op->p) {
           case 1: GS_F_INTERP(1); break;
           case 2: GS_F_INTERP(2); break;

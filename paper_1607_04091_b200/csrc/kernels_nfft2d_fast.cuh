@@ -2,222 +2,29 @@
 // Kaiser-Bessel window (w = 6, S = 13 taps) and p <= 4 (haar .. db4):
 //
 //  * samples are bin-sorted by 12x12 grid tile and, inside a tile, by cell
-//    (row-major); the work list is (tile, chunk of <= 512 samples) so dense
+//    (row-major); the work list is (tile, chunk of <= F_CHUNK samples) so dense
 //    tiles (the spiral's centre) split across CTAs;
 //  * k2f_interp  -- one CTA per chunk stages the tile's (T+12)^2 grid region,
 //    its 2 x 2p side-line segments and the 4 p x p corner blocks in shared
-//    memory once, then one thread per sample interpolates from shared memory
+//    memory once, then one thread per work unit (a pair of neighbouring
+//    samples of one cell row, or a single sample) interpolates from shared
+//    memory, loading each row window once for both samples
 //    (nufft.cpp:287-303 + freq2wave.cpp:255-301);
 //  * k2f_spread  -- output-stationary in registers: lane c < 24 owns grid
-//    column c of the 24-row region (24 complex accumulators) and the 2p
-//    x-line entries at column c, lanes 24..31 own the 2p y-lines.  A warp
-//    takes whole sample rows of the chunk, so the row offset of every rank-1
-//    update is a compile-time constant (12 instantiations) and all register
-//    indices are static.  The 4 warps' copies are folded once per chunk and
-//    written with no atomics (transpose of the interpolation,
-//    nufft.cpp:324-338 + freq2wave.cpp:332-385).
+//    column c, lanes 24..31 own the 2p y-lines, and warp w owns the band of
+//    F_BAND sample rows of the tile, so its accumulators span F_BAND + 12 rows
+//    (plus the 2p x-line entries at column c).  Every rank-1 update has a
+//    compile-time row offset, the sample pairs are software-pipelined, and the
+//    4 warps' bands are folded once per chunk and written with no atomics
+//    (transpose of the interpolation, nufft.cpp:324-338 + freq2wave.cpp:332-385).
 #pragma once
+#include <type_traits>
 #include "kernels_nfft.cuh"
 
 #define F_S 13
 #define F_T 12
 #define F_R 24
 #define F_CHUNK 160  // samples per work item (chunks of a tile are staged in shared memory)
-
-// ------------------------------------------------------------------ interpolation
-template <int P>
-__global__ void __launch_bounds__(128, 3) k2f_interp(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ ch_s0,
-                                                     const int* __restrict__ ch_s1, const int* __restrict__ ch_count,
-                                                     int cap, const int* __restrict__ base_x, const int* __restrict__ base_y,
-                                                     const double* __restrict__ wx_all, const double* __restrict__ wy_all,
-                                                     const cplx* __restrict__ recx_all, const cplx* __restrict__ recy_all,
-                                                     const cplx* __restrict__ G, const cplx* __restrict__ lines,
-                                                     const cplx* __restrict__ x, const int* __restrict__ out_perm,
-                                                     cplx* __restrict__ y) {
-  constexpr int S = F_S, T = F_T, R = F_R;
-  constexpr int E = P >= 2 ? 2 * P : 0;
-  constexpr int EE = E > 0 ? E : 1;
-  constexpr int RR = 1 + E;
-  constexpr int NC = P >= 2 ? 4 * P * P : 1;
-  constexpr int RS = R + 1;  // padded row stride: rows 384 B apart would alias the same banks
-  __shared__ cplx reg[R * RS];
-  __shared__ cplx ly[EE][R];
-  __shared__ cplx lx[EE][R];
-  __shared__ cplx cx[NC];
-  const int prob = blockIdx.y, c = blockIdx.x;
-  if (c >= ch_count[prob]) return;
-  const int tile = ch_tile[prob * cap + c], s0 = ch_s0[prob * cap + c], s1 = ch_s1[prob * cap + c];
-  const int ty = tile / Pp.nt, tx = tile - ty * Pp.nt;
-  const int n_ov = Pp.n_ov, mask = n_ov - 1, n = Pp.n;
-  const cplx* g = G + (int64_t)prob * n_ov * n_ov;
-  // asynchronous 16-B copies (cp.async): all of the tile's staging is in flight at once
-  auto cp16 = [](cplx* dst, const cplx* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
-                     static_cast<unsigned>(__cvta_generic_to_shared(dst))),
-                 "l"(src)
-                 : "memory");
-  };
-  for (int i = threadIdx.x; i < R * R; i += blockDim.x) {
-    const int r = i / R, cc = i - r * R;
-    cp16(reg + r * RS + cc, g + (int64_t)((ty * T + r) & mask) * n_ov + ((tx * T + cc) & mask));
-  }
-  if (E > 0) {
-    const cplx* LY = lines + (int64_t)prob * 2 * E * n_ov;
-    const cplx* LX = LY + (int64_t)E * n_ov;
-    for (int i = threadIdx.x; i < E * R; i += blockDim.x) {
-      const int e = i / R, r = i - e * R;
-      cp16(&ly[e][r], LY + (int64_t)e * n_ov + ((ty * T + r) & mask));
-      cp16(&lx[e][r], LX + (int64_t)e * n_ov + ((tx * T + r) & mask));
-    }
-    const cplx* X = x + (int64_t)prob * n * n;
-    for (int q = threadIdx.x; q < 4 * P * P; q += blockDim.x) {
-      const int k = q / (P * P), rem = q - k * P * P, i = rem / P, j = rem - i * P;
-      const int row0 = (k < 2) ? 0 : n - P, col0 = (k % 2 == 0) ? 0 : n - P;
-      cp16(cx + q, X + (int64_t)(col0 + j) * n + row0 + i);
-    }
-  }
-  // the chunk's window weights (contiguous ranges, staged 16-B aligned-down)
-  const int64_t g0 = (int64_t)prob * Pp.M + s0;
-  const int nn = s1 - s0;
-  auto stage = [&](double* dst, const double* src, int count) -> const double* {
-    const uintptr_t a = reinterpret_cast<uintptr_t>(src), al = a & ~uintptr_t(15);
-    const int off = (int)(a - al), nv = (off + count * 8 + 15) / 16;
-    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-    for (int i = threadIdx.x; i < nv; i += blockDim.x)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d + 16u * i),
-                   "l"(reinterpret_cast<const char*>(al) + 16 * i)
-                   : "memory");
-    return reinterpret_cast<const double*>(reinterpret_cast<const char*>(dst) + off);
-  };
-  extern __shared__ __align__(16) double fi_dyn[];  // [2][F_CHUNK * S + 2]
-  double* swy = fi_dyn;
-  double* swx = fi_dyn + F_CHUNK * S + 2;
-  const double* wys = stage(swy, wy_all + g0 * S, nn * S);
-  const double* wxs = stage(swx, wx_all + g0 * S, nn * S);
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
-  __syncthreads();
-  for (int s = s0 + threadIdx.x; s < s1; s += blockDim.x) {
-    const int64_t gs = (int64_t)prob * Pp.M + s;
-    const int oy = base_y[gs] - ty * T, ox = base_x[gs] - tx * T;
-    const double* wyp = wys + (s - s0) * S;
-    const double* wxp = wxs + (s - s0) * S;
-    const cplx* rx = recx_all + gs * RR;
-    const cplx* ry = recy_all + gs * RR;
-    const cplx Dx = ldg2(rx), Dy = ldg2(ry);
-    // out = Dx Dy acc + Dx (b . ux) + a^T (C b + Dy uy): interior (freq2wave.cpp:255),
-    // the 4 corner blocks C (260-270) and both side families (272-301), with
-    // a = [Lx|Rx](m,:), b = [Ly|Ry](m,:)
-    cplx bv[EE];
-#pragma unroll
-    for (int e = 0; e < E; ++e) bv[e] = ldg2(ry + 1 + e);
-    cplx out;
-    {
-      double wx[S];
-#pragma unroll
-      for (int t = 0; t < S; ++t) wx[t] = wxp[t];
-      cplx acc = mk(0, 0);
-#pragma unroll
-      for (int t0 = 0; t0 < S; ++t0) {
-        const cplx* row = reg + (oy + t0) * RS + ox;
-        cplx ra = mk(0, 0);
-#pragma unroll
-        for (int t1 = 0; t1 < S; ++t1) ra = caxpy(ra, wx[t1], row[t1]);
-        acc = caxpy(acc, wyp[t0], ra);
-      }
-      out = cmul(cmul(Dx, Dy), acc);
-      if (E > 0) {
-        cplx sx = mk(0, 0);
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          cplx u = mk(0, 0);
-#pragma unroll
-          for (int t = 0; t < S; ++t) u = caxpy(u, wx[t], lx[e][ox + t]);
-          sx = cadd(sx, cmul(bv[e], u));
-        }
-        out = cadd(out, cmul(Dx, sx));
-      }
-    }
-    if (E > 0) {
-      double wy[S];
-#pragma unroll
-      for (int t = 0; t < S; ++t) wy[t] = wyp[t];
-#pragma unroll
-      for (int i = 0; i < E; ++i) {
-        const int hi = i < P ? 0 : 1, ii = i - hi * P;
-        cplx u = mk(0, 0);
-#pragma unroll
-        for (int t = 0; t < S; ++t) u = caxpy(u, wy[t], ly[i][oy + t]);
-        cplx v = cmul(Dy, u);
-#pragma unroll
-        for (int j = 0; j < E; ++j) {
-          const int hj = j < P ? 0 : 1, jj = j - hj * P;
-          v = cadd(v, cmul(cx[(2 * hi + hj) * P * P + ii * P + jj], bv[j]));
-        }
-        out = cadd(out, cmul(ldg2(rx + 1 + i), v));
-      }
-    }
-    const int64_t o = out_perm ? (int64_t)out_perm[gs] : s;
-    y[(int64_t)prob * Pp.M + o] = out;
-  }
-}
-
-// ------------------------------------------------------------------ spreading
-#define F_WARPS 4
-
-template <int P>
-struct FSpread {
-  static constexpr int E = P >= 2 ? 2 * P : 0;
-  static constexpr int EE = E > 0 ? E : 1;
-  static constexpr int RR = 1 + E;
-  static constexpr int NCE = P >= 2 ? 4 * P * P : 0;
-  static constexpr int NCU = NCE > 0 ? (NCE + 31) / 32 : 1;
-  static constexpr int PER_WARP = F_R * F_R + 2 * E * F_R;  // region + y-lines + x-lines
-  // staged chunk (structure of arrays, in sample order)
-  // each staged array gets 16 B of slack: copies start at the 16-B-aligned address below
-  static constexpr size_t STG_WY = 0;
-  static constexpr size_t STG_WX = STG_WY + sizeof(double) * F_CHUNK * F_S + 32;
-  static constexpr size_t STG_RX = STG_WX + sizeof(double) * F_CHUNK * F_S + 32;
-  static constexpr size_t STG_RY = STG_RX + sizeof(cplx) * F_CHUNK * RR + 16;
-  static constexpr size_t STG_YS = STG_RY + sizeof(cplx) * F_CHUNK * RR + 16;
-  static constexpr size_t STG_OX = STG_YS + sizeof(cplx) * F_CHUNK;
-  static constexpr size_t STG_END = STG_OX + sizeof(int) * F_CHUNK;
-  static constexpr size_t FOLD = sizeof(cplx) * (F_WARPS * PER_WARP + F_WARPS * (NCE > 0 ? NCE : 1));
-  static constexpr size_t MAIN = (STG_END > FOLD ? STG_END : FOLD);  // fold buffer aliases the staging
-  struct Scratch {  // derived per-sample values shared inside a warp (two samples in flight)
-    cplx d[2][32];
-    double2 wy[16];  // row taps of the two samples, packed (wy_a[t], wy_b[t])
-  };
-  static constexpr size_t bytes() { return (MAIN + 15) / 16 * 16 + sizeof(Scratch) * F_WARPS; }
-};
-
-// acc[OY + t] += w[t].x u0 + w[t].y u1, t < 13 (w = the two samples' row taps,
-// packed pairwise), with OY a compile-time row offset
-template <int OY>
-__device__ __forceinline__ void f_upd(cplx (&acc)[F_R], cplx u0, cplx u1, const double2* w) {
-#pragma unroll
-  for (int t = 0; t < F_S; ++t) {
-    const double2 ww = w[t];
-    acc[OY + t].x = fma(ww.y, u1.x, fma(ww.x, u0.x, acc[OY + t].x));
-    acc[OY + t].y = fma(ww.y, u1.y, fma(ww.x, u0.y, acc[OY + t].y));
-  }
-}
-__device__ __forceinline__ void f_upd_dispatch(int oy, cplx (&acc)[F_R], cplx u0, cplx u1, const double2* w) {
-  switch (oy) {
-    case 0: f_upd<0>(acc, u0, u1, w); break;
-    case 1: f_upd<1>(acc, u0, u1, w); break;
-    case 2: f_upd<2>(acc, u0, u1, w); break;
-    case 3: f_upd<3>(acc, u0, u1, w); break;
-    case 4: f_upd<4>(acc, u0, u1, w); break;
-    case 5: f_upd<5>(acc, u0, u1, w); break;
-    case 6: f_upd<6>(acc, u0, u1, w); break;
-    case 7: f_upd<7>(acc, u0, u1, w); break;
-    case 8: f_upd<8>(acc, u0, u1, w); break;
-    case 9: f_upd<9>(acc, u0, u1, w); break;
-    case 10: f_upd<10>(acc, u0, u1, w); break;
-    case 11: f_upd<11>(acc, u0, u1, w); break;
-    default: __builtin_unreachable();
-  }
-}
 
 // cooperative 16-byte copy of [src, src + bytes) global -> shared; the copy starts
 // at the aligned address below src, the returned pointer is src's image
@@ -234,6 +41,326 @@ __device__ __forceinline__ unsigned char* f_stage(unsigned char* dst, const void
 }
 __device__ __forceinline__ void f_stage_wait() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
+// ------------------------------------------------------------------ interpolation
+// Work units of the interpolation: a chunk's samples are walked in sorted order
+// and consecutive samples in the same cell row whose columns differ by at most
+// F_PD are fused into one unit, so the unit loads each grid row / side-line
+// window once (F_W = 13 + F_PD entries) for both samples.  Everything else is a
+// single-sample unit (second slot 0xffff).  Built once per operator; units of
+// chunk (prob, c) are stored from the chunk's first sample index on.
+#define F_PD 3
+#define F_W (F_S + F_PD)
+// Shared-memory column map of the staged region and x-lines: column c lives at
+// f(c) = c + c/2.  Unit windows start at even columns ws in {0, 2, .., 8}, so
+// f(ws + j) = f(ws) + f(j) (constant offsets per tap) and f(ws) mod 8 =
+// {0, 3, 6, 1, 4} puts the quarter-warp's windows in distinct 16-B bank groups;
+// the row stride 39 (= 7 mod 8) keeps the next cell row's windows apart too.
+#define F_RS2 39
+// interpolation CTA shape (measured on C5: 4 warps x 3 CTAs/SM beat 3 x 4 and
+// 2 x 4; the factor records are read through L1, which a larger shared-memory
+// carve-out would shrink)
+#ifndef F_ITHREADS
+#define F_ITHREADS 128
+#define F_IBLOCKS 3
+#endif
+#ifndef F_IUNROLL
+#define F_IUNROLL 2  // unroll of the interpolation row / line loops
+#endif
+__host__ __device__ constexpr int f_col(int c) { return c + (c >> 1); }
+
+__global__ void k2f_build_units(const int* __restrict__ ch_tile, const int* __restrict__ ch_s0,
+                                const int* __restrict__ ch_s1, const int* __restrict__ ch_count, int cap, int B, int M, int nt,
+                                const int* __restrict__ base_x, const int* __restrict__ base_y,
+                                unsigned* __restrict__ units, int* __restrict__ ucount) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)B * cap) return;
+  const int prob = (int)(i / cap), c = (int)(i - (int64_t)prob * cap);
+  if (c >= ch_count[prob]) {
+    ucount[i] = 0;
+    return;
+  }
+  const int s0 = ch_s0[i], s1 = ch_s1[i];
+  const int tx0 = (ch_tile[i] % nt) * F_T;
+  const int64_t g0 = (int64_t)prob * M;
+  unsigned* U = units + g0 + s0;
+  int k = 0;
+  for (int s = s0; s < s1; ++k) {
+    const int by = base_y[g0 + s], bx = base_x[g0 + s];
+    // window start of the unit: even column, at most R - W (see f_col)
+    const int ws = min((bx - tx0) & ~1, F_R - F_W) + tx0;
+    if (s + 1 < s1 && base_y[g0 + s + 1] == by && base_x[g0 + s + 1] >= bx && base_x[g0 + s + 1] - ws <= F_PD) {
+      U[k] = (unsigned)(s - s0) | ((unsigned)(s + 1 - s0) << 16);
+      s += 2;
+    } else {
+      U[k] = (unsigned)(s - s0) | (0xffffu << 16);
+      s += 1;
+    }
+  }
+  ucount[i] = k;
+}
+
+// dynamic shared memory of k2f_interp: the chunk's staged weights and records
+template <int P>
+struct FInterp {
+  static constexpr int RR = 1 + (P >= 2 ? 2 * P : 0);
+  static constexpr size_t WY = 0;
+  static constexpr size_t WX = WY + sizeof(double) * F_CHUNK * F_S + 32;
+  static constexpr size_t RX = WX + sizeof(double) * F_CHUNK * F_S + 32;
+  static constexpr size_t RY = RX + sizeof(cplx) * F_CHUNK * RR + 16;
+  static constexpr size_t bytes() { return RX; }  // records are read through L1 (RX, RY: unused)
+};
+
+template <int P>
+__global__ void __launch_bounds__(F_ITHREADS, F_IBLOCKS) k2f_interp(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ ch_s0,
+                                                     const int* __restrict__ ch_s1, const int* __restrict__ ch_count,
+                                                     int cap, const unsigned* __restrict__ units,
+                                                     const int* __restrict__ ucount, const int* __restrict__ base_x,
+                                                     const int* __restrict__ base_y, const double* __restrict__ wx_all,
+                                                     const double* __restrict__ wy_all, const cplx* __restrict__ recx_all,
+                                                     const cplx* __restrict__ recy_all, const cplx* __restrict__ G,
+                                                     const cplx* __restrict__ lines, const cplx* __restrict__ x,
+                                                     const int* __restrict__ out_perm, cplx* __restrict__ y) {
+  constexpr int S = F_S, T = F_T, R = F_R, W = F_W, IU = F_IUNROLL;
+  constexpr int E = P >= 2 ? 2 * P : 0;
+  constexpr int EE = E > 0 ? E : 1;
+  constexpr int RR = 1 + E;
+  constexpr int NC = P >= 2 ? 4 * P * P : 1;
+  constexpr int RS = F_RS2;  // row stride of the column-mapped region (f_col)
+  constexpr int LX = f_col(R - 1) + 1;
+  __shared__ cplx reg[R * RS];
+  __shared__ cplx ly[EE][R];
+  __shared__ cplx lx[EE][LX];
+  __shared__ cplx cx[NC];
+  const int prob = blockIdx.y, c = blockIdx.x;
+  if (c >= ch_count[prob]) return;
+  const int64_t chunk = (int64_t)prob * cap + c;
+  const int tile = ch_tile[chunk], s0 = ch_s0[chunk], s1 = ch_s1[chunk];
+  const int ty = tile / Pp.nt, tx = tile - ty * Pp.nt;
+  const int n_ov = Pp.n_ov, mask = n_ov - 1, n = Pp.n;
+  const cplx* g = G + (int64_t)prob * n_ov * n_ov;
+  // asynchronous 16-B copies (cp.async): all of the tile's staging is in flight at once
+  auto cp16 = [](cplx* dst, const cplx* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
+                     static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+  };
+  for (int i = threadIdx.x; i < R * R; i += blockDim.x) {
+    const int r = i / R, cc = i - r * R;
+    cp16(reg + r * RS + f_col(cc), g + (int64_t)((ty * T + r) & mask) * n_ov + ((tx * T + cc) & mask));
+  }
+  if (E > 0) {
+    const cplx* LY = lines + (int64_t)prob * 2 * E * n_ov;
+    const cplx* LX = LY + (int64_t)E * n_ov;
+    for (int i = threadIdx.x; i < E * R; i += blockDim.x) {
+      const int e = i / R, r = i - e * R;
+      cp16(&ly[e][r], LY + (int64_t)e * n_ov + ((ty * T + r) & mask));
+      cp16(&lx[e][f_col(r)], LX + (int64_t)e * n_ov + ((tx * T + r) & mask));
+    }
+    const cplx* X = x + (int64_t)prob * n * n;
+    for (int q = threadIdx.x; q < 4 * P * P; q += blockDim.x) {
+      const int k = q / (P * P), rem = q - k * P * P, i = rem / P, j = rem - i * P;
+      const int row0 = (k < 2) ? 0 : n - P, col0 = (k % 2 == 0) ? 0 : n - P;
+      cp16(cx + q, X + (int64_t)(col0 + j) * n + row0 + i);
+    }
+  }
+  // the chunk's window weights (contiguous ranges, staged 16-B aligned-down;
+  // layout FInterp<P>)
+  const int64_t g0 = (int64_t)prob * Pp.M + s0;
+  const int nn = s1 - s0;
+  extern __shared__ __align__(16) unsigned char fi_dyn[];
+  using FI = FInterp<P>;
+  const double* wys = reinterpret_cast<const double*>(f_stage(fi_dyn + FI::WY, wy_all + g0 * S, sizeof(double) * S * nn));
+  const double* wxs = reinterpret_cast<const double*>(f_stage(fi_dyn + FI::WX, wx_all + g0 * S, sizeof(double) * S * nn));
+  f_stage_wait();
+  __syncthreads();
+  const unsigned* U = units + g0;
+  const int nu = ucount[chunk];
+  for (int k = threadIdx.x; k < nu; k += blockDim.x) {
+    const unsigned uv = U[k];
+    const int la = (int)(uv & 0xffffu), lr = (int)(uv >> 16);
+    const bool two = lr != 0xffff;
+    const int lb = two ? lr : la;
+    const int64_t ga = g0 + la, gb = g0 + lb;
+    const int oy = base_y[ga] - ty * T;
+    const int oxa = base_x[ga] - tx * T, oxb = base_x[gb] - tx * T;
+    const int ws = min(oxa & ~1, R - W);  // shared even column window [ws, ws + W) inside the region
+    const int da = oxa - ws, db = oxb - ws;
+    // column taps of both samples on the shared window (zero outside each sample's support)
+    double wa[W], wb[W];
+    const double* wxa = wxs + la * S;
+    const double* wxb = wxs + lb * S;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      const int ja = j - da, jb = j - db;
+      const double va = wxa[ja < 0 ? 0 : (ja >= S ? S - 1 : ja)];
+      const double vb = wxb[jb < 0 ? 0 : (jb >= S ? S - 1 : jb)];
+      wa[j] = (ja >= 0 && ja < S) ? va : 0.0;
+      wb[j] = (two && jb >= 0 && jb < S) ? vb : 0.0;
+    }
+    const double* wya = wys + la * S;
+    const double* wyb = wys + lb * S;
+    const cplx* rxa = recx_all + ga * RR;
+    const cplx* rxb = recx_all + gb * RR;
+    const cplx* rya = recy_all + ga * RR;
+    const cplx* ryb = recy_all + gb * RR;
+    // out = Dx Dy acc + Dx (b . ux) + a^T (C b + Dy uy): interior (freq2wave.cpp:255),
+    // the 4 corner blocks C (260-270) and both side families (272-301), with
+    // a = [Lx|Rx](m,:), b = [Ly|Ry](m,:)
+    cplx outa, outb;
+    {
+      cplx acca = mk(0, 0), accb = mk(0, 0);
+#pragma unroll IU
+      for (int t0 = 0; t0 < S; ++t0) {
+        const cplx* row = reg + (oy + t0) * RS + f_col(ws);
+        cplx ra[2] = {mk(0, 0), mk(0, 0)}, rb[2] = {mk(0, 0), mk(0, 0)};  // even / odd taps: shorter chains
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+          const cplx v = row[f_col(j)];
+          ra[j & 1] = caxpy(ra[j & 1], wa[j], v);
+          rb[j & 1] = caxpy(rb[j & 1], wb[j], v);
+        }
+        acca = caxpy(acca, wya[t0], cadd(ra[0], ra[1]));
+        accb = caxpy(accb, wyb[t0], cadd(rb[0], rb[1]));
+      }
+      const cplx Dxa = ldg2(rxa), Dxb = ldg2(rxb);
+      outa = cmul(cmul(Dxa, ldg2(rya)), acca);
+      outb = cmul(cmul(Dxb, ldg2(ryb)), accb);
+      if (E > 0) {
+        cplx sxa = mk(0, 0), sxb = mk(0, 0);
+#pragma unroll IU
+        for (int e = 0; e < E; ++e) {
+          cplx ua[2] = {mk(0, 0), mk(0, 0)}, ub[2] = {mk(0, 0), mk(0, 0)};
+#pragma unroll
+          for (int j = 0; j < W; ++j) {
+            const cplx v = lx[e][f_col(ws) + f_col(j)];
+            ua[j & 1] = caxpy(ua[j & 1], wa[j], v);
+            ub[j & 1] = caxpy(ub[j & 1], wb[j], v);
+          }
+          sxa = cadd(sxa, cmul(ldg2(rya + 1 + e), cadd(ua[0], ua[1])));
+          sxb = cadd(sxb, cmul(ldg2(ryb + 1 + e), cadd(ub[0], ub[1])));
+        }
+        outa = cadd(outa, cmul(Dxa, sxa));
+        outb = cadd(outb, cmul(Dxb, sxb));
+      }
+    }
+    if (E > 0) {
+      // side y-lines: Dy sum_i a_i uy_i, both samples sharing the line loads
+      // (freq2wave.cpp:287-301)
+      double ta[S], tb[S];
+#pragma unroll
+      for (int t = 0; t < S; ++t) {
+        ta[t] = wya[t];
+        tb[t] = wyb[t];
+      }
+      cplx sya = mk(0, 0), syb = mk(0, 0);
+#pragma unroll IU
+      for (int i = 0; i < E; ++i) {
+        cplx ua[2] = {mk(0, 0), mk(0, 0)}, ub[2] = {mk(0, 0), mk(0, 0)};
+#pragma unroll
+        for (int t = 0; t < S; ++t) {
+          const cplx v = ly[i][oy + t];
+          ua[t & 1] = caxpy(ua[t & 1], ta[t], v);
+          ub[t & 1] = caxpy(ub[t & 1], tb[t], v);
+        }
+        sya = cadd(sya, cmul(ldg2(rxa + 1 + i), cadd(ua[0], ua[1])));
+        syb = cadd(syb, cmul(ldg2(rxb + 1 + i), cadd(ub[0], ub[1])));
+      }
+      outa = cadd(outa, cmul(ldg2(rya), sya));
+      outb = cadd(outb, cmul(ldg2(ryb), syb));
+      // corners a^T C b of both samples, each C entry loaded once (freq2wave.cpp:260-270)
+      cplx bva[EE], bvb[EE];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        bva[e] = ldg2(rya + 1 + e);
+        bvb[e] = ldg2(ryb + 1 + e);
+      }
+      cplx oa = mk(0, 0), ob = mk(0, 0);
+#pragma unroll 1
+      for (int i = 0; i < E; ++i) {
+        const int hi = i < P ? 0 : 1, ii = i - hi * P;
+        cplx va = mk(0, 0), vb = mk(0, 0);
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+          const int hj = j < P ? 0 : 1, jj = j - hj * P;
+          const cplx cc = cx[(2 * hi + hj) * P * P + ii * P + jj];
+          va = cadd(va, cmul(cc, bva[j]));
+          vb = cadd(vb, cmul(cc, bvb[j]));
+        }
+        oa = cadd(oa, cmul(ldg2(rxa + 1 + i), va));
+        ob = cadd(ob, cmul(ldg2(rxb + 1 + i), vb));
+      }
+      outa = cadd(outa, oa);
+      outb = cadd(outb, ob);
+    }
+    const int64_t base = (int64_t)prob * Pp.M;
+    y[base + (out_perm ? (int64_t)out_perm[ga] : (int64_t)(s0 + la))] = outa;
+    if (two) y[base + (out_perm ? (int64_t)out_perm[gb] : (int64_t)(s0 + lb))] = outb;
+  }
+}
+
+// ------------------------------------------------------------------ spreading
+#ifndef F_WARPS
+#define F_WARPS 4
+#endif
+#define F_BAND (F_T / F_WARPS)   // sample rows of a tile per warp
+#define F_AR (F_BAND - 1 + F_S)  // accumulator rows a warp's band touches
+
+// compile-time loop: f(integral_constant<int, K>) for K in [K0, N)
+template <int K0, int N, class Fn>
+__device__ __forceinline__ void f_static_for(Fn&& f) {
+  if constexpr (K0 < N) {
+    f(std::integral_constant<int, K0>{});
+    f_static_for<K0 + 1, N>(f);
+  }
+}
+
+template <int P>
+struct FSpread {
+  static constexpr int E = P >= 2 ? 2 * P : 0;
+  static constexpr int EE = E > 0 ? E : 1;
+  static constexpr int RR = 1 + E;
+  static constexpr int NCE = P >= 2 ? 4 * P * P : 0;
+  static constexpr int NCU = NCE > 0 ? (NCE + 31) / 32 : 1;
+  // per-warp fold record: band region + band of the y-lines + x-lines
+  static constexpr int PER_WARP = F_AR * F_R + E * F_AR + E * F_R;
+  // staged chunk (structure of arrays, in sample order)
+  // each staged array gets 16 B of slack: copies start at the 16-B-aligned address below
+  static constexpr size_t STG_WY = 0;
+  static constexpr size_t STG_WX = STG_WY + sizeof(double) * F_CHUNK * F_S + 32;
+  static constexpr size_t STG_RX = STG_WX + sizeof(double) * F_CHUNK * F_S + 32;
+  static constexpr size_t STG_RY = STG_RX + sizeof(cplx) * F_CHUNK * RR + 16;
+  static constexpr size_t STG_YS = STG_RY + sizeof(cplx) * F_CHUNK * RR + 16;
+  static constexpr size_t STG_OX = STG_YS + sizeof(cplx) * F_CHUNK;
+  static constexpr size_t STG_END = STG_OX + sizeof(int) * F_CHUNK;
+  static constexpr size_t FOLD = sizeof(cplx) * (F_WARPS * PER_WARP + F_WARPS * (NCE > 0 ? NCE : 1));
+  static constexpr size_t MAIN = (STG_END > FOLD ? STG_END : FOLD);  // fold buffer aliases the staging
+  struct Scratch {  // derived per-sample values of one sample pair, shared inside a warp
+    cplx d[2][32];
+    double2 wy[16];  // row taps of the two samples, packed (wy_a[t], wy_b[t])
+  };
+  // two scratch buffers per warp: the next pair is derived while the current one updates
+  static constexpr size_t bytes() { return (MAIN + 15) / 16 * 16 + sizeof(Scratch) * 2 * F_WARPS; }
+};
+
+// acc[OY + t] += w[t].x u0 + w[t].y u1, t < 13 (w = the two samples' row taps,
+// packed pairwise), with OY a compile-time row offset inside the warp's band
+template <int OY>
+__device__ __forceinline__ void f_upd(cplx (&acc)[F_AR], cplx u0, cplx u1, const double2* w) {
+#pragma unroll
+  for (int t = 0; t < F_S; ++t) {
+    const double2 ww = w[t];
+    acc[OY + t].x = fma(ww.y, u1.x, fma(ww.x, u0.x, acc[OY + t].x));
+    acc[OY + t].y = fma(ww.y, u1.y, fma(ww.x, u0.y, acc[OY + t].y));
+  }
+}
+
+
+// Warp w owns the F_BAND sample rows [w F_BAND, (w+1) F_BAND) of the tile, so its
+// register accumulators span only F_AR rows and every row offset is a
+// compile-time constant (one specialised loop per band row, no dispatch).  Pairs
+// of samples are software-pipelined: the next pair's derived values are loaded
+// and multiplied while the current pair's rank-1 updates issue.
 template <int P>
 __global__ void __launch_bounds__(32 * F_WARPS, 2)
 k2f_spread(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ ch_s0, const int* __restrict__ ch_s1,
@@ -242,11 +369,13 @@ k2f_spread(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ ch_s
            const cplx* __restrict__ recy_all, const cplx* __restrict__ yin, const int* __restrict__ in_perm,
            cplx* __restrict__ TB, cplx* __restrict__ TL, cplx* __restrict__ TC) {
   using F = FSpread<P>;
-  constexpr int S = F_S, T = F_T, R = F_R, E = F::E, EE = F::EE, RR = F::RR, NCE = F::NCE, NCU = F::NCU;
+  using Scr = typename F::Scratch;
+  constexpr int S = F_S, T = F_T, R = F_R, AR = F_AR, BAND = F_BAND, E = F::E, EE = F::EE, RR = F::RR,
+                NCE = F::NCE, NCU = F::NCU;
   extern __shared__ __align__(16) unsigned char fsm_raw[];
   cplx* s_ys = reinterpret_cast<cplx*>(fsm_raw + F::STG_YS);
   int* s_ox = reinterpret_cast<int*>(fsm_raw + F::STG_OX);
-  typename F::Scratch* scr_all = reinterpret_cast<typename F::Scratch*>(fsm_raw + (F::MAIN + 15) / 16 * 16);
+  Scr* scr_all = reinterpret_cast<Scr*>(fsm_raw + (F::MAIN + 15) / 16 * 16);
   __shared__ int rs[T + 1];
   const int prob = blockIdx.y, c = blockIdx.x;
   if (c >= ch_count[prob]) return;
@@ -280,13 +409,14 @@ k2f_spread(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ ch_s
     rs[threadIdx.x] = lo;
   }
   __syncthreads();
-  typename F::Scratch& scr = scr_all[warp];
-  cplx acc[R];
+  Scr* cur = scr_all + 2 * warp;
+  Scr* nxt = cur + 1;
+  cplx acc[AR];
   cplx accx[EE];
   cplx cacc[NCU];
   int cqa[NCU], cqb[NCU];
 #pragma unroll
-  for (int r = 0; r < R; ++r) acc[r] = mk(0, 0);
+  for (int r = 0; r < AR; ++r) acc[r] = mk(0, 0);
 #pragma unroll
   for (int e = 0; e < EE; ++e) accx[e] = mk(0, 0);
 #pragma unroll
@@ -298,60 +428,94 @@ k2f_spread(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ ch_s
     cqb[uu] = 1 + ((k % 2 == 0) ? 0 : P) + j;  // record index of the (Ly | Ry) column
   }
   const int ly = E > 0 ? ((lane >= R && lane - R < E) ? lane - R : 0) : 0;  // y-line lane
-  // lane roles of the derived values (see the loop): A from ry (lanes 0..7) or rx,
-  // record index 1 + e (clamped to the family) or 0 (lane >= 24); B = Dx | 1 | Dy
+  // lane roles of the derived values: A from ry (lanes 0..7) or rx, record index
+  // 1 + e (clamped to the family) or 0 (lane >= 24); B = Dx | 1 | Dy
   const int role_e = E > 0 ? ((lane & 7) < E ? (lane & 7) : E - 1) : 0;
   const bool role_a_y = lane < 8;
   const int role_idx = (lane < 24 && E > 0) ? 1 + role_e : 0;
   const int role_b = lane < 8 ? 0 : (lane < 16 ? 1 : 2);
-  for (int oy = warp; oy < T; oy += F_WARPS) {
+  const cplx* base_a = (role_a_y ? s_ry : s_rx) + role_idx;  // per-lane record columns (branch-free loads)
+  const cplx* base_b = role_b == 2 ? s_ry : s_rx;
+  const bool b_one = role_b == 1;
+  // derived per-sample values of the pair (i0, i1), one per lane, z = conj(A B) ys:
+  //   lanes 0..7  vx_e = conj(By(m,e) Dx) y   (side_y_edge, freq2wave.cpp:376)
+  //   lanes 8..15 ca_i = conj(Ax(m,i)) y      (corner rows, freq2wave.cpp:351)
+  //   lanes 16..23 vy_e = conj(Ax(m,e) Dy) y  (side_x_edge, freq2wave.cpp:363)
+  //   lane 24      v2  = conj(Dx Dy) y        (interior,    freq2wave.cpp:335)
+  // plus this lane's column tap w1 of each sample and the pair's packed row taps.
+  // The second amplitude is scaled by kb (0 for the odd tail, whose second slot
+  // repeats the first sample).
+  auto load_pair = [&](int i0, int i1, double kb, cplx (&dv)[2], double2& wyp, double (&w1)[2]) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int i = k ? i1 : i0;
+      const cplx ys = k ? cscale(s_ys[i], kb) : s_ys[i];
+      const cplx Av = base_a[i * RR];
+      const cplx Bl = base_b[i * RR];
+      const cplx Bv = b_one ? mk(1.0, 0.0) : Bl;
+      dv[k] = cmul(conj_(cmul(Av, Bv)), ys);
+      const int t1 = lane - s_ox[i];
+      const bool colv = lane < R && t1 >= 0 && t1 < S;
+      w1[k] = colv ? s_wx[i * S + (t1 < 0 ? 0 : (t1 >= S ? S - 1 : t1))] : 0.0;
+    }
+    const int tl = lane < S ? lane : 0;
+    wyp = make_double2(s_wy[i0 * S + tl], s_wy[i1 * S + tl]);
+  };
+  auto store_pair = [&](Scr* sc, const cplx (&dv)[2], double2 wyp) {
+    sc->d[0][lane] = dv[0];
+    sc->d[1][lane] = dv[1];
+    if (lane < S) sc->wy[lane] = wyp;
+  };
+  // update amplitude of this lane: column tap x interior value (region lanes) or
+  // the y-line value (lanes 24..24+E)
+  auto lane_u = [&](const Scr* sc, const double (&w1)[2], cplx (&u)[2]) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const cplx ug = cscale(sc->d[k][24], w1[k]);
+      u[k] = lane < R ? ug : ((E > 0 && lane - R < E) ? sc->d[k][16 + ly] : mk(0, 0));
+    }
+  };
+  auto band_row = [&](auto KC) {
+    constexpr int k = decltype(KC)::value;
+    const int oy = warp * BAND + k;
     const int a = rs[oy], b = rs[oy + 1];
+    if (a >= b) return;
+    cplx dv[2], u[2];
+    double2 wyp;
+    double w1[2], w1n[2];
+    load_pair(a, a + 1 < b ? a + 1 : a, a + 1 < b ? 1.0 : 0.0, dv, wyp, w1);
+    __syncwarp();  // previous readers of *cur are done
+    store_pair(cur, dv, wyp);
+    __syncwarp();
+    lane_u(cur, w1, u);
     for (int s = a; s < b; s += 2) {
-      const int sb = s + 1 < b ? s + 1 : s;     // odd tail: second slot repeats the first ...
-      const double kb = s + 1 < b ? 1.0 : 0.0;  // ... with zero amplitude
-      // derived per-sample values, one per lane, z = conj(A B) ys:
-      //   lanes 0..7  vx_e = conj(By(m,e) Dx) y   (side_y_edge, freq2wave.cpp:376)
-      //   lanes 8..15 ca_i = conj(Ax(m,i)) y      (corner rows, freq2wave.cpp:351)
-      //   lanes 16..23 vy_e = conj(Ax(m,e) Dy) y  (side_x_edge, freq2wave.cpp:363)
-      //   lane 24      v2  = conj(Dx Dy) y        (interior,    freq2wave.cpp:335)
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const int i = k ? sb : s;
-        const cplx* rx = s_rx + i * RR;
-        const cplx* ry = s_ry + i * RR;
-        const cplx ys = k ? cscale(s_ys[i], kb) : s_ys[i];
-        const cplx Av = role_a_y ? ry[role_idx] : rx[role_idx];
-        const cplx Bv = role_b == 0 ? rx[0] : (role_b == 1 ? mk(1.0, 0.0) : ry[0]);
-        scr.d[k][lane] = cmul(conj_(cmul(Av, Bv)), ys);
-      }
-      if (lane < S) scr.wy[lane] = make_double2(s_wy[s * S + lane], s_wy[sb * S + lane]);
-      __syncwarp();
-      cplx u[2];
-      double w1[2];
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const int i = k ? sb : s;
-        const int t1 = lane - s_ox[i];
-        const bool colv = lane < R && t1 >= 0 && t1 < S;
-        w1[k] = colv ? s_wx[i * S + (t1 < 0 ? 0 : (t1 >= S ? S - 1 : t1))] : 0.0;
-        const cplx ug = cscale(scr.d[k][24], w1[k]);
-        u[k] = lane < R ? ug : ((E > 0 && lane - R < E) ? scr.d[k][16 + ly] : mk(0, 0));
-      }
-      f_upd_dispatch(oy, acc, u[0], u[1], scr.wy);
+      const int sb = s + 1 < b ? s + 1 : s;
+      const int sn = s + 2;  // next pair (indices clamped; unused past the row end)
+      load_pair(sn < b ? sn : b - 1, sn + 1 < b ? sn + 1 : b - 1, sn + 1 < b ? 1.0 : 0.0, dv, wyp, w1n);
+      f_upd<k>(acc, u[0], u[1], cur->wy);
       if (E > 0) {
 #pragma unroll
-        for (int e = 0; e < E; ++e) accx[e] = caxpy(caxpy(accx[e], w1[0], scr.d[0][e]), w1[1], scr.d[1][e]);
+        for (int e = 0; e < E; ++e) accx[e] = caxpy(caxpy(accx[e], w1[0], cur->d[0][e]), w1[1], cur->d[1][e]);
         const cplx* rya = s_ry + s * RR;
         const cplx* ryb = s_ry + sb * RR;
 #pragma unroll
         for (int uu = 0; uu < NCU; ++uu)  // corners (freq2wave.cpp:349-353)
           if (lane + 32 * uu < NCE)
-            cacc[uu] = cadd(cadd(cacc[uu], cmul(scr.d[0][8 + cqa[uu]], conj_(rya[cqb[uu]]))),
-                            cmul(scr.d[1][8 + cqa[uu]], conj_(ryb[cqb[uu]])));
+            cacc[uu] = cadd(cadd(cacc[uu], cmul(cur->d[0][8 + cqa[uu]], conj_(rya[cqb[uu]]))),
+                            cmul(cur->d[1][8 + cqa[uu]], conj_(ryb[cqb[uu]])));
       }
+      store_pair(nxt, dv, wyp);
       __syncwarp();
+      lane_u(nxt, w1n, u);
+      w1[0] = w1n[0];
+      w1[1] = w1n[1];
+      Scr* t = cur;
+      cur = nxt;
+      nxt = t;
     }
-  }
+  };
+  static_assert(BAND * F_WARPS == T, "the warps' bands tile the sample rows");
+  f_static_for<0, BAND>(band_row);
   __syncthreads();  // the fold buffer aliases the staging area
   // dump the warp copies, fold, write this chunk's region / lines / corners once
   cplx* buf = reinterpret_cast<cplx*>(fsm_raw);  // [F_WARPS][PER_WARP]
@@ -359,12 +523,12 @@ k2f_spread(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ ch_s
   cplx* mine = buf + warp * F::PER_WARP;
   if (lane < R) {
 #pragma unroll
-    for (int r = 0; r < R; ++r) mine[r * R + lane] = acc[r];
+    for (int r = 0; r < AR; ++r) mine[r * R + lane] = acc[r];
 #pragma unroll
-    for (int e = 0; e < E; ++e) mine[R * R + E * R + e * R + lane] = accx[e];
+    for (int e = 0; e < E; ++e) mine[AR * R + E * AR + e * R + lane] = accx[e];
   } else if (lane - R < E) {
 #pragma unroll
-    for (int r = 0; r < R; ++r) mine[R * R + (lane - R) * R + r] = acc[r];
+    for (int r = 0; r < AR; ++r) mine[AR * R + (lane - R) * AR + r] = acc[r];
   }
   if (NCE > 0) {
 #pragma unroll
@@ -377,18 +541,28 @@ k2f_spread(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ ch_s
   const int64_t chunk = (int64_t)prob * cap + c;
   cplx* tb = TB + chunk * R * R;
   for (int i = threadIdx.x; i < R * R; i += blockDim.x) {
-    cplx a = buf[i];
+    const int r = i / R, cc = i - r * R;
+    cplx a = mk(0, 0);
 #pragma unroll
-    for (int w = 1; w < F_WARPS; ++w) a = cadd(a, buf[w * F::PER_WARP + i]);
+    for (int w = 0; w < F_WARPS; ++w) {
+      const int rr = r - w * BAND;
+      if (rr >= 0 && rr < AR) a = cadd(a, buf[w * F::PER_WARP + rr * R + cc]);
+    }
     tb[i] = a;
   }
   if (E > 0) {
-    cplx* tl = TL + chunk * 2 * E * R;
-    for (int i = threadIdx.x; i < 2 * E * R; i += blockDim.x) {
-      cplx a = buf[R * R + i];
+    cplx* tl = TL + chunk * 2 * E * R;  // [y-lines e][row] then [x-lines e][column]
+    for (int i = threadIdx.x; i < E * R; i += blockDim.x) {
+      const int e = i / R, r = i - e * R;
+      cplx a = mk(0, 0), bx = mk(0, 0);
 #pragma unroll
-      for (int w = 1; w < F_WARPS; ++w) a = cadd(a, buf[w * F::PER_WARP + R * R + i]);
+      for (int w = 0; w < F_WARPS; ++w) {
+        const int rr = r - w * BAND;
+        if (rr >= 0 && rr < AR) a = cadd(a, buf[w * F::PER_WARP + AR * R + e * AR + rr]);
+        bx = cadd(bx, buf[w * F::PER_WARP + AR * R + E * AR + i]);
+      }
       tl[i] = a;
+      tl[E * R + i] = bx;
     }
     cplx* tc = TC + chunk * NCE;
     for (int q = threadIdx.x; q < NCE; q += blockDim.x) {
