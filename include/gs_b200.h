@@ -137,6 +137,13 @@ int gs_gen_grid(int64_t M, double eps, int dim, double* out);
 int gs_gen_jitter(int64_t M, double eps, double eta, uint64_t seed, int dim, double* out);
 int gs_gen_spiral(int turns, double points_per_turn, double K, double* out);
 int gs_voronoi_weights(int dim, int64_t M, const double* coords, double K, double* mu, int nthreads);
+/* density(samples, K).delta_raw (weights.cpp:135-176; replaces gs::density) */
+int gs_density(int dim, int64_t M, const double* coords, double K, double* delta_raw, int nthreads);
+/* bench harness right-hand side: n seeded coefficients, interleaved re,im
+ * (bench.cpp:30-36 seeded_coefficients) */
+int gs_seeded_coefficients(int64_t n, uint64_t seed, double* out);
+/* truncated-cosine test signal at 1D frequencies (signals.cpp:27-37) */
+int gs_truncated_cosine(int64_t M, const double* xi, double* out);
 const char* gs_inputs_last_error(void);
 
 const char* gs_last_error(void);

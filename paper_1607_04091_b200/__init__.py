@@ -25,7 +25,7 @@ from typing import Optional
 import numpy as np
 
 __all__ = [
-    "Error", "UsageError", "ShapeError", "DomainError", "NumericalError", "CudaError",
+    "Error", "UsageError", "FileFormatError", "ShapeError", "DomainError", "NumericalError", "CudaError",
     "SamplingSet", "Freq2WaveOptions", "Freq2WaveOp", "SolveOptions", "SolveStats",
     "freq2wave", "apply_forward", "apply_adjoint", "solve_least_squares", "CglsSession",
     "family_p", "ROUTES", "lib_path", "load_library",
@@ -52,6 +52,10 @@ class UsageError(Error):
     exit_code = 2
 
 
+class FileFormatError(Error):
+    exit_code = 3
+
+
 class ShapeError(Error):
     exit_code = 4
 
@@ -68,7 +72,7 @@ class CudaError(Error):
     exit_code = 7
 
 
-_ERRS = {2: UsageError, 4: ShapeError, 5: DomainError, 6: NumericalError, 7: CudaError}
+_ERRS = {2: UsageError, 3: FileFormatError, 4: ShapeError, 5: DomainError, 6: NumericalError, 7: CudaError}
 ROUTES = {1: "uniform_1d", 2: "nfft_1d", 3: "nfft_2d", 4: "tensor_2d"}
 
 

@@ -8,6 +8,9 @@
 //     unprocessed point is farther than twice the cell's farthest vertex --
 //     beyond that no bisector can cut the cell, so the polygon equals the
 //     reference's clip against all M points (weights.cpp:59-70).
+//   * the density report, the bench harness's seeded coefficients and the
+//     truncated-cosine test signal (weights.cpp:135-176, bench.cpp:30-36,
+//     signals.cpp:12-37) for the command-line front end.
 // Multi-threaded with std::thread.  Not on the timed path.
 #include <algorithm>
 #include <atomic>
@@ -112,8 +115,11 @@ int gs_gen_spiral(int turns, double ppt, double K, double* out) {
   return 0;
 }
 
-// Voronoi cell measures inside [-K, K]^dim (weights.cpp:95-133), exact, fast.
-int gs_voronoi_weights(int dim, int64_t M, const double* coords, double K, double* mu, int nthreads) {
+// Voronoi cells clipped to [-K, K]^dim (weights.cpp:95-133), exact, fast.
+// mu[m] = cell measure; rad[m] (optional) = farthest cell vertex from point m,
+// i.e. the largest distance from a vertex of cell m to its nearest sample
+// (weights.cpp:135-171 takes the supremum of these over all cells).
+static int voronoi_cells(int dim, int64_t M, const double* coords, double K, double* mu, double* rad, int nthreads) {
   if (!(K > 0)) {
     g_in_err = "K must be positive";
     return 5;
@@ -138,7 +144,11 @@ int gs_voronoi_weights(int dim, int64_t M, const double* coords, double K, doubl
     for (int64_t i = 0; i < M; ++i) {
       double lo = i == 0 ? -K : 0.5 * (coords[order[i - 1]] + coords[order[i]]);
       double hi = i + 1 == M ? K : 0.5 * (coords[order[i]] + coords[order[i + 1]]);
-      mu[order[i]] = hi - lo;
+      if (mu) mu[order[i]] = hi - lo;
+      // density candidates (weights.cpp:147-150): the region ends, half gaps
+      if (rad) rad[order[i]] = std::max(i == 0 ? coords[order[0]] + K : 0.0,
+                                        i + 1 == M ? K - coords[order[i]]
+                                                   : 0.5 * (coords[order[i + 1]] - coords[order[i]]));
     }
     return 0;
   }
@@ -212,13 +222,76 @@ int gs_voronoi_weights(int dim, int64_t M, const double* coords, double K, doubl
           for (const P2& v : poly) rmax2 = std::max(rmax2, (v.x - own.x) * (v.x - own.x) + (v.y - own.y) * (v.y - own.y));
           if (covers_all || 4.0 * rmax2 <= reach * reach) break;
         }
-        mu[m] = area(poly);
+        if (mu) mu[m] = area(poly);
+        if (rad) {
+          double r = 0.0;
+          for (const P2& v : poly) r = std::max(r, std::hypot(v.x - own.x, v.y - own.y));
+          rad[m] = r;
+        }
       }
     }
   };
   std::vector<std::thread> th;
   for (int t = 0; t < nthreads; ++t) th.emplace_back(worker);
   for (auto& t : th) t.join();
+  return 0;
+}
+
+int gs_voronoi_weights(int dim, int64_t M, const double* coords, double K, double* mu, int nthreads) {
+  return voronoi_cells(dim, M, coords, K, mu, nullptr, nthreads);
+}
+
+// density(samples, K) (weights.cpp:135-176): delta_raw = sup over Y_K of the
+// distance to the nearest sample, attained at a vertex of the clipped
+// tessellation -- the farthest vertex of some cell from that cell's own point.
+int gs_density(int dim, int64_t M, const double* coords, double K, double* delta_raw, int nthreads) {
+  std::vector<double> rad(M > 0 ? M : 1);
+  const int rc = voronoi_cells(dim, M, coords, K, nullptr, rad.data(), nthreads);
+  if (rc) return rc;
+  double d = 0.0;
+  for (int64_t m = 0; m < M; ++m) d = std::max(d, rad[m]);
+  *delta_raw = d;
+  return 0;
+}
+
+// bench.cpp:30-36: x_k = (U(-1,1), U(-1,1)) from mt19937_64(seed ^ golden ratio)
+int gs_seeded_coefficients(int64_t n, uint64_t seed, double* out) {
+  if (n < 0) {
+    g_in_err = "negative count";
+    return 4;
+  }
+  std::mt19937_64 rng(seed ^ 0x9e3779b97f4a7c15ull);
+  std::uniform_real_distribution<double> unit(-1.0, 1.0);
+  for (int64_t k = 0; k < n; ++k) {
+    const double re = unit(rng);
+    const double im = unit(rng);
+    out[2 * k] = re;
+    out[2 * k + 1] = im;
+  }
+  return 0;
+}
+
+// signals.cpp:12-37: analytic transform of cos(2 pi x) on [-1/2, 0)
+int gs_truncated_cosine(int64_t M, const double* xi, double* out) {
+  const double pi = 3.14159265358979323846;
+  auto g = [&](double a, double& re, double& im) {  // (e^{i pi a} - 1) / (2 pi i a), 1/2 at a = 0
+    if (a == 0.0) {
+      re = 0.5;
+      im = 0.0;
+      return;
+    }
+    const double nr = std::cos(pi * a) - 1.0, ni = std::sin(pi * a);
+    const double d = 2.0 * pi * a;  // (nr + i ni) / (i d) = ni / d - i nr / d
+    re = ni / d;
+    im = -nr / d;
+  };
+  for (int64_t m = 0; m < M; ++m) {
+    double ar, ai, br, bi;
+    g(xi[m] - 1.0, ar, ai);
+    g(xi[m] + 1.0, br, bi);
+    out[2 * m] = 0.5 * (ar + br);
+    out[2 * m + 1] = 0.5 * (ai + bi);
+  }
   return 0;
 }
 
