@@ -131,6 +131,19 @@ int gs_op_export_factors(gs_op* op, int b, int axis, double* D, double* L, doubl
 int gs_profile_pair(gs_op* op, int reps, void* stream, int max_kernels, double* ms_out,
                     char* names_out, int* count);
 
+/* Dyadic-grid evaluation (dyadic.hpp:27-64; front-end row SURVEY 8(f)4).
+ * Tables of the interior scaling function / of edge function k of one side
+ * at resolution R (evaluate_scaling_dyadic, evaluate_boundary_dyadic):
+ * values[i] = phi(support_begin + i / 2^R); values == NULL -> sizes only.
+ * gs_weval = weval_1d (dim 1, 2^J real coefficients, 2^R + 1 outputs) or
+ * weval_2d (dim 2, 4^J coefficients x-fastest, (2^R + 1)^2 outputs, row =
+ * y).  Buffers are host or device pointers. */
+int gs_scaling_dyadic(int family_p, int R, double* values, int64_t* len, int64_t* support_begin, void* stream);
+int gs_boundary_dyadic(int family_p, int left, int R, int k, double* values, int64_t* len, int64_t* support_begin,
+                       void* stream);
+int gs_weval(int dim, int family_p, int J, int R, const double* coeffs, int64_t coeffs_len, double* out,
+             void* stream);
+
 /* Input harness (reference patterns.cpp generators, exact fast Voronoi
  * weights with weights.cpp semantics); host-only, not on the timed path. */
 int gs_gen_grid(int64_t M, double eps, int dim, double* out);

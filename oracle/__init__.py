@@ -248,6 +248,48 @@ def voronoi(dim, coords, K):
     return mu
 
 
+class FTable:
+    """dyadic.hpp FunctionTable: samples at support_begin + i / 2^R."""
+
+    def __init__(self, R, support_begin, values):
+        self.resolution, self.support_begin, self.values = R, support_begin, values
+
+    def value_at(self, numerator):
+        idx = numerator - (self.support_begin << self.resolution)
+        return float(self.values[idx]) if 0 <= idx < self.values.size else 0.0
+
+
+def _table(call):
+    n, sb = C.c_longlong(0), C.c_longlong(0)
+    _chk(call(None, C.byref(n), C.byref(sb)))
+    out = np.empty(n.value)
+    _chk(call(_p(out), C.byref(n), C.byref(sb)))
+    return out, sb.value
+
+
+def scaling_dyadic(p, R):
+    v, sb = _table(lambda o, n, s: lib().orc_scaling_dyadic(C.c_int(p), C.c_int(R), o, n, s))
+    return FTable(R, sb, v)
+
+
+def boundary_dyadic(p, left, R):
+    out = []
+    for k in range(p):
+        v, sb = _table(lambda o, n, s, k=k: lib().orc_boundary_dyadic(C.c_int(p), C.c_int(int(left)), C.c_int(R),
+                                                                      C.c_int(k), o, n, s))
+        out.append(FTable(R, sb, v))
+    return out
+
+
+def weval(dim, p, J, R, coeffs):
+    coeffs = _f64(coeffs).ravel()
+    g = (1 << R) + 1
+    out = np.empty(g if dim == 1 else g * g)
+    _chk(lib().orc_weval(C.c_int(dim), C.c_int(p), C.c_int(J), C.c_int(R), _p(coeffs), C.c_longlong(coeffs.size),
+                         _p(out)))
+    return out
+
+
 def wrap_half_open(z):
     return lib().orc_wrap_half_open(float(z))
 

@@ -17,6 +17,8 @@
 //   solver.cpp:19-91      solve_least_squares (CGNR)
 //   patterns.cpp:14-74    gen_grid / gen_jitter / gen_spiral
 //   weights.cpp:99-226    voronoi_weights (1D midpoints, 2D half-plane clipping)
+//   dyadic.cpp:14-231     integer values, dyadic cascades (interior + edge),
+//                         weval_1d / weval_2d (front-end row SURVEY 8(f)4)
 // Third-party stand-ins: FFTW (unnormalised c2c, FORWARD = -1) is replaced by
 // our own radix-2 FFT (direct DFT for non power-of-two lengths); Eigen by
 // plain loops.  Results agree with the reference to roundoff.
@@ -1052,6 +1054,215 @@ std::vector<double> voronoi(int dim, const std::vector<double>& c, double K) {  
     return mu;
 }
 
+
+// ---------------------------------------------------------------- dyadic evaluation (dyadic.cpp)
+// Least squares by Householder QR of the (n+1) x n consistent system
+// (Eigen colPivHouseholderQr, dyadic.cpp:29): the solution is unique.
+std::vector<double> qr_solve(std::vector<double> A, std::vector<double> b, int rows, int cols) {
+    for (int k = 0; k < cols; ++k) {
+        double nrm = 0.0;
+        for (int i = k; i < rows; ++i) nrm += A[i * cols + k] * A[i * cols + k];
+        nrm = std::sqrt(nrm);
+        if (nrm == 0.0) continue;
+        double alpha = A[k * cols + k] > 0 ? -nrm : nrm;
+        std::vector<double> v(rows, 0.0);
+        for (int i = k; i < rows; ++i) v[i] = A[i * cols + k];
+        v[k] -= alpha;
+        double vv = 0.0;
+        for (int i = k; i < rows; ++i) vv += v[i] * v[i];
+        if (vv == 0.0) continue;
+        for (int j = k; j < cols; ++j) {
+            double d = 0.0;
+            for (int i = k; i < rows; ++i) d += v[i] * A[i * cols + j];
+            d = 2.0 * d / vv;
+            for (int i = k; i < rows; ++i) A[i * cols + j] -= d * v[i];
+        }
+        double d = 0.0;
+        for (int i = k; i < rows; ++i) d += v[i] * b[i];
+        d = 2.0 * d / vv;
+        for (int i = k; i < rows; ++i) b[i] -= d * v[i];
+    }
+    std::vector<double> x(cols);
+    for (int i = cols - 1; i >= 0; --i) {
+        double acc = b[i];
+        for (int j = i + 1; j < cols; ++j) acc -= A[i * cols + j] * x[j];
+        x[i] = acc / A[i * cols + i];
+    }
+    return x;
+}
+
+// phi at the integers -p+2..p-1: eigenvector of T(n,m) = 2 h(2n - m) for
+// eigenvalue 1, sum 1 (dyadic.cpp:14-35)
+std::vector<double> integer_values(const Family& fam) {
+    int p = fam.p, n = 2 * p - 2;
+    auto tap = [&](int k) { return (k < -p + 1 || k > p) ? 0.0 : fam.taps[k + p - 1]; };
+    std::vector<double> sys((n + 1) * n, 0.0), rhs(n + 1, 0.0);
+    for (int r = 0; r < n; ++r)
+        for (int c = 0; c < n; ++c) sys[r * n + c] = 2.0 * tap(2 * (r - p + 2) - (c - p + 2)) - (r == c ? 1.0 : 0.0);
+    for (int c = 0; c < n; ++c) sys[n * n + c] = 1.0;
+    rhs[n] = 1.0;
+    std::vector<double> v = qr_solve(sys, rhs, n + 1, n);
+    double res = 0.0;
+    for (int r = 0; r <= n; ++r) {
+        double acc = -rhs[r];
+        for (int c = 0; c < n; ++c) acc += sys[r * n + c] * v[c];
+        res += acc * acc;
+    }
+    if (std::sqrt(res) > 1e-10) numerical("integer value eigenproblem did not solve");
+    return v;
+}
+
+struct FTable {  // dyadic.hpp:13-25
+    int R = 0;
+    long long support_begin = 0;
+    std::vector<double> values;
+    double at(long long num) const {
+        long long idx = num - (support_begin << R);
+        if (idx < 0 || idx >= (long long)values.size()) return 0.0;
+        return values[(size_t)idx];
+    }
+};
+
+FTable scaling_dyadic(const Family& fam, int R) {  // dyadic.cpp:37-68
+    if (R < 0) domain("resolution must be >= 0");
+    FTable t;
+    t.R = R;
+    t.support_begin = -fam.p + 1;
+    size_t len = ((size_t)(2 * fam.p - 1) << R) + 1;
+    t.values.assign(len, 0.0);
+    if (fam.p == 1) {
+        for (size_t i = 0; i + 1 < len; ++i) t.values[i] = 1.0;
+        return t;
+    }
+    std::vector<double> iv = integer_values(fam);
+    for (size_t k = 0; k < iv.size(); ++k) t.values[(k + 1) << R] = iv[k];
+    for (int r = 1; r <= R; ++r) {
+        long long step = 1LL << (R - r);
+        for (long long i = step; i < (long long)len; i += 2 * step) {
+            long long nx = (t.support_begin << R) + i;
+            double acc = 0.0;
+            for (int k = -fam.p + 1; k <= fam.p; ++k) acc += fam.taps[k + fam.p - 1] * t.at(2 * nx - ((long long)k << R));
+            t.values[(size_t)i] = 2.0 * acc;
+        }
+    }
+    return t;
+}
+
+std::vector<FTable> boundary_dyadic(const Family& fam, bool left, int R) {  // dyadic.cpp:70-115
+    if (fam.p < 2) domain("boundary functions require p >= 2");
+    if (R < 0) domain("resolution must be >= 0");
+    const int p = fam.p;
+    const gsdata::FamilyData& f = gsdata::kFamilies[p - 1];
+    const double* H = left ? f.left_H : f.right_H;
+    const double* h = left ? f.left_h : f.right_h;
+    const double* seed = left ? f.left_seed : f.right_seed;
+    FTable interior = scaling_dyadic(fam, R);
+    std::vector<FTable> tabs(p);
+    for (int k = 0; k < p; ++k) {
+        FTable& t = tabs[k];
+        t.R = R;
+        t.support_begin = left ? 0 : -(p + k);
+        t.values.assign(((size_t)(p + k) << R) + 1, 0.0);
+        for (int d = 0; d <= p + k; ++d) {
+            long long nn = left ? d : -d;
+            t.values[(size_t)((nn - t.support_begin) << R)] = seed[k * 2 * p + d];
+        }
+    }
+    const double sqrt2 = std::sqrt(2.0);
+    for (int r = 1; r <= R; ++r) {
+        long long step = 1LL << (R - r);
+        for (int k = 0; k < p; ++k) {
+            FTable& t = tabs[k];
+            for (long long i = step; i < (long long)t.values.size(); i += 2 * step) {
+                long long nx = (t.support_begin << R) + i;
+                double acc = 0.0;
+                for (int l = 0; l < p; ++l) acc += H[k * p + l] * tabs[l].at(2 * nx);
+                for (int m = p; m <= p + 2 * k; ++m) {
+                    long long arg = left ? 2 * nx - ((long long)m << R) : 2 * nx + ((long long)(m + 1) << R);
+                    acc += h[k * (2 * p - 1) + (m - p)] * interior.at(arg);
+                }
+                t.values[(size_t)i] = sqrt2 * acc;
+            }
+        }
+    }
+    return tabs;
+}
+
+// sink(i, w * 2^{J/2} * basis column c at grid point i)  (dyadic.cpp:121-170)
+struct Basis {
+    const Family& fam;
+    int J, R, tabres;
+    long long n_grid;
+    FTable interior;
+    std::vector<FTable> left, right;
+    double amplitude;
+    Basis(const Family& f, int J_, int R_)
+        : fam(f), J(J_), R(R_), tabres(R_ - J_), n_grid(1LL << R_), interior(scaling_dyadic(f, R_ - J_)),
+          amplitude(std::exp2(0.5 * J_)) {
+        if (f.p >= 2) {
+            left = boundary_dyadic(f, true, tabres);
+            right = boundary_dyadic(f, false, tabres);
+        }
+    }
+    template <class Sink>
+    void column(long long c, double w, Sink&& sink) const {
+        long long n = 1LL << J, unit = 1LL << tabres;
+        double scale = w * amplitude;
+        if (fam.p >= 2 && c < fam.p) {
+            const FTable& t = left[(size_t)c];
+            long long hi = std::min<long long>(n_grid, (fam.p + c) * unit);
+            for (long long i = 0; i <= hi; ++i) sink(i, scale * t.values[(size_t)i]);
+        } else if (fam.p >= 2 && c >= n - fam.p) {
+            const FTable& t = right[(size_t)(n - 1 - c)];
+            long long lo = std::max<long long>(0, n_grid - (fam.p + (n - 1 - c)) * unit);
+            for (long long i = lo; i <= n_grid; ++i) sink(i, scale * t.at(i - n_grid));
+        } else {
+            long long lo = std::max<long long>(0, (c - fam.p + 1) * unit);
+            long long hi = std::min<long long>(n_grid, (c + fam.p) * unit);
+            for (long long i = lo; i <= hi; ++i) sink(i, scale * interior.at(i - c * unit));
+        }
+    }
+};
+
+void check_weval(const Family& fam, int J, int R, size_t got, size_t want) {  // dyadic.cpp:172-180
+    if ((1LL << J) < 2 * fam.p) domain("scale too small: 2^J must be >= 2p");
+    if (R < J) domain("resolution too coarse: R must be >= J");
+    if (got != want) shape("coefficient vector has wrong length");
+}
+
+std::vector<double> weval(int dim, const Family& fam, int J, int R, const std::vector<double>& coeffs) {
+    const size_t n = (size_t)1 << J, g = ((size_t)1 << R) + 1;
+    check_weval(fam, J, R, coeffs.size(), dim == 1 ? n : n * n);
+    Basis basis(fam, J, R);
+    if (dim == 1) {  // dyadic.cpp:184-199
+        std::vector<double> out(g, 0.0);
+        for (size_t c = 0; c < n; ++c) {
+            double w = coeffs[c];
+            if (w == 0.0) continue;
+            basis.column((long long)c, w, [&](long long i, double v) { out[(size_t)i] += v; });
+        }
+        return out;
+    }
+    // dyadic.cpp:201-230: out(iy, ix) = sum_j (B X^T)(iy, j) B(ix, j), X(i, j) = coeffs[j n + i]
+    std::vector<double> B(g * n, 0.0);
+    for (size_t c = 0; c < n; ++c) basis.column((long long)c, 1.0, [&](long long i, double v) { B[(size_t)i * n + c] = v; });
+    std::vector<double> Z(g * n, 0.0);
+    for (size_t a = 0; a < g; ++a)
+        for (size_t i = 0; i < n; ++i) {
+            double b = B[a * n + i];
+            if (b == 0.0) continue;
+            for (size_t j = 0; j < n; ++j) Z[a * n + j] += b * coeffs[i * n + j];
+        }
+    std::vector<double> out(g * g, 0.0);
+    for (size_t a = 0; a < g; ++a)
+        for (size_t bx = 0; bx < g; ++bx) {
+            double acc = 0.0;
+            for (size_t j = 0; j < n; ++j) acc += Z[a * n + j] * B[bx * n + j];
+            out[a * g + bx] = acc;
+        }
+    return out;
+}
+
 }  // namespace orc
 
 // ============================================================================
@@ -1267,6 +1478,33 @@ int orc_voronoi(int dim, long long M, const double* coords, double K, double* mu
         std::vector<double> c(coords, coords + M * dim);
         auto v = orc::voronoi(dim, c, K);
         std::memcpy(mu, v.data(), v.size() * 8);
+    });
+}
+// dyadic tables / evaluation (dyadic.cpp); two-call pattern: out == NULL -> sizes only
+int orc_scaling_dyadic(int p, int R, double* out, long long* len, long long* support_begin) {
+    return guard([&] {
+        orc::FTable t = orc::scaling_dyadic(orc::make_family(p), R);
+        *len = (long long)t.values.size();
+        *support_begin = t.support_begin;
+        if (out) std::memcpy(out, t.values.data(), t.values.size() * 8);
+    });
+}
+int orc_boundary_dyadic(int p, int left, int R, int k, double* out, long long* len, long long* support_begin) {
+    return guard([&] {
+        auto tabs = orc::boundary_dyadic(orc::make_family(p), left != 0, R);
+        if (k < 0 || k >= p) orc::domain("edge function index out of range");
+        const orc::FTable& t = tabs[(size_t)k];
+        *len = (long long)t.values.size();
+        *support_begin = t.support_begin;
+        if (out) std::memcpy(out, t.values.data(), t.values.size() * 8);
+    });
+}
+int orc_weval(int dim, int p, int J, int R, const double* coeffs, long long ncoeffs, double* out) {
+    return guard([&] {
+        if (dim != 1 && dim != 2) orc::domain("dim must be 1 or 2");
+        std::vector<double> c(coeffs, coeffs + ncoeffs);
+        auto v = orc::weval(dim, orc::make_family(p), J, R, c);
+        std::memcpy(out, v.data(), v.size() * 8);
     });
 }
 double orc_wrap_half_open(double z) { return orc::wrap_half_open(z); }

@@ -6,11 +6,9 @@ sidecar JSON and exit codes, routed through this package's C-ABI
     gen          sampling pattern -> frequency file       (gs_main.cpp:44-66)
     weights      Voronoi weights + density report          (gs_main.cpp:74-84)
     reconstruct  least-squares reconstruction on the GPU   (gs_main.cpp:108-171)
+    evaluate     coefficients on a dyadic grid (GPU)       (gs_main.cpp:179-198)
     bench        registry benchmark problem on the GPU     (gs_main.cpp:205-213,
                                                             bench.cpp:40-150)
-
-``evaluate`` (dyadic-grid evaluation, dyadic.cpp) is SURVEY 8(f)4 and not part
-of this build; it exits with a usage error.
 """
 from __future__ import annotations
 
@@ -207,7 +205,16 @@ def cmd_bench(a) -> int:
 
 
 def cmd_evaluate(a) -> int:
-    raise UsageError("evaluate: dyadic-grid evaluation (weval, dyadic.cpp) is not part of this build")
+    """gs_main.cpp:179-198: real part of the coefficients -> weval -> CSV / PGM."""
+    from . import dyadic
+    cf = gsio.read_coefficient_file(a.coefficient_file)
+    real = np.ascontiguousarray(cf.values.real)
+    if cf.dim == 1:
+        gsio.write_evaluation_csv(a.output, dyadic.weval_1d(real, cf.family, cf.J, a.resolution))
+    else:
+        gsio.write_evaluation_pgm(a.output, dyadic.weval_2d(real, cf.family, cf.J, a.resolution))
+    print(f"wrote {a.output}")
+    return 0
 
 
 # ------------------------------------------------------------------ parser (gs_main.cpp:217-291)

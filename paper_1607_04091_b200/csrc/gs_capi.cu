@@ -878,6 +878,9 @@ int guard_call(const std::function<void()>& f) {
   }
 }
 
+// ------------------------------------------------------------------ dyadic evaluation
+#include "dyadic_host.cuh"
+
 // ------------------------------------------------------------------ CGLS
 struct Session {
   gs_op* op = nullptr;
@@ -1359,6 +1362,50 @@ int gs_op_export_factors(gs_op* op, int b, int axis, double* D, double* L, doubl
       }
     }
   });
+}
+
+
+// ---------------------------------------------------------------- dyadic evaluation (dyadic.hpp)
+static cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int gs_scaling_dyadic(int family_p, int R, double* values, int64_t* len, int64_t* support_begin, void* stream) {
+  return guard_call([&] {
+    if (family_p < 1 || family_p > 8) fail(GS_ERR_DOMAIN, "unsupported family");
+    if (!len || !support_begin) fail(GS_ERR_USAGE, "null output");
+    if (!values) {  // sizes only
+      if (R < 0) fail(GS_ERR_DOMAIN, "resolution must be >= 0");
+      *len = ((int64_t)(2 * family_p - 1) << R) + 1;
+      *support_begin = -family_p + 1;
+      return;
+    }
+    DyTables T;
+    dy_build(T, family_p, R, false, as_stream(stream));
+    *len = T.P.len[0];
+    *support_begin = T.P.sb[0];
+    dy_copy_table(T, 0, values, as_stream(stream));
+  });
+}
+
+int gs_boundary_dyadic(int family_p, int left, int R, int k, double* values, int64_t* len, int64_t* support_begin,
+                       void* stream) {
+  return guard_call([&] {
+    if (family_p < 1 || family_p > 8) fail(GS_ERR_DOMAIN, "unsupported family");
+    if (family_p < 2) fail(GS_ERR_DOMAIN, "boundary functions require p >= 2");
+    if (R < 0) fail(GS_ERR_DOMAIN, "resolution must be >= 0");
+    if (k < 0 || k >= family_p) fail(GS_ERR_DOMAIN, "edge function index out of range");
+    if (!len || !support_begin) fail(GS_ERR_USAGE, "null output");
+    *len = ((int64_t)(family_p + k) << R) + 1;
+    *support_begin = left ? 0 : -(family_p + k);
+    if (!values) return;
+    DyTables T;
+    dy_build(T, family_p, R, true, as_stream(stream));
+    dy_copy_table(T, left ? 1 + k : 1 + family_p + k, values, as_stream(stream));
+  });
+}
+
+int gs_weval(int dim, int family_p, int J, int R, const double* coeffs, int64_t coeffs_len, double* out,
+             void* stream) {
+  return guard_call([&] { dy_weval(dim, family_p, J, R, coeffs, coeffs_len, out, as_stream(stream)); });
 }
 
 }  // extern "C"

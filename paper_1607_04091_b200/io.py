@@ -216,6 +216,33 @@ def read_coefficient_file(path) -> CoefficientFile:
     return CoefficientFile(dim, family, J, r.doubles(2 * count, "coefficients").view(np.complex128).copy())
 
 
+# ------------------------------------------------------------------ evaluations (io.cpp:277-297)
+def write_evaluation_csv(path, ev) -> None:
+    """1D: header x,value; x = i / 2^R - 1/2."""
+    if ev.dim != 1:
+        raise ShapeError("CSV evaluation output is 1D only")
+    vals = np.asarray(ev.values, dtype=np.float64).ravel()
+    with _open_out(path, False) as out:
+        out.write("x,value\n")
+        for i, v in enumerate(vals[: ev.points_per_axis()]):
+            out.write(f"{_fmt(i * 2.0 ** -ev.resolution - 0.5)},{_fmt(v)}\n")
+
+
+def write_evaluation_pgm(path, ev) -> None:
+    """2D: binary 16-bit big-endian PGM, value range in the comment line."""
+    if ev.dim != 2:
+        raise ShapeError("PGM evaluation output is 2D only")
+    vals = np.asarray(ev.values, dtype=np.float64).ravel()
+    g = ev.points_per_axis()
+    lo, hi = float(vals.min()), float(vals.max())
+    scale = 65535.0 / (hi - lo) if hi > lo else 0.0
+    t = (vals - lo) * scale  # std::lround: half away from zero
+    words = (np.sign(t) * np.floor(np.abs(t) + 0.5)).astype(np.int64).astype(">u2")
+    with _open_out(path, True) as out:
+        out.write(f"P5\n# min {_fmt(lo)} max {_fmt(hi)}\n{g} {g}\n65535\n".encode())
+        out.write(words.tobytes())
+
+
 # ------------------------------------------------------------------ weight files (io.cpp:299-321)
 def write_weight_file(path, mu) -> None:
     with _open_out(path, False) as out:

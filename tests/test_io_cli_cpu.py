@@ -246,7 +246,7 @@ def test_cli_usage_and_error_exit_codes(tmp_path, capsys):
                      "--scale-J", "2", "-o", str(tmp_path / "c")]) == 4           # count mismatch: ShapeError
     assert cli.main(["reconstruct", str(tmp_path / "f.csv"), str(tmp_path / "y.csv"), "--family", "haar",
                      "--scale-J", "2", "--weighted", "--unweighted", "-o", str(tmp_path / "c")]) == 2
-    assert cli.main(["evaluate", "c", "--resolution", "3", "-o", "e"]) == 2
+    assert cli.main(["evaluate", str(tmp_path / "missing"), "--resolution", "3", "-o", "e"]) == 3
     assert cli.main(["bench", "nosuch"]) == 5
     capsys.readouterr()
 
