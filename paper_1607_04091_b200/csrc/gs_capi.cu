@@ -212,6 +212,8 @@ struct gs_op {
   bool fast2d = false;  // kernels_nfft2d_fast.cuh path (w = 6, p <= 4)
   int cap = 1;          // chunk capacity per problem (2D work list)
   DBuf<int> ch_tile, ch_s0, ch_s1, ch_count, tcs;
+  DBuf<int2> cov;        // per grid coordinate: (tile, offset) of the regions covering it
+  DBuf<int> covn;
   DBuf<unsigned> units;  // fast 2D interpolation work units (k2f_build_units)
   DBuf<int> ucount;
   DBuf<double> wts_x, wts_y;
@@ -253,7 +255,7 @@ void set_smem_attrs() {
   allow_big_smem(k2_cols_fft);
   allow_big_smem(k2_lines_fft);
   allow_big_smem(k2_spread);
-  allow_big_smem(k2_cols_ifft_gather);
+  allow_big_smem(k2_cols_ifft);
   allow_big_smem(k2_rows_ifft_crop);
   allow_big_smem(k2_edges);
   allow_big_smem(k2f_interp<1>);
@@ -374,7 +376,7 @@ void attach_phases(UniP& P, DBuf<cplx>& buf, cudaStream_t st) {
   P.ph_in = buf.p;
   P.ph_out = buf.p + P.n;
 }
-size_t uni_smem(const UniP& P) { return (size_t)P.N2 * sizeof(cplx) * (P.logN2 >= 0 ? 1 : 2); }
+size_t uni_smem(const UniP& P) { return (size_t)(P.logN2 >= 0 ? fpad_len(P.N2) : 2 * P.N2) * sizeof(cplx); }
 
 // ------------------------------------------------------------------ construction
 gs_op* create(const gs_op_desc* dsc) {
@@ -559,7 +561,7 @@ gs_op* create(const gs_op_desc* dsc) {
     P.T = op->fast2d ? F_T : std::min(16, n_ov);
     P.R = P.T + P.S - 1;
     P.nt = (n_ov + P.T - 1) / P.T;
-    P.CW = std::max(1, std::min(8, (int)((120 * 1024) / ((n_ov + 1) * (int)sizeof(cplx)))));
+    P.CW = std::max(1, std::min(8, (int)((120 * 1024) / ((fpad_len(n_ov) + 1) * (int)sizeof(cplx)))));
     while (n_ov % P.CW) --P.CW;
     d_xi_x.upload(xi_x.data(), total, st);
     if (d.dim == 2) d_xi_y.upload(xi_y.data(), total, st);
@@ -644,6 +646,17 @@ gs_op* create(const gs_op_desc* dsc) {
       op->ch_s1.upload(h_1.data(), h_1.size(), st);
       op->ch_count.upload(h_n.data(), h_n.size(), st);
       op->tcs.upload(tcs.data(), tcs.size(), st);
+      {  // coverage of each grid coordinate by tile regions (k2_fold_tiles)
+        std::vector<int2> hc((size_t)n_ov * MAX_COVER, int2{0, 0});
+        std::vector<int> hn(n_ov);
+        int tl[MAX_COVER], ll[MAX_COVER];
+        for (int r = 0; r < n_ov; ++r) {
+          hn[r] = cover(r, P.T, P.R, P.nt, n_ov, tl, ll);
+          for (int k = 0; k < hn[r]; ++k) hc[(size_t)r * MAX_COVER + k] = int2{tl[k], ll[k]};
+        }
+        op->cov.upload(hc.data(), hc.size(), st);
+        op->covn.upload(hn.data(), hn.size(), st);
+      }
       if (op->fast2d) {
         op->units.alloc(total);
         op->ucount.alloc((size_t)B * cap);
@@ -723,7 +736,7 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
     }
     case GS_ROUTE_NFFT_1D: {
       const NfP& P = op->np;
-      k_n1_embed_fft<<<B, 256, P.n_ov * sizeof(cplx), st>>>(P, x, op->deconv.p, op->G.p, op->tw.p, op->logLmax);
+      k_n1_embed_fft<<<B, 256, fpad_len(P.n_ov) * sizeof(cplx), st>>>(P, x, op->deconv.p, op->G.p, op->tw.p, op->logLmax);
       pmark("k_n1_embed_fft", st);
       k_n1_interp<<<dim3(nblk(op->M, 128), B), 128, 0, st>>>(P, op->base_x.p, op->wts_x.p, op->rec_x.p, op->G.p, x,
                                                               perm_io ? op->perm.p : nullptr, y);
@@ -732,14 +745,14 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
     }
     case GS_ROUTE_NFFT_2D: {
       const NfP& P = op->np;
-      k2_rows_embed_fft<<<dim3(P.n, B), 256, P.n_ov * sizeof(cplx), st>>>(P, x, op->deconv.p, op->G.p, op->tw.p,
+      k2_rows_embed_fft<<<dim3(P.n, B), 256, fpad_len(P.n_ov) * sizeof(cplx), st>>>(P, x, op->deconv.p, op->G.p, op->tw.p,
                                                                           op->logLmax);
       pmark("k2_rows_embed_fft", st);
-      k2_cols_fft<<<dim3(P.n_ov / P.CW, B), 256, (size_t)P.CW * (P.n_ov + 1) * sizeof(cplx), st>>>(P, op->G.p, op->tw.p,
+      k2_cols_fft<<<dim3(P.n_ov / P.CW, B), 256, (size_t)P.CW * (fpad_len(P.n_ov) + 1) * sizeof(cplx), st>>>(P, op->G.p, op->tw.p,
                                                                                                    op->logLmax);
       pmark("k2_cols_fft", st);
       if (P.edges) {
-        k2_lines_fft<<<dim3(4 * P.p, B), 256, P.n_ov * sizeof(cplx), st>>>(P, x, op->deconv.p, op->lines.p, op->tw.p,
+        k2_lines_fft<<<dim3(4 * P.p, B), 256, fpad_len(P.n_ov) * sizeof(cplx), st>>>(P, x, op->deconv.p, op->lines.p, op->tw.p,
                                                                            op->logLmax);
         pmark("k2_lines_fft", st);
       }
@@ -799,7 +812,7 @@ void adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
       k_n1_spread<<<dim3(nblk(P.n_ov, 128), B), 128, 0, st>>>(P, op->bins.p, op->wts_x.p, op->rec_x.p, y,
                                                                perm_io ? op->perm.p : nullptr, op->G.p);
       pmark("k_n1_spread", st);
-      k_n1_ifft_crop<<<B, 256, P.n_ov * sizeof(cplx), st>>>(P, op->G.p, op->deconv.p, op->rec_x.p, y,
+      k_n1_ifft_crop<<<B, 256, fpad_len(P.n_ov) * sizeof(cplx), st>>>(P, op->G.p, op->deconv.p, op->rec_x.p, y,
                                                             perm_io ? op->perm.p : nullptr, z, op->tw.p, op->logLmax);
       pmark("k_n1_ifft_crop", st);
       break;
@@ -829,10 +842,13 @@ void adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
             perm_io ? op->perm.p : nullptr, op->TB.p, op->TL.p, op->TC.p);
         pmark("k2_spread", st);
       }
-      k2_cols_ifft_gather<<<dim3(P.n_ov / P.CW, B), 256, (size_t)P.CW * (P.n_ov + 1) * sizeof(cplx), st>>>(
-          P, op->TB.p, op->tcs.p, op->cap, op->G.p, op->tw.p, op->logLmax);
-      pmark("k2_cols_ifft_gather", st);
-      k2_rows_ifft_crop<<<dim3(P.n, B), 256, P.n_ov * sizeof(cplx), st>>>(P, op->G.p, op->deconv.p, z, op->tw.p,
+      k2_fold_tiles<<<dim3(P.nt * P.nt, B), (P.T * P.T + 31) / 32 * 32, 0, st>>>(P, op->TB.p, op->tcs.p, op->cap,
+                                                                                op->cov.p, op->covn.p, op->G.p);
+      pmark("k2_fold_tiles", st);
+      k2_cols_ifft<<<dim3(P.n_ov / P.CW, B), 256, (size_t)P.CW * (fpad_len(P.n_ov) + 1) * sizeof(cplx), st>>>(
+          P, op->G.p, op->tw.p, op->logLmax);
+      pmark("k2_cols_ifft", st);
+      k2_rows_ifft_crop<<<dim3(P.n, B), 256, fpad_len(P.n_ov) * sizeof(cplx), st>>>(P, op->G.p, op->deconv.p, z, op->tw.p,
                                                                           op->logLmax);
       pmark("k2_rows_ifft_crop", st);
       if (P.edges) {
@@ -843,7 +859,7 @@ void adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
         k2_fold_corners<<<dim3(nblk(ngroups * 4 * P.p * P.p, 128), B), 128, 0, st>>>(
             P, op->TC.p, op->ch_count.p, op->cap, ngroups, op->TCF.p);
         pmark("k2_fold_corners", st);
-        k2_edges<<<dim3(4 * P.p + 1, B), 256, P.n_ov * sizeof(cplx), st>>>(
+        k2_edges<<<dim3(4 * P.p + 1, B), 256, fpad_len(P.n_ov) * sizeof(cplx), st>>>(
             P, op->TLF.p, op->TCF.p, op->tcs.p, op->ch_count.p, op->cap, op->deconv.p, z, op->tw.p, op->logLmax);
         pmark("k2_edges", st);
       }

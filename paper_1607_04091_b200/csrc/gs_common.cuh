@@ -62,6 +62,65 @@ __device__ __forceinline__ void block_fft_bitrev(cplx* buf, int logL, int count,
   }
 }
 
+// ---------------------------------------------------------------------------
+// Same transform as block_fft_bitrev (bit-reversed input, natural output,
+// identical butterflies and twiddles in the same stage order -> bit-identical
+// results) with three radix-2 stages fused per pass in registers: a thread
+// loads 8 elements at stride h, runs stages s, s+1, s+2 on them and stores
+// them back, so a 512-point line takes 3 shared-memory round trips and 3
+// barriers instead of 9.  Element i of line c lives at buf[c*lstride + fpad(i)]
+// (one pad slot per 8 elements keeps the stride-8 first pass conflict-free).
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ int fpad(int i) { return i + (i >> 3); }
+__host__ __device__ __forceinline__ int fpad_len(int L) { return L + (L >> 3); }
+
+template <int NST>
+__device__ __forceinline__ void fft_fused_pass(cplx* buf, int logL, int s, int count, int lstride,
+                                               const cplx* __restrict__ tw, int logLmax, int sign) {
+  constexpr int G = 1 << NST;
+  const int h = 1 << (s - 1);
+  const int per = (1 << logL) / G;
+  const int groups = count * per;
+  for (int t = threadIdx.x; t < groups; t += blockDim.x) {
+    const int c = t / per, j = t - c * per;
+    const int jh = j & (h - 1);
+    const int i0 = (j >> (s - 1)) * (G * h) + jh;
+    cplx* base = buf + c * lstride;
+    cplx v[G];
+#pragma unroll
+    for (int m = 0; m < G; ++m) v[m] = base[fpad(i0 + m * h)];
+#pragma unroll
+    for (int q = 0; q < NST; ++q) {
+      const int twshift = logLmax - (s + q);
+#pragma unroll
+      for (int m = 0; m < G; ++m) {
+        if ((m >> q) & 1) continue;
+        const int k = jh + (m & ((1 << q) - 1)) * h;
+        cplx w = ldg2(tw + (k << twshift));
+        if (sign > 0) w.y = -w.y;
+        const cplx u = v[m], x = cmul(v[m + (1 << q)], w);
+        v[m] = cadd(u, x);
+        v[m + (1 << q)] = csub(u, x);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < G; ++m) base[fpad(i0 + m * h)] = v[m];
+  }
+}
+
+__device__ __forceinline__ void block_fft_padded(cplx* buf, int logL, int count, int lstride,
+                                                 const cplx* __restrict__ tw, int logLmax, int sign) {
+  int s = 1;
+  while (s <= logL) {
+    const int nst = logL - s + 1 >= 3 ? 3 : logL - s + 1;
+    if (nst == 3) fft_fused_pass<3>(buf, logL, s, count, lstride, tw, logLmax, sign);
+    else if (nst == 2) fft_fused_pass<2>(buf, logL, s, count, lstride, tw, logLmax, sign);
+    else fft_fused_pass<1>(buf, logL, s, count, lstride, tw, logLmax, sign);
+    __syncthreads();
+    s += nst;
+  }
+}
+
 __device__ __forceinline__ int bitrev(int i, int logL) { return (int)(__brev((unsigned)i) >> (32 - logL)); }
 
 // Direct DFT fallback (non power-of-two lengths, uniform route only):

@@ -34,18 +34,18 @@ __global__ void k_n1_embed_fft(NfP P, const cplx* __restrict__ x, const double* 
   const int prob = blockIdx.x;
   x += (int64_t)prob * P.n;
   G += (int64_t)prob * P.n_ov;
-  for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) sm[i] = mk(0, 0);
+  for (int i = threadIdx.x; i < fpad_len(P.n_ov); i += blockDim.x) sm[i] = mk(0, 0);
   __syncthreads();
   for (int idx = threadIdx.x; idx < P.n; idx += blockDim.x) {
     int k = idx - P.n / 2;
     cplx v = x[idx];
     if (P.edges && (idx < P.p || idx >= P.n - P.p)) v = mk(0, 0);
     int pos = (k + P.n_ov) & (P.n_ov - 1);
-    sm[bitrev(pos, P.log_nov)] = cscale(v, deconv[idx]);
+    sm[fpad(bitrev(pos, P.log_nov))] = cscale(v, deconv[idx]);
   }
   __syncthreads();
-  block_fft_bitrev(sm, P.log_nov, 1, 0, tw, logLmax, -1);
-  for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) G[i] = sm[i];
+  block_fft_padded(sm, P.log_nov, 1, 0, tw, logLmax, -1);
+  for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) G[i] = sm[fpad(i)];
 }
 
 // interpolation + D + L/R  (nufft.cpp:273-284, freq2wave.cpp:232-236)
@@ -110,12 +110,12 @@ __global__ void k_n1_ifft_crop(NfP P, const cplx* __restrict__ line, const doubl
   const int prob = blockIdx.x;
   line += (int64_t)prob * P.n_ov;
   z += (int64_t)prob * P.n;
-  for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) sm[bitrev(i, P.log_nov)] = line[i];
+  for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) sm[fpad(bitrev(i, P.log_nov))] = line[i];
   __syncthreads();
-  block_fft_bitrev(sm, P.log_nov, 1, 0, tw, logLmax, +1);
+  block_fft_padded(sm, P.log_nov, 1, 0, tw, logLmax, +1);
   for (int idx = threadIdx.x; idx < P.n; idx += blockDim.x) {
     int k = idx - P.n / 2;
-    cplx v = cscale(sm[(k + P.n_ov) & (P.n_ov - 1)], deconv[idx]);
+    cplx v = cscale(sm[fpad((k + P.n_ov) & (P.n_ov - 1))], deconv[idx]);
     if (P.edges && (idx < P.p || idx >= P.n - P.p)) v = mk(0, 0);
     z[idx] = v;
   }
@@ -160,38 +160,38 @@ __global__ void k2_rows_embed_fft(NfP P, const cplx* __restrict__ x, const doubl
     return;
   }
   const cplx* xr = x + (int64_t)prob * P.n * P.n + (int64_t)j * P.n;
-  for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) sm[i] = mk(0, 0);
+  for (int i = threadIdx.x; i < fpad_len(P.n_ov); i += blockDim.x) sm[i] = mk(0, 0);
   __syncthreads();
   const double d0 = deconv[j];
   for (int i = threadIdx.x; i < P.n; i += blockDim.x) {
     cplx v = xr[i];
     if (P.edges && (i < P.p || i >= P.n - P.p)) v = mk(0, 0);
     int pos = (i - P.n / 2 + P.n_ov) & (P.n_ov - 1);
-    sm[bitrev(pos, P.log_nov)] = cscale(v, d0 * deconv[i]);
+    sm[fpad(bitrev(pos, P.log_nov))] = cscale(v, d0 * deconv[i]);
   }
   __syncthreads();
-  block_fft_bitrev(sm, P.log_nov, 1, 0, tw, logLmax, -1);
-  for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) grow[i] = sm[i];
+  block_fft_padded(sm, P.log_nov, 1, 0, tw, logLmax, -1);
+  for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) grow[i] = sm[fpad(i)];
 }
 
 // FFT_{-} along y of CW columns; only the n rows carrying data are loaded
 __global__ void k2_cols_fft(NfP P, cplx* __restrict__ G, const cplx* __restrict__ tw, int logLmax) {
   extern __shared__ cplx sm[];
   const int c0 = blockIdx.x * P.CW, prob = blockIdx.y;
-  const int ls = P.n_ov + 1;
+  const int ls = fpad_len(P.n_ov) + 1;
   cplx* g = G + (int64_t)prob * P.n_ov * P.n_ov;
   for (int i = threadIdx.x; i < P.CW * ls; i += blockDim.x) sm[i] = mk(0, 0);
   __syncthreads();
   for (int t = threadIdx.x; t < P.n * P.CW; t += blockDim.x) {
     const int jj = t / P.CW, cc = t - jj * P.CW;
     const int r = (jj - P.n / 2 + P.n_ov) & (P.n_ov - 1);
-    sm[cc * ls + bitrev(r, P.log_nov)] = g[(int64_t)r * P.n_ov + c0 + cc];
+    sm[cc * ls + fpad(bitrev(r, P.log_nov))] = g[(int64_t)r * P.n_ov + c0 + cc];
   }
   __syncthreads();
-  block_fft_bitrev(sm, P.log_nov, P.CW, ls, tw, logLmax, -1);
+  block_fft_padded(sm, P.log_nov, P.CW, ls, tw, logLmax, -1);
   for (int t = threadIdx.x; t < P.n_ov * P.CW; t += blockDim.x) {
     const int r = t / P.CW, cc = t - r * P.CW;
-    g[(int64_t)r * P.n_ov + c0 + cc] = sm[cc * ls + r];
+    g[(int64_t)r * P.n_ov + c0 + cc] = sm[cc * ls + fpad(r)];
   }
 }
 
@@ -209,17 +209,17 @@ __global__ void k2_lines_fft(NfP P, const cplx* __restrict__ x, const double* __
   const int e = yline ? L : L - twop;
   const int fixed = edge_index(e, P.n, P.p);
   const cplx* X = x + (int64_t)prob * P.n * P.n;
-  for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) sm[i] = mk(0, 0);
+  for (int i = threadIdx.x; i < fpad_len(P.n_ov); i += blockDim.x) sm[i] = mk(0, 0);
   __syncthreads();
   for (int v = P.p + threadIdx.x; v < P.n - P.p; v += blockDim.x) {
     cplx val = yline ? X[(int64_t)v * P.n + fixed] : X[(int64_t)fixed * P.n + v];
     int pos = (v - P.n / 2 + P.n_ov) & (P.n_ov - 1);
-    sm[bitrev(pos, P.log_nov)] = cscale(val, deconv[v]);
+    sm[fpad(bitrev(pos, P.log_nov))] = cscale(val, deconv[v]);
   }
   __syncthreads();
-  block_fft_bitrev(sm, P.log_nov, 1, 0, tw, logLmax, -1);
+  block_fft_padded(sm, P.log_nov, 1, 0, tw, logLmax, -1);
   cplx* out = lines + ((int64_t)prob * 2 * twop + L) * P.n_ov;
-  for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) out[i] = sm[i];
+  for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) out[i] = sm[fpad(i)];
 }
 
 // Per-point forward: 2D interpolation (nufft.cpp:287-303) scaled by Dx Dy,
@@ -408,7 +408,7 @@ k2_spread(NfP P, const int* __restrict__ tile_start, const int* __restrict__ bas
 // (tile, local offset) pairs: region of tile t spans [t*T, t*T + R) mod n_ov;
 // the last tile may be partial (n_ov need not be a multiple of T).
 #define MAX_COVER 8
-__device__ __forceinline__ int cover(int r, int T, int R, int nt, int n_ov, int* tl, int* ll) {
+__host__ __device__ __forceinline__ int cover(int r, int T, int R, int nt, int n_ov, int* tl, int* ll) {
   int k = 0;
   const int dmax = (R + T - 1) / T;
   for (int d = 0; d <= dmax && d < nt; ++d) {
@@ -422,43 +422,52 @@ __device__ __forceinline__ int cover(int r, int T, int R, int nt, int n_ov, int*
   return k;
 }
 
-// Sum over every chunk of every covering tile of its region entry at cell (r, c)
-// (chunks of a tile: tcs[tile] .. tcs[tile+1]; TBp already offset to the problem)
-__device__ __forceinline__ cplx gather_cell(const NfP& P, const cplx* __restrict__ TBp, const int* __restrict__ tcs,
-                                            int r, int c) {
-  cplx a = mk(0, 0);
-  int ty[MAX_COVER], ly[MAX_COVER], tx[MAX_COVER], lx[MAX_COVER];
-  const int ny = cover(r, P.T, P.R, P.nt, P.n_ov, ty, ly);
-  const int nx = cover(c, P.T, P.R, P.nt, P.n_ov, tx, lx);
-  for (int i = 0; i < ny; ++i)
-    for (int j = 0; j < nx; ++j) {
-      const int tile = ty[i] * P.nt + tx[j];
-      for (int ch = tcs[tile]; ch < tcs[tile + 1]; ++ch)
-        a = cadd(a, ldg2(TBp + ((int64_t)ch * P.R + ly[i]) * P.R + lx[j]));
-    }
-  return a;
-}
-
-// gather tile regions -> FFT_{+} along y for CW columns -> G (rows that the
-// crop keeps only)
-__global__ void k2_cols_ifft_gather(NfP P, const cplx* __restrict__ TB, const int* __restrict__ tcs_all, int cap,
-                                    cplx* __restrict__ G, const cplx* __restrict__ tw, int logLmax) {
-  extern __shared__ cplx sm[];
-  const int c0 = blockIdx.x * P.CW, prob = blockIdx.y;
-  const int ls = P.n_ov + 1;
+// Fold the per-chunk adjoint partials into the oversampled grid: one CTA per
+// (tile, problem) writes the tile's T x T core cells of G, each the sum over
+// every chunk of every tile whose (T+S-1)^2 region covers the cell (coverage
+// per coordinate precomputed in cov / covn, same order as cover()).  Reads of
+// the partial rows are contiguous along x; every G cell is written once.
+__global__ void k2_fold_tiles(NfP P, const cplx* __restrict__ TB, const int* __restrict__ tcs_all, int cap,
+                              const int2* __restrict__ cov, const int* __restrict__ covn, cplx* __restrict__ G) {
+  const int tile = blockIdx.x, prob = blockIdx.y;
+  const int ty = tile / P.nt, tx = tile - ty * P.nt;
   const cplx* TBp = TB + (int64_t)prob * cap * P.R * P.R;
   const int* tcs = tcs_all + (int64_t)prob * (P.nt * P.nt + 1);
+  cplx* g = G + (int64_t)prob * P.n_ov * P.n_ov;
+  for (int q = threadIdx.x; q < P.T * P.T; q += blockDim.x) {
+    const int r = ty * P.T + q / P.T, c = tx * P.T + q % P.T;
+    if (r >= P.n_ov || c >= P.n_ov) continue;
+    cplx a = mk(0, 0);
+    const int ny = covn[r], nx = covn[c];
+    for (int i = 0; i < ny; ++i) {
+      const int2 yv = cov[r * MAX_COVER + i];
+      for (int j = 0; j < nx; ++j) {
+        const int2 xv = cov[c * MAX_COVER + j];
+        const int tl = yv.x * P.nt + xv.x;
+        for (int ch = tcs[tl]; ch < tcs[tl + 1]; ++ch)
+          a = cadd(a, ldg2(TBp + ((int64_t)ch * P.R + yv.y) * P.R + xv.y));
+      }
+    }
+    g[(int64_t)r * P.n_ov + c] = a;
+  }
+}
+
+// FFT_{+} along y for CW columns of G; only the rows the crop keeps are written
+__global__ void k2_cols_ifft(NfP P, cplx* __restrict__ G, const cplx* __restrict__ tw, int logLmax) {
+  extern __shared__ cplx sm[];
+  const int c0 = blockIdx.x * P.CW, prob = blockIdx.y;
+  const int ls = fpad_len(P.n_ov) + 1;
+  cplx* g = G + (int64_t)prob * P.n_ov * P.n_ov;
   for (int t = threadIdx.x; t < P.n_ov * P.CW; t += blockDim.x) {
     const int r = t / P.CW, cc = t - r * P.CW;
-    sm[cc * ls + bitrev(r, P.log_nov)] = gather_cell(P, TBp, tcs, r, c0 + cc);
+    sm[cc * ls + fpad(bitrev(r, P.log_nov))] = g[(int64_t)r * P.n_ov + c0 + cc];
   }
   __syncthreads();
-  block_fft_bitrev(sm, P.log_nov, P.CW, ls, tw, logLmax, +1);
-  cplx* g = G + (int64_t)prob * P.n_ov * P.n_ov;
+  block_fft_padded(sm, P.log_nov, P.CW, ls, tw, logLmax, +1);
   for (int t = threadIdx.x; t < P.n * P.CW; t += blockDim.x) {
     const int jj = t / P.CW, cc = t - jj * P.CW;
     const int r = (jj - P.n / 2 + P.n_ov) & (P.n_ov - 1);
-    g[(int64_t)r * P.n_ov + c0 + cc] = sm[cc * ls + r];
+    g[(int64_t)r * P.n_ov + c0 + cc] = sm[cc * ls + fpad(r)];
   }
 }
 
@@ -475,12 +484,12 @@ __global__ void k2_rows_ifft_crop(NfP P, const cplx* __restrict__ G, const doubl
   }
   const int r = (j - P.n / 2 + P.n_ov) & (P.n_ov - 1);
   const cplx* grow = G + ((int64_t)prob * P.n_ov + r) * P.n_ov;
-  for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) sm[bitrev(i, P.log_nov)] = grow[i];
+  for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) sm[fpad(bitrev(i, P.log_nov))] = grow[i];
   __syncthreads();
-  block_fft_bitrev(sm, P.log_nov, 1, 0, tw, logLmax, +1);
+  block_fft_padded(sm, P.log_nov, 1, 0, tw, logLmax, +1);
   const double d0 = deconv[j];
   for (int i = threadIdx.x; i < P.n; i += blockDim.x) {
-    cplx v = cscale(sm[(i - P.n / 2 + P.n_ov) & (P.n_ov - 1)], d0 * deconv[i]);
+    cplx v = cscale(sm[fpad((i - P.n / 2 + P.n_ov) & (P.n_ov - 1))], d0 * deconv[i]);
     if (P.edges && (i < P.p || i >= P.n - P.p)) v = mk(0, 0);
     zr[i] = v;
   }
@@ -562,13 +571,13 @@ __global__ void k2_edges(NfP P, const cplx* __restrict__ TLF, const cplx* __rest
     int tk[MAX_COVER], lk[MAX_COVER];
     const int nc = cover(pos, T, R, nt, P.n_ov, tk, lk);
     for (int i = 0; i < nc; ++i) a = cadd(a, TLFp[((int64_t)tk[i] * twop + e) * R + lk[i]]);
-    sm[bitrev(pos, P.log_nov)] = a;
+    sm[fpad(bitrev(pos, P.log_nov))] = a;
   }
   __syncthreads();
-  block_fft_bitrev(sm, P.log_nov, 1, 0, tw, logLmax, +1);
+  block_fft_padded(sm, P.log_nov, 1, 0, tw, logLmax, +1);
   const int fixed = edge_index(e, n, p);
   for (int v = p + threadIdx.x; v < n - p; v += blockDim.x) {
-    cplx val = cscale(sm[(v - n / 2 + P.n_ov) & (P.n_ov - 1)], deconv[v]);
+    cplx val = cscale(sm[fpad((v - n / 2 + P.n_ov) & (P.n_ov - 1))], deconv[v]);
     if (yline) Z[(int64_t)v * n + fixed] = val;  // Z(i_e, j)
     else Z[(int64_t)fixed * n + v] = val;        // Z(i, j_e)
   }

@@ -37,19 +37,20 @@ __global__ void k_uni_fwd(UniP P, const cplx* __restrict__ x, Strided xs, const 
   if (post) post += prob * post_prob + vec * ys.vec;
   const bool pow2 = P.logN2 >= 0;
   const int R = 1 + (P.edges ? 2 * P.p : 0);
-  for (int i = threadIdx.x; i < P.N2; i += blockDim.x) sm[i] = mk(0, 0);
+  const int slots = pow2 ? fpad_len(P.N2) : P.N2;  // power-of-two lengths use the padded FFT layout
+  for (int i = threadIdx.x; i < slots; i += blockDim.x) sm[i] = mk(0, 0);
   __syncthreads();
   for (int l = threadIdx.x; l < P.n; l += blockDim.x) {
     cplx v = x[l * xs.elem];
     if (P.edges && (l < P.p || l >= P.n - P.p)) v = mk(0, 0);  // freq2wave.cpp:224-230
     cplx z = cmul(v, ldg2(P.ph_in + l));
     int pos = P.q * l;
-    sm[pow2 ? bitrev(pos, P.logN2) : pos] = z;
+    sm[pow2 ? fpad(bitrev(pos, P.logN2)) : pos] = z;
   }
   __syncthreads();
   cplx* Z = sm;
   if (pow2) {
-    block_fft_bitrev(sm, P.logN2, 1, 0, tw, logLmax, -1);
+    block_fft_padded(sm, P.logN2, 1, 0, tw, logLmax, -1);
   } else {
     block_dft(sm, sm + P.N2, P.N2, -1);
     Z = sm + P.N2;
@@ -61,7 +62,7 @@ __global__ void k_uni_fwd(UniP P, const cplx* __restrict__ x, Strided xs, const 
       xt[c] = x[(P.n - P.p + c) * xs.elem];
     }
   for (int m = threadIdx.x; m < P.M; m += blockDim.x) {
-    cplx o = cmul(ldg2(P.ph_out + m), Z[m]);
+    cplx o = cmul(ldg2(P.ph_out + m), Z[pow2 ? fpad(m) : m]);
     const cplx* r = rec + (int64_t)m * R;
     cplx ym = cmul(r[0], o);
     if (P.edges) {
@@ -89,7 +90,8 @@ __global__ void k_uni_adj(UniP P, const cplx* __restrict__ y, Strided ys, const 
   if (pre) pre += prob * pre_prob + vec * ys.vec;
   const bool pow2 = P.logN2 >= 0;
   const int R = 1 + (P.edges ? 2 * P.p : 0);
-  for (int i = threadIdx.x; i < P.N2; i += blockDim.x) sm[i] = mk(0, 0);
+  const int slots = pow2 ? fpad_len(P.N2) : P.N2;
+  for (int i = threadIdx.x; i < slots; i += blockDim.x) sm[i] = mk(0, 0);
   __syncthreads();
   cplx eh[8], et[8];
   for (int c = 0; c < 8; ++c) eh[c] = et[c] = mk(0, 0);
@@ -99,7 +101,7 @@ __global__ void k_uni_adj(UniP P, const cplx* __restrict__ y, Strided ys, const 
     const cplx* r = rec + (int64_t)m * R;
     cplx v = cmul(conj_(r[0]), u);  // freq2wave.cpp:315
     cplx val = cmul(v, conj_(ldg2(P.ph_out + m)));  // e^{-i pi N xi_m}, nufft.cpp:443-445
-    sm[pow2 ? bitrev(m, P.logN2) : m] = val;
+    sm[pow2 ? fpad(bitrev(m, P.logN2)) : m] = val;
     if (P.edges)
       for (int c = 0; c < P.p; ++c) {
         eh[c] = cadd(eh[c], cmul(conj_(r[1 + c]), u));
@@ -109,13 +111,13 @@ __global__ void k_uni_adj(UniP P, const cplx* __restrict__ y, Strided ys, const 
   __syncthreads();
   cplx* Z = sm;
   if (pow2) {
-    block_fft_bitrev(sm, P.logN2, 1, 0, tw, logLmax, +1);
+    block_fft_padded(sm, P.logN2, 1, 0, tw, logLmax, +1);
   } else {
     block_dft(sm, sm + P.N2, P.N2, +1);
     Z = sm + P.N2;
   }
   for (int l = threadIdx.x; l < P.n; l += blockDim.x) {
-    cplx v = cmul(Z[P.q * l], conj_(ldg2(P.ph_in + l)));
+    cplx v = cmul(Z[pow2 ? fpad(P.q * l) : P.q * l], conj_(ldg2(P.ph_in + l)));
     if (P.edges && (l < P.p || l >= P.n - P.p)) v = mk(0, 0);  // freq2wave.cpp:318-321
     z[l * zs.elem] = v;
   }
