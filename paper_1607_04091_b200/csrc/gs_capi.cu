@@ -266,6 +266,10 @@ void set_smem_attrs() {
   allow_big_smem(k2f_spread<2>);
   allow_big_smem(k2f_spread<3>);
   allow_big_smem(k2f_spread<4>);
+  allow_big_smem(k2f_spread_mma<1>);
+  allow_big_smem(k2f_spread_mma<2>);
+  allow_big_smem(k2f_spread_mma<3>);
+  allow_big_smem(k2f_spread_mma<4>);
   done = true;
 }
 
@@ -697,6 +701,16 @@ struct Prof {
 };
 Prof g_prof;
 std::atomic<long long> g_launches{0};  // kernels this library has launched (gs_launch_count)
+// 2D spreading variant: FP64 tensor cores (default) or the lane-per-column
+// DFMA kernel (GS_B200_SPREAD=dfma, for A/B measurements)
+bool spread_mma() {
+  static const bool on = [] {
+    const char* e = std::getenv("GS_B200_SPREAD");
+    return !(e && std::string(e) == "dfma");
+  }();
+  return on;
+}
+
 void pmark(const char* name, cudaStream_t st) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   if (!g_prof.on) return;
@@ -824,9 +838,14 @@ void adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
         const dim3 grid(op->cap, B);
         const int* pp = perm_io ? op->perm.p : nullptr;
 #define GS_F_SPREAD(PP)                                                                                          \
-  k2f_spread<PP><<<grid, 32 * F_WARPS, FSpread<PP>::bytes(), st>>>(                                          \
-      P, op->ch_tile.p, op->ch_s0.p, op->ch_s1.p, op->ch_count.p, op->cap, op->base_x.p, op->base_y.p,            \
-      op->wts_x.p, op->wts_y.p, op->rec_x.p, op->rec_y.p, y, pp, op->TB.p, op->TL.p, op->TC.p)
+  if (spread_mma())                                                                                              \
+    k2f_spread_mma<PP><<<grid, 32 * F_WARPS, FSpreadM<PP>::bytes(), st>>>(                                     \
+        P, op->ch_tile.p, op->ch_s0.p, op->ch_s1.p, op->ch_count.p, op->cap, op->base_x.p, op->base_y.p,          \
+        op->wts_x.p, op->wts_y.p, op->rec_x.p, op->rec_y.p, y, pp, op->TB.p, op->TL.p, op->TC.p);                 \
+  else                                                                                                           \
+    k2f_spread<PP><<<grid, 32 * F_WARPS, FSpread<PP>::bytes(), st>>>(                                          \
+        P, op->ch_tile.p, op->ch_s0.p, op->ch_s1.p, op->ch_count.p, op->cap, op->base_x.p, op->base_y.p,          \
+        op->wts_x.p, op->wts_y.p, op->rec_x.p, op->rec_y.p, y, pp, op->TB.p, op->TL.p, op->TC.p)
         switch (op->p) {
           case 1: GS_F_SPREAD(1); break;
           case 2: GS_F_SPREAD(2); break;

@@ -573,3 +573,219 @@ k2f_spread(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ ch_s
     }
   }
 }
+
+// ------------------------------------------------------------------ spreading on the FP64 tensor cores
+// k2f_spread_mma: the same chunk outputs as k2f_spread, computed as small
+// real GEMMs over the chunk's samples with mma.sync m8n8k4 f64 (DMMA; B200's
+// FP64 tensor rate equals its DFMA rate, but one DMMA does 256 FMAs, so the
+// kernel issues ~8x fewer instructions than the lane-per-column form and
+// needs no shared-memory broadcasts).  Warp w owns the sample rows
+// [3w, 3w+3) of the tile (accumulator rows band0 .. band0+15); K = the warp's
+// samples, 4 per step.  With thread (g, t) = (lane/4, lane%4) and s_t the
+// step's t-th sample:
+//   region  G(r, c)   += sum_s wy_s(r - oy_s) [wx_s(c - ox_s) v2_s]     A1 x B1  (re | im column halves)
+//   y-lines LY(e, r)  += sum_s vy_e(s) wy_s(r - oy_s)                   [vy re; im] x A1^T
+//   x-lines LX(e, c)  += sum_s vx_e(s) wx_s(c - ox_s)                   [vx re; im] x B3
+//   corners P(i', j') += sum_s [ca re; im](i) [b re | im](j)            -> C = ca conj(b)
+// with v2 = conj(Dx Dy) y, vx_e = conj(By_e Dx) y, ca_i = conj(Ax_i) y,
+// vy_e = conj(Ax_e Dy) y (freq2wave.cpp:332-385).  The fragment values are
+// gathered straight from the staged chunk: A1(r, s_t) and the B2 operand of
+// the y-lines are the same register, B3 is the bare column tap.
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+template <int P>
+struct FSpreadM {
+  static constexpr int E = P >= 2 ? 2 * P : 0;
+  // per-warp fold record: region 16 x 24 (complex), y-lines 8 x 16, x-lines 8 x 24 (complex), corner P 16 x 16 (real)
+  static constexpr int REG = 16 * F_R, LYN = 8 * 16, LXN = 8 * F_R, PN = 16 * 16 / 2;  // in complex units
+  static constexpr int PER_WARP = REG + LYN + LXN + PN;
+  static constexpr size_t FOLD = sizeof(cplx) * F_WARPS * PER_WARP;
+  static constexpr size_t MAIN = (FSpread<P>::STG_END > FOLD ? FSpread<P>::STG_END : FOLD);
+  static constexpr size_t bytes() { return (MAIN + 15) / 16 * 16; }
+};
+
+template <int P>
+__global__ void __launch_bounds__(32 * F_WARPS, 2)
+k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ ch_s0, const int* __restrict__ ch_s1,
+               const int* __restrict__ ch_count, int cap, const int* __restrict__ base_x,
+               const int* __restrict__ base_y, const double* __restrict__ wx_all, const double* __restrict__ wy_all,
+               const cplx* __restrict__ recx_all, const cplx* __restrict__ recy_all, const cplx* __restrict__ yin,
+               const int* __restrict__ in_perm, cplx* __restrict__ TB, cplx* __restrict__ TL, cplx* __restrict__ TC) {
+  using F = FSpread<P>;
+  using FM = FSpreadM<P>;
+  constexpr int S = F_S, T = F_T, R = F_R, BAND = F_BAND, E = F::E, RR = F::RR, NCE = F::NCE;
+  extern __shared__ __align__(16) unsigned char fsm_raw[];
+  cplx* s_ys = reinterpret_cast<cplx*>(fsm_raw + F::STG_YS);
+  int* s_ox = reinterpret_cast<int*>(fsm_raw + F::STG_OX);
+  __shared__ int rs[T + 1];
+  __shared__ unsigned char s_oy[F_CHUNK];
+  const int prob = blockIdx.y, c = blockIdx.x;
+  if (c >= ch_count[prob]) return;
+  const int tile = ch_tile[prob * cap + c], s0 = ch_s0[prob * cap + c], s1 = ch_s1[prob * cap + c];
+  const int n = s1 - s0;
+  const int ty = tile / Pp.nt, tx = tile - ty * Pp.nt;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int64_t g0 = (int64_t)prob * Pp.M + s0;
+  // ---- stage the chunk (as k2f_spread)
+  const double* s_wy = reinterpret_cast<const double*>(f_stage(fsm_raw + F::STG_WY, wy_all + g0 * S, sizeof(double) * S * n));
+  const double* s_wx = reinterpret_cast<const double*>(f_stage(fsm_raw + F::STG_WX, wx_all + g0 * S, sizeof(double) * S * n));
+  const cplx* s_rx = reinterpret_cast<const cplx*>(f_stage(fsm_raw + F::STG_RX, recx_all + g0 * RR, sizeof(cplx) * RR * n));
+  const cplx* s_ry = reinterpret_cast<const cplx*>(f_stage(fsm_raw + F::STG_RY, recy_all + g0 * RR, sizeof(cplx) * RR * n));
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int64_t gs = g0 + i;
+    s_ys[i] = ldg2(yin + (int64_t)prob * Pp.M + (in_perm ? (int64_t)in_perm[gs] : (int64_t)(s0 + i)));
+    s_ox[i] = base_x[gs] - tx * T;
+    s_oy[i] = (unsigned char)(base_y[gs] - ty * T);
+  }
+  f_stage_wait();
+  __syncthreads();
+  if (threadIdx.x <= T) {  // row starts (samples are sorted by cell, row-major, in a tile)
+    const int key = threadIdx.x;
+    int lo = 0, hi = n;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((int)s_oy[mid] < key) lo = mid + 1;
+      else hi = mid;
+    }
+    rs[threadIdx.x] = lo;
+  }
+  __syncthreads();
+  const int band0 = warp * BAND;
+  const int sa = rs[band0], sb = rs[band0 + BAND];
+  double rg[2][6][2], ly[2][2][2], lx[2][3][2], co[2][2][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+#pragma unroll
+    for (int j = 0; j < 6; ++j) rg[i][j][0] = rg[i][j][1] = 0.0;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) ly[i][j][0] = ly[i][j][1] = co[i][j][0] = co[i][j][1] = 0.0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) lx[i][j][0] = lx[i][j][1] = 0.0;
+  }
+  for (int k0 = sa; k0 < sb; k0 += 4) {
+    const int sl = k0 + t;
+    const bool valid = sl < sb;
+    const int sc = valid ? sl : sa;
+    const int oy = s_oy[sc], ox = s_ox[sc];
+    double a1[2], b3[3];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int d = band0 + mt * 8 + g - oy;
+      const double v = s_wy[sc * S + (d < 0 ? 0 : (d >= S ? S - 1 : d))];
+      a1[mt] = (valid && d >= 0 && d < S) ? v : 0.0;
+    }
+#pragma unroll
+    for (int nt = 0; nt < 3; ++nt) {
+      const int d = nt * 8 + g - ox;
+      const double v = s_wx[sc * S + (d < 0 ? 0 : (d >= S ? S - 1 : d))];
+      b3[nt] = (valid && d >= 0 && d < S) ? v : 0.0;
+    }
+    const cplx* rx = s_rx + sc * RR;
+    const cplx* ry = s_ry + sc * RR;
+    const cplx yv = valid ? s_ys[sc] : mk(0, 0);  // padded K slots contribute nothing
+    const cplx t1 = cmul(conj_(rx[0]), yv);  // conj(Dx) y
+    const cplx Dy = ry[0];
+    const cplx v2 = cmul(conj_(Dy), t1);     // conj(Dx Dy) y
+#pragma unroll
+    for (int nt = 0; nt < 3; ++nt) {
+      const double bre = b3[nt] * v2.x, bim = b3[nt] * v2.y;
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        dmma884(rg[mt][nt][0], rg[mt][nt][1], a1[mt], bre);
+        dmma884(rg[mt][nt + 3][0], rg[mt][nt + 3][1], a1[mt], bim);
+      }
+    }
+    if (E > 0) {
+      const bool ge = g < E;
+      const cplx Ax = rx[1 + (ge ? g : 0)], By = ry[1 + (ge ? g : 0)];
+      const cplx vx = ge ? cmul(conj_(By), t1) : mk(0, 0);  // conj(By_e Dx) y
+      const cplx ca = ge ? cmul(conj_(Ax), yv) : mk(0, 0);  // conj(Ax_i) y
+      const cplx vy = cmul(conj_(Dy), ca);                  // conj(Ax_e Dy) y
+      const cplx bj = ge ? By : mk(0, 0);
+      const double vyc[2] = {vy.x, vy.y}, vxc[2] = {vx.x, vx.y}, cac[2] = {ca.x, ca.y}, bjc[2] = {bj.x, bj.y};
+#pragma unroll
+      for (int mm = 0; mm < 2; ++mm) {
+#pragma unroll
+        for (int nn = 0; nn < 2; ++nn) {
+          dmma884(ly[mm][nn][0], ly[mm][nn][1], vyc[mm], a1[nn]);
+          dmma884(co[mm][nn][0], co[mm][nn][1], cac[mm], bjc[nn]);
+        }
+#pragma unroll
+        for (int nt = 0; nt < 3; ++nt) dmma884(lx[mm][nt][0], lx[mm][nt][1], vxc[mm], b3[nt]);
+      }
+    }
+  }
+  __syncthreads();  // the fold buffer aliases the staging area
+  cplx* buf = reinterpret_cast<cplx*>(fsm_raw);
+  cplx* mine = buf + warp * FM::PER_WARP;
+  cplx* mreg = mine;                 // [16][R]  band-relative rows
+  cplx* mly = mine + FM::REG;        // [8][16]  y-line e, band-relative row
+  cplx* mlx = mly + FM::LYN;         // [8][R]   x-line e, column
+  double* mp = reinterpret_cast<double*>(mlx + FM::LXN);  // [16][16] corner products
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 3; ++nt)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) mreg[(mt * 8 + g) * R + nt * 8 + 2 * t + j] = mk(rg[mt][nt][j], rg[mt][nt + 3][j]);
+  if (E > 0) {
+#pragma unroll
+    for (int nn = 0; nn < 2; ++nn)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        mly[g * 16 + nn * 8 + 2 * t + j] = mk(ly[0][nn][j], ly[1][nn][j]);
+#pragma unroll
+        for (int mm = 0; mm < 2; ++mm) mp[(mm * 8 + g) * 16 + nn * 8 + 2 * t + j] = co[mm][nn][j];
+      }
+#pragma unroll
+    for (int nt = 0; nt < 3; ++nt)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) mlx[g * R + nt * 8 + 2 * t + j] = mk(lx[0][nt][j], lx[1][nt][j]);
+  }
+  __syncthreads();
+  const int64_t chunk = (int64_t)prob * cap + c;
+  cplx* tb = TB + chunk * R * R;
+  for (int i = threadIdx.x; i < R * R; i += blockDim.x) {
+    const int r = i / R, cc = i - r * R;
+    cplx a = mk(0, 0);
+#pragma unroll
+    for (int w = 0; w < F_WARPS; ++w) {
+      const int rr = r - w * BAND;
+      if (rr >= 0 && rr < 16) a = cadd(a, buf[w * FM::PER_WARP + rr * R + cc]);
+    }
+    tb[i] = a;
+  }
+  if (E > 0) {
+    cplx* tl = TL + chunk * 2 * E * R;  // [y-lines e][row] then [x-lines e][column]
+    for (int i = threadIdx.x; i < E * R; i += blockDim.x) {
+      const int e = i / R, r = i - e * R;
+      cplx a = mk(0, 0), bx = mk(0, 0);
+#pragma unroll
+      for (int w = 0; w < F_WARPS; ++w) {
+        const cplx* wb = buf + w * FM::PER_WARP;
+        const int rr = r - w * BAND;
+        if (rr >= 0 && rr < 16) a = cadd(a, wb[FM::REG + e * 16 + rr]);
+        bx = cadd(bx, wb[FM::REG + FM::LYN + e * R + r]);
+      }
+      tl[i] = a;
+      tl[E * R + i] = bx;
+    }
+    cplx* tc = TC + chunk * NCE;
+    for (int q = threadIdx.x; q < NCE; q += blockDim.x) {
+      const int k = q / (P * P), rem = q - k * P * P, i = rem / P, j = rem - i * P;
+      const int ip = (k < 2 ? 0 : P) + i, jp = (k % 2 == 0 ? 0 : P) + j;  // ca index (Lx | Rx), b index (Ly | Ry)
+      double re = 0.0, im = 0.0;
+#pragma unroll
+      for (int w = 0; w < F_WARPS; ++w) {
+        const double* wp = reinterpret_cast<const double*>(buf + w * FM::PER_WARP + FM::REG + FM::LYN + FM::LXN);
+        re += wp[ip * 16 + jp] + wp[(8 + ip) * 16 + 8 + jp];   // sum ca conj(b): Re = car br + cai bi
+        im += wp[(8 + ip) * 16 + jp] - wp[ip * 16 + 8 + jp];   //                 Im = cai br - car bi
+      }
+      tc[q] = mk(re, im);
+    }
+  }
+}
