@@ -266,6 +266,10 @@ void set_smem_attrs() {
   allow_big_smem(k2f_spread<2>);
   allow_big_smem(k2f_spread<3>);
   allow_big_smem(k2f_spread<4>);
+  allow_big_smem(k2f_interp_mma<1>);
+  allow_big_smem(k2f_interp_mma<2>);
+  allow_big_smem(k2f_interp_mma<3>);
+  allow_big_smem(k2f_interp_mma<4>);
   allow_big_smem(k2f_spread_mma<1>);
   allow_big_smem(k2f_spread_mma<2>);
   allow_big_smem(k2f_spread_mma<3>);
@@ -703,6 +707,13 @@ Prof g_prof;
 std::atomic<long long> g_launches{0};  // kernels this library has launched (gs_launch_count)
 // 2D spreading variant: FP64 tensor cores (default) or the lane-per-column
 // DFMA kernel (GS_B200_SPREAD=dfma, for A/B measurements)
+bool interp_mma() {
+  static const bool on = [] {
+    const char* e = std::getenv("GS_B200_INTERP");
+    return !(e && std::string(e) == "dfma");
+  }();
+  return on;
+}
 bool spread_mma() {
   static const bool on = [] {
     const char* e = std::getenv("GS_B200_SPREAD");
@@ -774,9 +785,15 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
         const dim3 grid(op->cap, B);
         const int* pp = perm_io ? op->perm.p : nullptr;
 #define GS_F_INTERP(PP)                                                                                            \
-  k2f_interp<PP><<<grid, F_ITHREADS, FInterp<PP>::bytes(), st>>>(                                    \
-      P, op->ch_tile.p, op->ch_s0.p, op->ch_s1.p, op->ch_count.p, op->cap, op->units.p, op->ucount.p, op->base_x.p, \
-      op->base_y.p, op->wts_x.p, op->wts_y.p, op->rec_x.p, op->rec_y.p, op->G.p, op->lines.p, x, pp, y)
+  if (interp_mma())                                                                                                \
+    k2f_interp_mma<PP><<<grid, 32 * F_WARPS * F_IMSPLIT, FInterpM<PP>::bytes(), st>>>(                                       \
+        P, op->ch_tile.p, op->ch_s0.p, op->ch_s1.p, op->ch_count.p, op->cap, op->base_x.p, op->base_y.p,            \
+        op->wts_x.p, op->wts_y.p, op->rec_x.p, op->rec_y.p, op->G.p, op->lines.p, x, pp, y);                        \
+  else                                                                                                             \
+    k2f_interp<PP><<<grid, F_ITHREADS, FInterp<PP>::bytes(), st>>>(                                              \
+        P, op->ch_tile.p, op->ch_s0.p, op->ch_s1.p, op->ch_count.p, op->cap, op->units.p, op->ucount.p,             \
+        op->base_x.p, op->base_y.p, op->wts_x.p, op->wts_y.p, op->rec_x.p, op->rec_y.p, op->G.p, op->lines.p, x,   \
+        pp, y)
         switch (op->p) {
           case 1: GS_F_INTERP(1); break;
           case 2: GS_F_INTERP(2); break;
@@ -839,7 +856,7 @@ void adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
         const int* pp = perm_io ? op->perm.p : nullptr;
 #define GS_F_SPREAD(PP)                                                                                          \
   if (spread_mma())                                                                                              \
-    k2f_spread_mma<PP><<<grid, 32 * F_WARPS, FSpreadM<PP>::bytes(), st>>>(                                     \
+    k2f_spread_mma<PP><<<grid, 32 * F_MWARPS, FSpreadM<PP>::bytes(), st>>>(                                     \
         P, op->ch_tile.p, op->ch_s0.p, op->ch_s1.p, op->ch_count.p, op->cap, op->base_x.p, op->base_y.p,          \
         op->wts_x.p, op->wts_y.p, op->rec_x.p, op->rec_y.p, y, pp, op->TB.p, op->TL.p, op->TC.p);                 \
   else                                                                                                           \

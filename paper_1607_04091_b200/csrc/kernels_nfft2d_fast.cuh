@@ -41,6 +41,43 @@ __device__ __forceinline__ unsigned char* f_stage(unsigned char* dst, const void
 }
 __device__ __forceinline__ void f_stage_wait() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
+// TMA bulk staging (cp.async.bulk, one issuing thread, completion on an
+// mbarrier): copy [src, src + bytes) rounded out to 16-B boundaries into dst;
+// returns src's image in shared memory and adds the copied bytes to *tx.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void bar_expect(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* bar, unsigned parity) {
+  unsigned done = 0;
+  while (!done)
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ unsigned bulk_bytes(const void* src, size_t bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(src), al = a & ~uintptr_t(15);
+  return (unsigned)((a - al + bytes + 15) & ~size_t(15));
+}
+__device__ __forceinline__ unsigned char* bulk_stage(unsigned char* dst, const void* src, size_t bytes, uint64_t* bar) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(src), al = a & ~uintptr_t(15);
+  const unsigned n = (unsigned)((a - al + bytes + 15) & ~size_t(15));
+  if (n)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(al), "r"(n), "r"(smem_u32(bar))
+                 : "memory");
+  return dst + (a - al);
+}
+
 // ------------------------------------------------------------------ interpolation
 // Work units of the interpolation: a chunk's samples are walked in sorted order
 // and consecutive samples in the same cell row whose columns differ by at most
@@ -597,19 +634,30 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
       : "d"(a), "d"(b));
 }
 
+// CTA of the DMMA spreading kernel: F_MSPLIT warps per band of F_BAND sample
+// rows (they take alternate K steps of the band's samples), so 2 CTAs/SM hold
+// 4 x F_MSPLIT warps per SMSP pair -- enough to keep the DMMA pipe fed
+#ifndef F_MSPLIT
+#define F_MSPLIT 1
+#endif
+#define F_MWARPS (F_WARPS * F_MSPLIT)
+#ifndef F_MUNROLL
+#define F_MUNROLL 2  // K steps per loop trip: the next step's fragments load under this step's DMMAs
+#endif
+
 template <int P>
 struct FSpreadM {
   static constexpr int E = P >= 2 ? 2 * P : 0;
   // per-warp fold record: region 16 x 24 (complex), y-lines 8 x 16, x-lines 8 x 24 (complex), corner P 16 x 16 (real)
   static constexpr int REG = 16 * F_R, LYN = 8 * 16, LXN = 8 * F_R, PN = 16 * 16 / 2;  // in complex units
   static constexpr int PER_WARP = REG + LYN + LXN + PN;
-  static constexpr size_t FOLD = sizeof(cplx) * F_WARPS * PER_WARP;
+  static constexpr size_t FOLD = sizeof(cplx) * F_WARPS * PER_WARP;  // one record per band
   static constexpr size_t MAIN = (FSpread<P>::STG_END > FOLD ? FSpread<P>::STG_END : FOLD);
   static constexpr size_t bytes() { return (MAIN + 15) / 16 * 16; }
 };
 
 template <int P>
-__global__ void __launch_bounds__(32 * F_WARPS, 2)
+__global__ void __launch_bounds__(32 * F_MWARPS, 2)
 k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ ch_s0, const int* __restrict__ ch_s1,
                const int* __restrict__ ch_count, int cap, const int* __restrict__ base_x,
                const int* __restrict__ base_y, const double* __restrict__ wx_all, const double* __restrict__ wy_all,
@@ -617,7 +665,7 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
                const int* __restrict__ in_perm, cplx* __restrict__ TB, cplx* __restrict__ TL, cplx* __restrict__ TC) {
   using F = FSpread<P>;
   using FM = FSpreadM<P>;
-  constexpr int S = F_S, T = F_T, R = F_R, BAND = F_BAND, E = F::E, RR = F::RR, NCE = F::NCE;
+  constexpr int S = F_S, T = F_T, R = F_R, BAND = F_BAND, E = F::E, RR = F::RR, NCE = F::NCE, MU = F_MUNROLL;
   extern __shared__ __align__(16) unsigned char fsm_raw[];
   cplx* s_ys = reinterpret_cast<cplx*>(fsm_raw + F::STG_YS);
   int* s_ox = reinterpret_cast<int*>(fsm_raw + F::STG_OX);
@@ -630,19 +678,34 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   const int ty = tile / Pp.nt, tx = tile - ty * Pp.nt;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int64_t g0 = (int64_t)prob * Pp.M + s0;
-  // ---- stage the chunk (as k2f_spread)
-  const double* s_wy = reinterpret_cast<const double*>(f_stage(fsm_raw + F::STG_WY, wy_all + g0 * S, sizeof(double) * S * n));
-  const double* s_wx = reinterpret_cast<const double*>(f_stage(fsm_raw + F::STG_WX, wx_all + g0 * S, sizeof(double) * S * n));
-  const cplx* s_rx = reinterpret_cast<const cplx*>(f_stage(fsm_raw + F::STG_RX, recx_all + g0 * RR, sizeof(cplx) * RR * n));
-  const cplx* s_ry = reinterpret_cast<const cplx*>(f_stage(fsm_raw + F::STG_RY, recy_all + g0 * RR, sizeof(cplx) * RR * n));
+  // ---- stage the chunk: weights and factor records by TMA bulk copies (one
+  // thread, mbarrier completion), samples and cell offsets by the threads
+  __shared__ __align__(8) uint64_t stage_bar;
+  const double* wy_src = wy_all + g0 * S;
+  const double* wx_src = wx_all + g0 * S;
+  const cplx* rx_src = recx_all + g0 * RR;
+  const cplx* ry_src = recy_all + g0 * RR;
+  const double* s_wy = reinterpret_cast<const double*>(fsm_raw + F::STG_WY + (reinterpret_cast<uintptr_t>(wy_src) & 15));
+  const double* s_wx = reinterpret_cast<const double*>(fsm_raw + F::STG_WX + (reinterpret_cast<uintptr_t>(wx_src) & 15));
+  const cplx* s_rx = reinterpret_cast<const cplx*>(fsm_raw + F::STG_RX + (reinterpret_cast<uintptr_t>(rx_src) & 15));
+  const cplx* s_ry = reinterpret_cast<const cplx*>(fsm_raw + F::STG_RY + (reinterpret_cast<uintptr_t>(ry_src) & 15));
+  if (threadIdx.x == 0) {
+    bar_init(&stage_bar);
+    bar_expect(&stage_bar, bulk_bytes(wy_src, sizeof(double) * S * n) + bulk_bytes(wx_src, sizeof(double) * S * n) +
+                               bulk_bytes(rx_src, sizeof(cplx) * RR * n) + bulk_bytes(ry_src, sizeof(cplx) * RR * n));
+    bulk_stage(fsm_raw + F::STG_WY, wy_src, sizeof(double) * S * n, &stage_bar);
+    bulk_stage(fsm_raw + F::STG_WX, wx_src, sizeof(double) * S * n, &stage_bar);
+    bulk_stage(fsm_raw + F::STG_RX, rx_src, sizeof(cplx) * RR * n, &stage_bar);
+    bulk_stage(fsm_raw + F::STG_RY, ry_src, sizeof(cplx) * RR * n, &stage_bar);
+  }
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const int64_t gs = g0 + i;
     s_ys[i] = ldg2(yin + (int64_t)prob * Pp.M + (in_perm ? (int64_t)in_perm[gs] : (int64_t)(s0 + i)));
     s_ox[i] = base_x[gs] - tx * T;
     s_oy[i] = (unsigned char)(base_y[gs] - ty * T);
   }
-  f_stage_wait();
-  __syncthreads();
+  __syncthreads();  // barrier initialised, samples staged
+  bar_wait(&stage_bar, 0);
   if (threadIdx.x <= T) {  // row starts (samples are sorted by cell, row-major, in a tile)
     const int key = threadIdx.x;
     int lo = 0, hi = n;
@@ -654,7 +717,8 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
     rs[threadIdx.x] = lo;
   }
   __syncthreads();
-  const int band0 = warp * BAND;
+  const int band = warp % F_WARPS, half = warp / F_WARPS;  // band of rows, K-step parity
+  const int band0 = band * BAND;
   const int sa = rs[band0], sb = rs[band0 + BAND];
   double rg[2][6][2], ly[2][2][2], lx[2][3][2], co[2][2][2];
 #pragma unroll
@@ -666,7 +730,8 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
 #pragma unroll
     for (int j = 0; j < 3; ++j) lx[i][j][0] = lx[i][j][1] = 0.0;
   }
-  for (int k0 = sa; k0 < sb; k0 += 4) {
+#pragma unroll MU
+  for (int k0 = sa + 4 * half; k0 < sb; k0 += 4 * F_MSPLIT) {
     const int sl = k0 + t;
     const bool valid = sl < sb;
     const int sc = valid ? sl : sa;
@@ -721,32 +786,41 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   }
   __syncthreads();  // the fold buffer aliases the staging area
   cplx* buf = reinterpret_cast<cplx*>(fsm_raw);
-  cplx* mine = buf + warp * FM::PER_WARP;
+  cplx* mine = buf + band * FM::PER_WARP;  // one record per band; the K-step halves add in turn
   cplx* mreg = mine;                 // [16][R]  band-relative rows
   cplx* mly = mine + FM::REG;        // [8][16]  y-line e, band-relative row
   cplx* mlx = mly + FM::LYN;         // [8][R]   x-line e, column
   double* mp = reinterpret_cast<double*>(mlx + FM::LXN);  // [16][16] corner products
+#pragma unroll 1
+  for (int h = 0; h < F_MSPLIT; ++h) {
+    if (half == h) {
+      const bool add = h > 0;
+      auto put = [&](cplx* dst, cplx v) { *dst = add ? cadd(*dst, v) : v; };
+      auto putd = [&](double* dst, double v) { *dst = add ? *dst + v : v; };
 #pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
+      for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < 3; ++nt)
+        for (int nt = 0; nt < 3; ++nt)
 #pragma unroll
-      for (int j = 0; j < 2; ++j) mreg[(mt * 8 + g) * R + nt * 8 + 2 * t + j] = mk(rg[mt][nt][j], rg[mt][nt + 3][j]);
-  if (E > 0) {
+          for (int j = 0; j < 2; ++j)
+            put(&mreg[(mt * 8 + g) * R + nt * 8 + 2 * t + j], mk(rg[mt][nt][j], rg[mt][nt + 3][j]));
+      if (E > 0) {
 #pragma unroll
-    for (int nn = 0; nn < 2; ++nn)
+        for (int nn = 0; nn < 2; ++nn)
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        mly[g * 16 + nn * 8 + 2 * t + j] = mk(ly[0][nn][j], ly[1][nn][j]);
+          for (int j = 0; j < 2; ++j) {
+            put(&mly[g * 16 + nn * 8 + 2 * t + j], mk(ly[0][nn][j], ly[1][nn][j]));
 #pragma unroll
-        for (int mm = 0; mm < 2; ++mm) mp[(mm * 8 + g) * 16 + nn * 8 + 2 * t + j] = co[mm][nn][j];
+            for (int mm = 0; mm < 2; ++mm) putd(&mp[(mm * 8 + g) * 16 + nn * 8 + 2 * t + j], co[mm][nn][j]);
+          }
+#pragma unroll
+        for (int nt = 0; nt < 3; ++nt)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) put(&mlx[g * R + nt * 8 + 2 * t + j], mk(lx[0][nt][j], lx[1][nt][j]));
       }
-#pragma unroll
-    for (int nt = 0; nt < 3; ++nt)
-#pragma unroll
-      for (int j = 0; j < 2; ++j) mlx[g * R + nt * 8 + 2 * t + j] = mk(lx[0][nt][j], lx[1][nt][j]);
+    }
+    __syncthreads();
   }
-  __syncthreads();
   const int64_t chunk = (int64_t)prob * cap + c;
   cplx* tb = TB + chunk * R * R;
   for (int i = threadIdx.x; i < R * R; i += blockDim.x) {
@@ -786,6 +860,241 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
         im += wp[(8 + ip) * 16 + jp] - wp[ip * 16 + 8 + jp];   //                 Im = cai br - car bi
       }
       tc[q] = mk(re, im);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ interpolation on the FP64 tensor cores
+// k2f_interp_mma: the forward 2D apply of a chunk as per-warp DMMA GEMMs.
+// Warp w takes the samples of sample rows [3w, 3w+3) eight at a time (one
+// sample per B column n = lane/4):
+//   H  = [G_re; G_im; LX_re; LX_im](band rows / lines, 24 cols) x Wx   (48 x 8, K = 24 columns)
+//   UY = [LY_re; LY_im](e, band rows) x Wy                              (16 x 8, K = 16 rows)
+//   CB = [[C_re, -C_im]; [C_im, C_re]] x [b_re; b_im]                   (16 x 8, K = 16)
+// with Wx(c, s) = wx_s(c - ox_s), Wy(r, s) = wy_s(r - oy_s), b_j = By_j(s).
+// A lane then holds, for two samples, row g of every product and forms
+//   Dx Dy sum_r wy(r) H_G(r) + Dx b_g ux_g + a_g (Dy uy_g + (C b)_g)
+// (interior freq2wave.cpp:255, sides 272-301, corners 260-270); a three-step
+// xor-shuffle over the 8 lanes of the sample finishes every sum.
+#define F_GS 28  // row stride (doubles) of the split re / im region: 8 rows x 4 columns hit 32 banks
+#ifndef F_IMUNROLL
+#define F_IMUNROLL 3  // sample tiles per loop trip (the next tile's DMMAs overlap this tile's epilogue)
+#endif
+#ifndef F_IMSPLIT
+#define F_IMSPLIT 1  // warps per band (alternate sample tiles)
+#endif
+
+template <int P>
+struct FInterpM {
+  static constexpr int RR = 1 + (P >= 2 ? 2 * P : 0);
+  // dynamic shared memory: staged weights and factor records (TMA bulk), then the split region / lines
+  static constexpr size_t WY = 0;
+  static constexpr size_t WX = WY + sizeof(double) * F_CHUNK * F_S + 32;
+  static constexpr size_t RX = WX + sizeof(double) * F_CHUNK * F_S + 32;
+  static constexpr size_t RY = RX + sizeof(cplx) * F_CHUNK * RR + 16;
+  static constexpr size_t GRE = RY + sizeof(cplx) * F_CHUNK * RR + 16;
+  static constexpr size_t GIM = GRE + sizeof(double) * F_R * F_GS;
+  static constexpr size_t LXRE = GIM + sizeof(double) * F_R * F_GS;
+  static constexpr size_t LXIM = LXRE + sizeof(double) * 8 * F_GS;
+  static constexpr size_t END = LXIM + sizeof(double) * 8 * F_GS;
+  static constexpr size_t bytes() { return END; }
+};
+
+template <int P>
+__global__ void __launch_bounds__(32 * F_WARPS * F_IMSPLIT, 2)
+k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ ch_s0, const int* __restrict__ ch_s1,
+               const int* __restrict__ ch_count, int cap, const int* __restrict__ base_x,
+               const int* __restrict__ base_y, const double* __restrict__ wx_all, const double* __restrict__ wy_all,
+               const cplx* __restrict__ recx_all, const cplx* __restrict__ recy_all, const cplx* __restrict__ G,
+               const cplx* __restrict__ lines, const cplx* __restrict__ x, const int* __restrict__ out_perm,
+               cplx* __restrict__ y) {
+  using FI = FInterpM<P>;
+  constexpr int S = F_S, T = F_T, R = F_R, BAND = F_BAND, RR = FI::RR, IMU = F_IMUNROLL;
+  constexpr int E = P >= 2 ? 2 * P : 0, EE = E > 0 ? E : 1;
+  extern __shared__ __align__(16) unsigned char fim_raw[];
+  double* gre = reinterpret_cast<double*>(fim_raw + FI::GRE);
+  double* gim = reinterpret_cast<double*>(fim_raw + FI::GIM);
+  double* lxre = reinterpret_cast<double*>(fim_raw + FI::LXRE);
+  double* lxim = reinterpret_cast<double*>(fim_raw + FI::LXIM);
+  __shared__ cplx lys[EE][R];
+  __shared__ cplx cxs[P >= 2 ? 4 * P * P : 1];
+  __shared__ int s_ox[F_CHUNK];
+  __shared__ unsigned char s_oy[F_CHUNK];
+  __shared__ int rs[T + 1];
+  __shared__ __align__(8) uint64_t stage_bar;
+  const int prob = blockIdx.y, c = blockIdx.x;
+  if (c >= ch_count[prob]) return;
+  const int64_t chunk = (int64_t)prob * cap + c;
+  const int tile = ch_tile[chunk], s0 = ch_s0[chunk], s1 = ch_s1[chunk];
+  const int n = s1 - s0;
+  const int ty = tile / Pp.nt, tx = tile - ty * Pp.nt;
+  const int n_ov = Pp.n_ov, mask = n_ov - 1, nn = Pp.n;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int64_t g0 = (int64_t)prob * Pp.M + s0;
+  // ---- staging: weights / records by TMA bulk copies; region and lines split into re / im
+  const double* wy_src = wy_all + g0 * S;
+  const double* wx_src = wx_all + g0 * S;
+  const cplx* rx_src = recx_all + g0 * RR;
+  const cplx* ry_src = recy_all + g0 * RR;
+  const double* s_wy = reinterpret_cast<const double*>(fim_raw + FI::WY + (reinterpret_cast<uintptr_t>(wy_src) & 15));
+  const double* s_wx = reinterpret_cast<const double*>(fim_raw + FI::WX + (reinterpret_cast<uintptr_t>(wx_src) & 15));
+  const cplx* s_rx = reinterpret_cast<const cplx*>(fim_raw + FI::RX + (reinterpret_cast<uintptr_t>(rx_src) & 15));
+  const cplx* s_ry = reinterpret_cast<const cplx*>(fim_raw + FI::RY + (reinterpret_cast<uintptr_t>(ry_src) & 15));
+  if (threadIdx.x == 0) {
+    bar_init(&stage_bar);
+    bar_expect(&stage_bar, bulk_bytes(wy_src, sizeof(double) * S * n) + bulk_bytes(wx_src, sizeof(double) * S * n) +
+                               bulk_bytes(rx_src, sizeof(cplx) * RR * n) + bulk_bytes(ry_src, sizeof(cplx) * RR * n));
+    bulk_stage(fim_raw + FI::WY, wy_src, sizeof(double) * S * n, &stage_bar);
+    bulk_stage(fim_raw + FI::WX, wx_src, sizeof(double) * S * n, &stage_bar);
+    bulk_stage(fim_raw + FI::RX, rx_src, sizeof(cplx) * RR * n, &stage_bar);
+    bulk_stage(fim_raw + FI::RY, ry_src, sizeof(cplx) * RR * n, &stage_bar);
+  }
+  const cplx* gp = G + (int64_t)prob * n_ov * n_ov;
+  for (int i = threadIdx.x; i < R * R; i += blockDim.x) {
+    const int r = i / R, cc = i - r * R;
+    const cplx v = ldg2(gp + (int64_t)((ty * T + r) & mask) * n_ov + ((tx * T + cc) & mask));
+    gre[r * F_GS + cc] = v.x;
+    gim[r * F_GS + cc] = v.y;
+  }
+  if (E > 0) {
+    const cplx* LY = lines + (int64_t)prob * 2 * E * n_ov;
+    const cplx* LX = LY + (int64_t)E * n_ov;
+    for (int i = threadIdx.x; i < 8 * R; i += blockDim.x) {
+      const int e = i / R, r = i - e * R;
+      const cplx vx = e < E ? ldg2(LX + (int64_t)e * n_ov + ((tx * T + r) & mask)) : mk(0, 0);
+      lxre[e * F_GS + r] = vx.x;
+      lxim[e * F_GS + r] = vx.y;
+      if (e < E) lys[e][r] = ldg2(LY + (int64_t)e * n_ov + ((ty * T + r) & mask));
+    }
+    const cplx* X = x + (int64_t)prob * nn * nn;
+    for (int q = threadIdx.x; q < 4 * P * P; q += blockDim.x) {
+      const int k = q / (P * P), rem = q - k * P * P, i = rem / P, j = rem - i * P;
+      const int row0 = (k < 2) ? 0 : nn - P, col0 = (k % 2 == 0) ? 0 : nn - P;
+      cxs[q] = ldg2(X + (int64_t)(col0 + j) * nn + row0 + i);
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    s_ox[i] = base_x[g0 + i] - tx * T;
+    s_oy[i] = (unsigned char)(base_y[g0 + i] - ty * T);
+  }
+  __syncthreads();
+  if (threadIdx.x <= T) {  // row starts
+    const int key = threadIdx.x;
+    int lo = 0, hi = n;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((int)s_oy[mid] < key) lo = mid + 1;
+      else hi = mid;
+    }
+    rs[threadIdx.x] = lo;
+  }
+  __syncthreads();
+  bar_wait(&stage_bar, 0);
+  const int band0 = (warp % F_WARPS) * BAND, half = warp / F_WARPS;
+  const int sa = rs[band0], sb = rs[band0 + BAND];
+  // constant A operands: y-lines [LY_re; LY_im](g, band0 + 4 ks + t), corner block matrix
+  double lyA[2][4], crA[2][4];
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const int row = band0 + ks * 4 + t;
+    const cplx v = (E > 0 && g < E && row < R) ? lys[g < E ? g : 0][row < R ? row : 0] : mk(0, 0);
+    lyA[0][ks] = v.x;
+    lyA[1][ks] = v.y;
+    const int part = ks >> 1, j = (ks & 1) * 4 + t;  // K index = (re | im part of b, j)
+    cplx cij = mk(0, 0);
+    if (E > 0 && g < E && j < E) {
+      const int hi = g < P ? 0 : 1, ii = g - hi * P, hj = j < P ? 0 : 1, jj = j - hj * P;
+      cij = cxs[(2 * hi + hj) * P * P + ii * P + jj];
+    }
+    crA[0][ks] = part == 0 ? cij.x : -cij.y;  // row block re:  C_re b_re - C_im b_im
+    crA[1][ks] = part == 0 ? cij.y : cij.x;   // row block im:  C_im b_re + C_re b_im
+  }
+#pragma unroll IMU
+  for (int n0 = sa + 8 * half; n0 < sb; n0 += 8 * F_IMSPLIT) {
+    // B operands for sample column g
+    const int sg = n0 + g;
+    const bool vg = sg < sb;
+    const int sgc = vg ? sg : sa;
+    const int oyg = s_oy[sgc], oxg = s_ox[sgc];
+    double wb[6], yb[4], cb[4];
+#pragma unroll
+    for (int ks = 0; ks < 6; ++ks) {
+      const int d = ks * 4 + t - oxg;
+      const double v = s_wx[sgc * S + (d < 0 ? 0 : (d >= S ? S - 1 : d))];
+      wb[ks] = (vg && d >= 0 && d < S) ? v : 0.0;
+    }
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      const int d = band0 + ks * 4 + t - oyg;
+      const double v = s_wy[sgc * S + (d < 0 ? 0 : (d >= S ? S - 1 : d))];
+      yb[ks] = (vg && d >= 0 && d < S) ? v : 0.0;
+      const int j = (ks & 1) * 4 + t;
+      const cplx bj = (E > 0 && vg && j < E) ? s_ry[sgc * RR + 1 + (j < E ? j : 0)] : mk(0, 0);
+      cb[ks] = (ks >> 1) ? bj.y : bj.x;
+    }
+    // products
+    double h[6][2], uy[2][2], cbo[2][2];
+#pragma unroll
+    for (int mt = 0; mt < 6; ++mt) h[mt][0] = h[mt][1] = 0.0;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) uy[mt][0] = uy[mt][1] = cbo[mt][0] = cbo[mt][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < 6; ++ks) {
+      const int col = ks * 4 + t;
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const double* src = mt < 2 ? gre : gim;
+        const int row = band0 + (mt & 1) * 8 + g;
+        const double a = row < R ? src[row * F_GS + col] : 0.0;
+        dmma884(h[mt][0], h[mt][1], a, wb[ks]);
+      }
+      if (E > 0) {
+        dmma884(h[4][0], h[4][1], lxre[g * F_GS + col], wb[ks]);
+        dmma884(h[5][0], h[5][1], lxim[g * F_GS + col], wb[ks]);
+      }
+    }
+    if (E > 0) {
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          dmma884(uy[mt][0], uy[mt][1], lyA[mt][ks], yb[ks]);
+          dmma884(cbo[mt][0], cbo[mt][1], crA[mt][ks], cb[ks]);
+        }
+    }
+    // epilogue: lane (g, t) holds row g of every product for samples n0 + 2t + j
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int sn = n0 + 2 * t + j;
+      const bool vn = sn < sb;
+      const int snc = vn ? sn : sa;
+      const int oyn = s_oy[snc];
+      const cplx* rx = s_rx + snc * RR;
+      const cplx* ry = s_ry + snc * RR;
+      const cplx Dx = rx[0], Dy = ry[0];
+      cplx rp = mk(0, 0);
+#pragma unroll
+      for (int mh = 0; mh < 2; ++mh) {
+        const int d = band0 + mh * 8 + g - oyn;
+        const double wv = s_wy[snc * S + (d < 0 ? 0 : (d >= S ? S - 1 : d))];
+        const double w = (d >= 0 && d < S) ? wv : 0.0;
+        rp = caxpy(rp, w, mk(h[mh][j], h[2 + mh][j]));
+      }
+      cplx part = cmul(cmul(Dx, Dy), rp);
+      if (E > 0 && g < E) {
+        const cplx ag = rx[1 + g], bg = ry[1 + g];
+        part = cadd(part, cmul(Dx, cmul(bg, mk(h[4][j], h[5][j]))));
+        part = cadd(part, cmul(ag, cadd(cmul(Dy, mk(uy[0][j], uy[1][j])), mk(cbo[0][j], cbo[1][j]))));
+      }
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        part.x += __shfl_xor_sync(0xffffffffu, part.x, o);
+        part.y += __shfl_xor_sync(0xffffffffu, part.y, o);
+      }
+      if (g == 0 && vn) {
+        const int64_t gs = g0 + sn;
+        y[(int64_t)prob * Pp.M + (out_perm ? (int64_t)out_perm[gs] : (int64_t)(s0 + sn))] = part;
+      }
     }
   }
 }

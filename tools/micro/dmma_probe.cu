@@ -50,8 +50,9 @@ int main() {
   const char* names[4] = {"mma m8n8k4 f64", "mma m16n8k4 f64", "mma m16n8k8 f64", "DFMA (fma)"};
   const double fma_per_inst_warp[4] = {8 * 8 * 4, 16 * 8 * 4, 16 * 8 * 8, 32 * 4};  // per unrolled step per warp
   for (int kind = 0; kind < 4; ++kind) {
-    for (int blocks_per_sm : {4, 8}) {
-      const int grid = 148 * blocks_per_sm, threads = 256, iters = 2000;
+    for (int cfg : {0, 1, 2, 3}) {
+      const int blocks_per_sm = cfg == 0 ? 2 : (cfg == 1 ? 4 : (cfg == 2 ? 8 : 16));
+      const int grid = 148 * blocks_per_sm, threads = 128, iters = 2000;
       auto launch = [&] {
         if (kind == 0) k<0><<<grid, threads>>>(out, iters, 1.0);
         else if (kind == 1) k<1><<<grid, threads>>>(out, iters, 1.0);
@@ -67,7 +68,7 @@ int main() {
       cudaEventElapsedTime(&ms, e0, e1);
       const double warps = (double)grid * threads / 32;
       const double fmas = warps * iters * 8 * fma_per_inst_warp[kind];
-      printf("%-18s blocks/SM %d: %.2f TFLOP/s (%.3f ms) err=%s\n", names[kind], blocks_per_sm, 2 * fmas / (ms * 1e-3) / 1e12,
+      printf("%-18s warps/SM %d: %.2f TFLOP/s (%.3f ms) err=%s\n", names[kind], blocks_per_sm * 4, 2 * fmas / (ms * 1e-3) / 1e12,
              ms, cudaGetErrorString(cudaGetLastError()));
     }
   }
