@@ -52,6 +52,8 @@ FULL_METRICS = [
     ("launch__registers_per_thread", "registers/thread"),
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe %"),
     ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "FP64 inst %"),
+    ("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active", "DMMA (FP64 tensor) pipe %"),
+    ("sm__issue_active.avg.pct_of_peak_sustained_elapsed", "issue active %"),
     ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem wavefronts"),
     ("l1tex__throughput.avg.pct_of_peak_sustained_active", "L1 throughput %"),
     ("lts__t_bytes.sum", "L2 bytes"),
