@@ -755,8 +755,13 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
     const cplx t1 = cmul(conj_(rx[0]), yv);  // conj(Dx) y
     const cplx Dy = ry[0];
     const cplx v2 = cmul(conj_(Dy), t1);     // conj(Dx Dy) y
+    // column tiles the step's 4 samples do not reach are all-zero: skip them (warp-uniform vote)
+    bool hit[3];
+#pragma unroll
+    for (int nt = 0; nt < 3; ++nt) hit[nt] = __any_sync(0xffffffffu, b3[nt] != 0.0);
 #pragma unroll
     for (int nt = 0; nt < 3; ++nt) {
+      if (!hit[nt]) continue;
       const double bre = b3[nt] * v2.x, bim = b3[nt] * v2.y;
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
@@ -780,7 +785,8 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
           dmma884(co[mm][nn][0], co[mm][nn][1], cac[mm], bjc[nn]);
         }
 #pragma unroll
-        for (int nt = 0; nt < 3; ++nt) dmma884(lx[mm][nt][0], lx[mm][nt][1], vxc[mm], b3[nt]);
+        for (int nt = 0; nt < 3; ++nt)
+          if (hit[nt]) dmma884(lx[mm][nt][0], lx[mm][nt][1], vxc[mm], b3[nt]);
       }
     }
   }
