@@ -386,6 +386,8 @@ void attach_phases(UniP& P, DBuf<cplx>& buf, cudaStream_t st) {
 }
 size_t uni_smem(const UniP& P) { return (size_t)(P.logN2 >= 0 ? fpad_len(P.N2) : 2 * P.N2) * sizeof(cplx); }
 
+bool interp_mma();  // kernel variant selectors (defined with the launch code)
+
 // ------------------------------------------------------------------ construction
 gs_op* create(const gs_op_desc* dsc) {
   if (!dsc) fail(GS_ERR_USAGE, "null descriptor");
@@ -665,7 +667,7 @@ gs_op* create(const gs_op_desc* dsc) {
         op->cov.upload(hc.data(), hc.size(), st);
         op->covn.upload(hn.data(), hn.size(), st);
       }
-      if (op->fast2d) {
+      if (op->fast2d && !interp_mma()) {  // work units of the DFMA interpolation variant only
         op->units.alloc(total);
         op->ucount.alloc((size_t)B * cap);
         k2f_build_units<<<nblk((int64_t)B * cap, 128), 128, 0, st>>>(op->ch_tile.p, op->ch_s0.p, op->ch_s1.p,

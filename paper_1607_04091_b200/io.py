@@ -37,7 +37,7 @@ def _parse(token: str, context: str) -> float:
         raise FileFormatError(f"cannot parse number '{token}' in {context}") from None
 
 
-def _read_text(path) -> list:
+def _read_text(path) -> bytes:
     try:
         with open(path, "rb") as f:
             raw = f.read()
