@@ -298,3 +298,31 @@ def test_c4_spiral_full_size_apply():
     ref, op = build_pair(2, 4, 9, c, weights=mu, bandwidth=512.0)
     assert op.route == "nfft_2d"
     check_apply(ref, op, rng)
+
+
+def test_dfma_kernel_variants_match_oracle():
+    """The lane-per-column DFMA spreading / fused-pair DFMA interpolation
+    variants (GS_B200_SPREAD=dfma, GS_B200_INTERP=dfma: the A/B baselines of
+    the DMMA kernels) keep parity too.  Run in a subprocess: the library reads
+    the selectors once per process."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, oracle, paper_1607_04091_b200 as gs
+rng = np.random.default_rng(3)
+c = oracle.gen_jitter(64, 0.5, 0.2, 7, 2)
+mu = oracle.voronoi(2, c, 16.5)
+ref = oracle.Op(2, 4, 5, c, weights=mu, bandwidth=16.5)
+op = gs.freq2wave(gs.SamplingSet(2, c), "db4", 5, bandwidth=16.5, weights=mu)
+x = rng.standard_normal(ref.cols) + 1j * rng.standard_normal(ref.cols)
+y = rng.standard_normal(ref.rows) + 1j * rng.standard_normal(ref.rows)
+ef = oracle.rel_error(gs.apply_forward(op, x), ref.forward(x))
+ea = oracle.rel_error(gs.apply_adjoint(op, y), ref.adjoint(y))
+assert ef <= 1e-10 and ea <= 1e-10, (ef, ea)
+print("ok", ef, ea)
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GS_B200_SPREAD="dfma", GS_B200_INTERP="dfma", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.startswith("ok"), r.stdout + r.stderr
