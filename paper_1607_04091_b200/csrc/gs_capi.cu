@@ -788,7 +788,7 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
         const int* pp = perm_io ? op->perm.p : nullptr;
 #define GS_F_INTERP(PP)                                                                                            \
   if (interp_mma())                                                                                                \
-    k2f_interp_mma<PP><<<grid, 32 * F_WARPS * F_IMSPLIT, FInterpM<PP>::bytes(), st>>>(                                       \
+    k2f_interp_mma<PP><<<grid, 32 * F_IWARPS * F_IMSPLIT, FInterpM<PP>::bytes(), st>>>(                                       \
         P, op->ch_tile.p, op->ch_s0.p, op->ch_s1.p, op->ch_count.p, op->cap, op->base_x.p, op->base_y.p,            \
         op->wts_x.p, op->wts_y.p, op->rec_x.p, op->rec_y.p, op->G.p, op->lines.p, x, pp, y);                        \
   else                                                                                                             \

@@ -886,6 +886,9 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
 #ifndef F_IMUNROLL
 #define F_IMUNROLL 3  // sample tiles per loop trip (the next tile's DMMAs overlap this tile's epilogue)
 #endif
+#ifndef F_IWARPS
+#define F_IWARPS 6  // warps (bands of F_T / F_IWARPS sample rows) of the DMMA interpolation CTA
+#endif
 #ifndef F_IMSPLIT
 #define F_IMSPLIT 1  // warps per band (alternate sample tiles)
 #endif
@@ -907,7 +910,7 @@ struct FInterpM {
 };
 
 template <int P>
-__global__ void __launch_bounds__(32 * F_WARPS * F_IMSPLIT, 2)
+__global__ void __launch_bounds__(32 * F_IWARPS * F_IMSPLIT, 2)
 k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ ch_s0, const int* __restrict__ ch_s1,
                const int* __restrict__ ch_count, int cap, const int* __restrict__ base_x,
                const int* __restrict__ base_y, const double* __restrict__ wx_all, const double* __restrict__ wy_all,
@@ -915,7 +918,7 @@ k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
                const cplx* __restrict__ lines, const cplx* __restrict__ x, const int* __restrict__ out_perm,
                cplx* __restrict__ y) {
   using FI = FInterpM<P>;
-  constexpr int S = F_S, T = F_T, R = F_R, BAND = F_BAND, RR = FI::RR, IMU = F_IMUNROLL;
+  constexpr int S = F_S, T = F_T, R = F_R, BAND = F_T / F_IWARPS, RR = FI::RR, IMU = F_IMUNROLL;
   constexpr int E = P >= 2 ? 2 * P : 0, EE = E > 0 ? E : 1;
   extern __shared__ __align__(16) unsigned char fim_raw[];
   double* gre = reinterpret_cast<double*>(fim_raw + FI::GRE);
@@ -996,7 +999,7 @@ k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   }
   __syncthreads();
   bar_wait(&stage_bar, 0);
-  const int band0 = (warp % F_WARPS) * BAND, half = warp / F_WARPS;
+  const int band0 = (warp % F_IWARPS) * BAND, half = warp / F_IWARPS;
   const int sa = rs[band0], sb = rs[band0 + BAND];
   // constant A operands: y-lines [LY_re; LY_im](g, band0 + 4 ks + t), corner block matrix
   double lyA[2][4], crA[2][4];
