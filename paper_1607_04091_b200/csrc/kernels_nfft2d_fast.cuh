@@ -884,7 +884,7 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
 // xor-shuffle over the 8 lanes of the sample finishes every sum.
 #define F_GS 28  // row stride (doubles) of the split re / im region: 8 rows x 4 columns hit 32 banks
 #ifndef F_IMUNROLL
-#define F_IMUNROLL 3  // sample tiles per loop trip (the next tile's DMMAs overlap this tile's epilogue)
+#define F_IMUNROLL 8  // sample tiles per loop trip: a whole band in one trip (DMMAs of one tile overlap the epilogue of another)
 #endif
 #ifndef F_IWARPS
 #define F_IWARPS 6  // warps (bands of F_T / F_IWARPS sample rows) of the DMMA interpolation CTA
