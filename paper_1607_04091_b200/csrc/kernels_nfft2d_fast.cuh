@@ -369,7 +369,8 @@ struct FSpread {
   static constexpr size_t STG_RY = STG_RX + sizeof(cplx) * F_CHUNK * RR + 16;
   static constexpr size_t STG_YS = STG_RY + sizeof(cplx) * F_CHUNK * RR + 16;
   static constexpr size_t STG_OX = STG_YS + sizeof(cplx) * F_CHUNK;
-  static constexpr size_t STG_END = STG_OX + sizeof(int) * F_CHUNK;
+  static constexpr size_t STG_BY = STG_OX + sizeof(int) * F_CHUNK + 16;  // raw window origins (DMMA kernel)
+  static constexpr size_t STG_END = STG_BY + sizeof(int) * F_CHUNK + 16;
   static constexpr size_t FOLD = sizeof(cplx) * (F_WARPS * PER_WARP + F_WARPS * (NCE > 0 ? NCE : 1));
   static constexpr size_t MAIN = (STG_END > FOLD ? STG_END : FOLD);  // fold buffer aliases the staging
   struct Scratch {  // derived per-sample values of one sample pair, shared inside a warp
@@ -668,9 +669,7 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   constexpr int S = F_S, T = F_T, R = F_R, BAND = F_BAND, E = F::E, RR = F::RR, NCE = F::NCE, MU = F_MUNROLL;
   extern __shared__ __align__(16) unsigned char fsm_raw[];
   cplx* s_ys = reinterpret_cast<cplx*>(fsm_raw + F::STG_YS);
-  int* s_ox = reinterpret_cast<int*>(fsm_raw + F::STG_OX);
   __shared__ int rs[T + 1];
-  __shared__ unsigned char s_oy[F_CHUNK];
   const int prob = blockIdx.y, c = blockIdx.x;
   if (c >= ch_count[prob]) return;
   const int tile = ch_tile[prob * cap + c], s0 = ch_s0[prob * cap + c], s1 = ch_s1[prob * cap + c];
@@ -689,29 +688,35 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   const double* s_wx = reinterpret_cast<const double*>(fsm_raw + F::STG_WX + (reinterpret_cast<uintptr_t>(wx_src) & 15));
   const cplx* s_rx = reinterpret_cast<const cplx*>(fsm_raw + F::STG_RX + (reinterpret_cast<uintptr_t>(rx_src) & 15));
   const cplx* s_ry = reinterpret_cast<const cplx*>(fsm_raw + F::STG_RY + (reinterpret_cast<uintptr_t>(ry_src) & 15));
+  // window origins and (sorted-order input) samples ride the same TMA transaction
+  const cplx* ys_src = yin + g0;
+  const int* s_bx = reinterpret_cast<const int*>(fsm_raw + F::STG_OX + (reinterpret_cast<uintptr_t>(base_x + g0) & 15));
+  const int* s_by = reinterpret_cast<const int*>(fsm_raw + F::STG_BY + (reinterpret_cast<uintptr_t>(base_y + g0) & 15));
   if (threadIdx.x == 0) {
     bar_init(&stage_bar);
     bar_expect(&stage_bar, bulk_bytes(wy_src, sizeof(double) * S * n) + bulk_bytes(wx_src, sizeof(double) * S * n) +
-                               bulk_bytes(rx_src, sizeof(cplx) * RR * n) + bulk_bytes(ry_src, sizeof(cplx) * RR * n));
+                               bulk_bytes(rx_src, sizeof(cplx) * RR * n) + bulk_bytes(ry_src, sizeof(cplx) * RR * n) +
+                               bulk_bytes(base_x + g0, sizeof(int) * n) + bulk_bytes(base_y + g0, sizeof(int) * n) +
+                               (in_perm ? 0u : bulk_bytes(ys_src, sizeof(cplx) * n)));
     bulk_stage(fsm_raw + F::STG_WY, wy_src, sizeof(double) * S * n, &stage_bar);
     bulk_stage(fsm_raw + F::STG_WX, wx_src, sizeof(double) * S * n, &stage_bar);
     bulk_stage(fsm_raw + F::STG_RX, rx_src, sizeof(cplx) * RR * n, &stage_bar);
     bulk_stage(fsm_raw + F::STG_RY, ry_src, sizeof(cplx) * RR * n, &stage_bar);
+    bulk_stage(fsm_raw + F::STG_OX, base_x + g0, sizeof(int) * n, &stage_bar);
+    bulk_stage(fsm_raw + F::STG_BY, base_y + g0, sizeof(int) * n, &stage_bar);
+    if (!in_perm) bulk_stage(fsm_raw + F::STG_YS, ys_src, sizeof(cplx) * n, &stage_bar);
   }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int64_t gs = g0 + i;
-    s_ys[i] = ldg2(yin + (int64_t)prob * Pp.M + (in_perm ? (int64_t)in_perm[gs] : (int64_t)(s0 + i)));
-    s_ox[i] = base_x[gs] - tx * T;
-    s_oy[i] = (unsigned char)(base_y[gs] - ty * T);
-  }
+  if (in_perm)  // caller-order input (public apply path): gather
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s_ys[i] = ldg2(yin + (int64_t)prob * Pp.M + in_perm[g0 + i]);
   __syncthreads();  // barrier initialised, samples staged
   bar_wait(&stage_bar, 0);
+  const int ty0 = ty * T, tx0 = tx * T;
   if (threadIdx.x <= T) {  // row starts (samples are sorted by cell, row-major, in a tile)
-    const int key = threadIdx.x;
+    const int key = ty0 + threadIdx.x;
     int lo = 0, hi = n;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if ((int)s_oy[mid] < key) lo = mid + 1;
+      if (s_by[mid] < key) lo = mid + 1;
       else hi = mid;
     }
     rs[threadIdx.x] = lo;
@@ -735,7 +740,7 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
     const int sl = k0 + t;
     const bool valid = sl < sb;
     const int sc = valid ? sl : sa;
-    const int oy = s_oy[sc], ox = s_ox[sc];
+    const int oy = s_by[sc] - ty0, ox = s_bx[sc] - tx0;
     double a1[2], b3[3];
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
