@@ -40,6 +40,18 @@ __device__ __forceinline__ unsigned char* f_stage(unsigned char* dst, const void
   return dst + off;
 }
 __device__ __forceinline__ void f_stage_wait() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+// single asynchronous 8-B / 16-B global -> shared copies (cp.async group; f_stage_wait completes them)
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { f_stage_wait(); }
 
 // TMA bulk staging (cp.async.bulk, one issuing thread, completion on an
 // mbarrier): copy [src, src + bytes) rounded out to 16-B boundaries into dst;
@@ -910,7 +922,9 @@ struct FInterpM {
   static constexpr size_t GIM = GRE + sizeof(double) * F_R * F_GS;
   static constexpr size_t LXRE = GIM + sizeof(double) * F_R * F_GS;
   static constexpr size_t LXIM = LXRE + sizeof(double) * 8 * F_GS;
-  static constexpr size_t END = LXIM + sizeof(double) * 8 * F_GS;
+  static constexpr size_t BX = LXIM + sizeof(double) * 8 * F_GS;  // raw window origins (TMA)
+  static constexpr size_t BY = BX + sizeof(int) * F_CHUNK + 16;
+  static constexpr size_t END = BY + sizeof(int) * F_CHUNK + 16;
   static constexpr size_t bytes() { return END; }
 };
 
@@ -930,10 +944,8 @@ k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   double* gim = reinterpret_cast<double*>(fim_raw + FI::GIM);
   double* lxre = reinterpret_cast<double*>(fim_raw + FI::LXRE);
   double* lxim = reinterpret_cast<double*>(fim_raw + FI::LXIM);
-  __shared__ cplx lys[EE][R];
-  __shared__ cplx cxs[P >= 2 ? 4 * P * P : 1];
-  __shared__ int s_ox[F_CHUNK];
-  __shared__ unsigned char s_oy[F_CHUNK];
+  __shared__ __align__(16) cplx lys[EE][R];
+  __shared__ __align__(16) cplx cxs[P >= 2 ? 4 * P * P : 1];
   __shared__ int rs[T + 1];
   __shared__ __align__(8) uint64_t stage_bar;
   const int prob = blockIdx.y, c = blockIdx.x;
@@ -942,10 +954,14 @@ k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   const int tile = ch_tile[chunk], s0 = ch_s0[chunk], s1 = ch_s1[chunk];
   const int n = s1 - s0;
   const int ty = tile / Pp.nt, tx = tile - ty * Pp.nt;
+  const int ty0 = ty * T, tx0 = tx * T;
   const int n_ov = Pp.n_ov, mask = n_ov - 1, nn = Pp.n;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int64_t g0 = (int64_t)prob * Pp.M + s0;
-  // ---- staging: weights / records by TMA bulk copies; region and lines split into re / im
+  // ---- staging, all of it asynchronous so that no thread waits on one load
+  // before issuing the next: weights / records / window origins by TMA bulk
+  // copies (mbarrier), the grid region and lines by cp.async 8-B copies split
+  // into re / im planes (cp.async group)
   const double* wy_src = wy_all + g0 * S;
   const double* wx_src = wx_all + g0 * S;
   const cplx* rx_src = recx_all + g0 * RR;
@@ -954,56 +970,64 @@ k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   const double* s_wx = reinterpret_cast<const double*>(fim_raw + FI::WX + (reinterpret_cast<uintptr_t>(wx_src) & 15));
   const cplx* s_rx = reinterpret_cast<const cplx*>(fim_raw + FI::RX + (reinterpret_cast<uintptr_t>(rx_src) & 15));
   const cplx* s_ry = reinterpret_cast<const cplx*>(fim_raw + FI::RY + (reinterpret_cast<uintptr_t>(ry_src) & 15));
+  const int* s_bx = reinterpret_cast<const int*>(fim_raw + FI::BX + (reinterpret_cast<uintptr_t>(base_x + g0) & 15));
+  const int* s_by = reinterpret_cast<const int*>(fim_raw + FI::BY + (reinterpret_cast<uintptr_t>(base_y + g0) & 15));
   if (threadIdx.x == 0) {
     bar_init(&stage_bar);
     bar_expect(&stage_bar, bulk_bytes(wy_src, sizeof(double) * S * n) + bulk_bytes(wx_src, sizeof(double) * S * n) +
-                               bulk_bytes(rx_src, sizeof(cplx) * RR * n) + bulk_bytes(ry_src, sizeof(cplx) * RR * n));
+                               bulk_bytes(rx_src, sizeof(cplx) * RR * n) + bulk_bytes(ry_src, sizeof(cplx) * RR * n) +
+                               bulk_bytes(base_x + g0, sizeof(int) * n) + bulk_bytes(base_y + g0, sizeof(int) * n));
     bulk_stage(fim_raw + FI::WY, wy_src, sizeof(double) * S * n, &stage_bar);
     bulk_stage(fim_raw + FI::WX, wx_src, sizeof(double) * S * n, &stage_bar);
     bulk_stage(fim_raw + FI::RX, rx_src, sizeof(cplx) * RR * n, &stage_bar);
     bulk_stage(fim_raw + FI::RY, ry_src, sizeof(cplx) * RR * n, &stage_bar);
+    bulk_stage(fim_raw + FI::BX, base_x + g0, sizeof(int) * n, &stage_bar);
+    bulk_stage(fim_raw + FI::BY, base_y + g0, sizeof(int) * n, &stage_bar);
   }
   const cplx* gp = G + (int64_t)prob * n_ov * n_ov;
+#pragma unroll 4
   for (int i = threadIdx.x; i < R * R; i += blockDim.x) {
     const int r = i / R, cc = i - r * R;
-    const cplx v = ldg2(gp + (int64_t)((ty * T + r) & mask) * n_ov + ((tx * T + cc) & mask));
-    gre[r * F_GS + cc] = v.x;
-    gim[r * F_GS + cc] = v.y;
+    const double* src = reinterpret_cast<const double*>(gp + (int64_t)((ty0 + r) & mask) * n_ov + ((tx0 + cc) & mask));
+    cp_async8(gre + r * F_GS + cc, src);
+    cp_async8(gim + r * F_GS + cc, src + 1);
   }
   if (E > 0) {
     const cplx* LY = lines + (int64_t)prob * 2 * E * n_ov;
     const cplx* LX = LY + (int64_t)E * n_ov;
-    for (int i = threadIdx.x; i < 8 * R; i += blockDim.x) {
+    for (int i = threadIdx.x; i < E * R; i += blockDim.x) {
       const int e = i / R, r = i - e * R;
-      const cplx vx = e < E ? ldg2(LX + (int64_t)e * n_ov + ((tx * T + r) & mask)) : mk(0, 0);
-      lxre[e * F_GS + r] = vx.x;
-      lxim[e * F_GS + r] = vx.y;
-      if (e < E) lys[e][r] = ldg2(LY + (int64_t)e * n_ov + ((ty * T + r) & mask));
+      const double* vx = reinterpret_cast<const double*>(LX + (int64_t)e * n_ov + ((tx0 + r) & mask));
+      cp_async8(lxre + e * F_GS + r, vx);
+      cp_async8(lxim + e * F_GS + r, vx + 1);
+      cp_async16(&lys[e][r], LY + (int64_t)e * n_ov + ((ty0 + r) & mask));
+    }
+    for (int i = E * R + threadIdx.x; i < 8 * R; i += blockDim.x) {  // rows E..7 of the x-line operand are zero
+      const int e = i / R, r = i - e * R;
+      lxre[e * F_GS + r] = 0.0;
+      lxim[e * F_GS + r] = 0.0;
     }
     const cplx* X = x + (int64_t)prob * nn * nn;
     for (int q = threadIdx.x; q < 4 * P * P; q += blockDim.x) {
       const int k = q / (P * P), rem = q - k * P * P, i = rem / P, j = rem - i * P;
       const int row0 = (k < 2) ? 0 : nn - P, col0 = (k % 2 == 0) ? 0 : nn - P;
-      cxs[q] = ldg2(X + (int64_t)(col0 + j) * nn + row0 + i);
+      cp_async16(&cxs[q], X + (int64_t)(col0 + j) * nn + row0 + i);
     }
   }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    s_ox[i] = base_x[g0 + i] - tx * T;
-    s_oy[i] = (unsigned char)(base_y[g0 + i] - ty * T);
-  }
-  __syncthreads();
-  if (threadIdx.x <= T) {  // row starts
-    const int key = threadIdx.x;
+  cp_async_wait_all();
+  __syncthreads();  // barrier initialised, region / lines / corners landed
+  bar_wait(&stage_bar, 0);
+  if (threadIdx.x <= T) {  // row starts (samples are sorted by cell, row-major, in a tile)
+    const int key = ty0 + threadIdx.x;
     int lo = 0, hi = n;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if ((int)s_oy[mid] < key) lo = mid + 1;
+      if (s_by[mid] < key) lo = mid + 1;
       else hi = mid;
     }
     rs[threadIdx.x] = lo;
   }
   __syncthreads();
-  bar_wait(&stage_bar, 0);
   const int band0 = (warp % F_IWARPS) * BAND, half = warp / F_IWARPS;
   const int sa = rs[band0], sb = rs[band0 + BAND];
   // constant A operands: y-lines [LY_re; LY_im](g, band0 + 4 ks + t), corner block matrix
@@ -1029,7 +1053,7 @@ k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
     const int sg = n0 + g;
     const bool vg = sg < sb;
     const int sgc = vg ? sg : sa;
-    const int oyg = s_oy[sgc], oxg = s_ox[sgc];
+    const int oyg = s_by[sgc] - ty0, oxg = s_bx[sgc] - tx0;
     double wb[6], yb[4], cb[4];
 #pragma unroll
     for (int ks = 0; ks < 6; ++ks) {
@@ -1082,7 +1106,7 @@ k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
       const int sn = n0 + 2 * t + j;
       const bool vn = sn < sb;
       const int snc = vn ? sn : sa;
-      const int oyn = s_oy[snc];
+      const int oyn = s_by[snc] - ty0;
       const cplx* rx = s_rx + snc * RR;
       const cplx* ry = s_ry + snc * RR;
       const cplx Dx = rx[0], Dy = ry[0];
