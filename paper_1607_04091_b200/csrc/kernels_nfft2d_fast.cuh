@@ -53,6 +53,44 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { f_stage_wait(); }
 
+// L2 prefetch (cp.async.bulk.prefetch) of [src, src + bytes) rounded out to 16 B
+__device__ __forceinline__ void l2_prefetch(const void* src, size_t bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(src), al = a & ~uintptr_t(15);
+  const unsigned n = (unsigned)((a - al + bytes + 15) & ~size_t(15));
+  if (n) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(al), "r"(n) : "memory");
+}
+// Chunks are dispatched in (problem, chunk) order, about F_PF at a time: a CTA
+// prefetches into L2 the per-sample streams of the chunk F_PF places after its
+// own, so that chunk's TMA staging hits L2 instead of waiting on HBM.
+// (measured on C5: +2% for the spreading, -2% for the interpolation, whose
+// staging is mostly the L2-resident grid region)
+#ifndef F_PF_SPREAD
+#define F_PF_SPREAD 296
+#endif
+#ifndef F_PF_INTERP
+#define F_PF_INTERP 0
+#endif
+template <int RR, int F_PF>
+__device__ __forceinline__ void prefetch_chunk_ahead(int prob, int c, int cap, int B, int M, const int* __restrict__ ch_s0,
+                                                     const int* __restrict__ ch_s1, const int* __restrict__ base_x,
+                                                     const int* __restrict__ base_y, const double* __restrict__ wx_all,
+                                                     const double* __restrict__ wy_all, const cplx* __restrict__ recx_all,
+                                                     const cplx* __restrict__ recy_all, const cplx* __restrict__ ys) {
+  const int64_t lin = (int64_t)prob * cap + c + F_PF;
+  if (F_PF <= 0 || lin >= (int64_t)B * cap) return;
+  const int p2 = (int)(lin / cap);
+  const int a = ch_s0[lin], n = ch_s1[lin] - a;
+  if (n <= 0) return;
+  const int64_t g = (int64_t)p2 * M + a;
+  l2_prefetch(wy_all + g * F_S, sizeof(double) * F_S * n);
+  l2_prefetch(wx_all + g * F_S, sizeof(double) * F_S * n);
+  l2_prefetch(recx_all + g * RR, sizeof(cplx) * RR * n);
+  l2_prefetch(recy_all + g * RR, sizeof(cplx) * RR * n);
+  l2_prefetch(base_x + g, sizeof(int) * n);
+  l2_prefetch(base_y + g, sizeof(int) * n);
+  if (ys) l2_prefetch(ys + g, sizeof(cplx) * n);
+}
+
 // TMA bulk staging (cp.async.bulk, one issuing thread, completion on an
 // mbarrier): copy [src, src + bytes) rounded out to 16-B boundaries into dst;
 // returns src's image in shared memory and adds the copied bytes to *tx.
@@ -718,6 +756,9 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
     bulk_stage(fsm_raw + F::STG_BY, base_y + g0, sizeof(int) * n, &stage_bar);
     if (!in_perm) bulk_stage(fsm_raw + F::STG_YS, ys_src, sizeof(cplx) * n, &stage_bar);
   }
+  if (threadIdx.x == 32)
+    prefetch_chunk_ahead<RR, F_PF_SPREAD>(prob, c, cap, gridDim.y, Pp.M, ch_s0, ch_s1, base_x, base_y, wx_all, wy_all,
+                                          recx_all, recy_all, in_perm ? nullptr : yin);
   if (in_perm)  // caller-order input (public apply path): gather
     for (int i = threadIdx.x; i < n; i += blockDim.x) s_ys[i] = ldg2(yin + (int64_t)prob * Pp.M + in_perm[g0 + i]);
   __syncthreads();  // barrier initialised, samples staged
@@ -752,19 +793,22 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
     const int sl = k0 + t;
     const bool valid = sl < sb;
     const int sc = valid ? sl : sa;
-    const int oy = s_by[sc] - ty0, ox = s_bx[sc] - tx0;
+    // padded K slots get window offsets no tap reaches (all-zero operands)
+    const int oy = valid ? s_by[sc] - ty0 : 64, ox = valid ? s_bx[sc] - tx0 : 64;
     double a1[2], b3[3];
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
       const int d = band0 + mt * 8 + g - oy;
-      const double v = s_wy[sc * S + (d < 0 ? 0 : (d >= S ? S - 1 : d))];
-      a1[mt] = (valid && d >= 0 && d < S) ? v : 0.0;
+      double v = 0.0;
+      if ((unsigned)d < (unsigned)S) v = s_wy[sc * S + d];
+      a1[mt] = v;
     }
 #pragma unroll
     for (int nt = 0; nt < 3; ++nt) {
       const int d = nt * 8 + g - ox;
-      const double v = s_wx[sc * S + (d < 0 ? 0 : (d >= S ? S - 1 : d))];
-      b3[nt] = (valid && d >= 0 && d < S) ? v : 0.0;
+      double v = 0.0;
+      if ((unsigned)d < (unsigned)S) v = s_wx[sc * S + d];
+      b3[nt] = v;
     }
     const cplx* rx = s_rx + sc * RR;
     const cplx* ry = s_ry + sc * RR;
@@ -984,6 +1028,9 @@ k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
     bulk_stage(fim_raw + FI::BX, base_x + g0, sizeof(int) * n, &stage_bar);
     bulk_stage(fim_raw + FI::BY, base_y + g0, sizeof(int) * n, &stage_bar);
   }
+  if (threadIdx.x == 32)
+    prefetch_chunk_ahead<RR, F_PF_INTERP>(prob, c, cap, gridDim.y, Pp.M, ch_s0, ch_s1, base_x, base_y, wx_all, wy_all,
+                                          recx_all, recy_all, nullptr);
   const cplx* gp = G + (int64_t)prob * n_ov * n_ov;
 #pragma unroll 4
   for (int i = threadIdx.x; i < R * R; i += blockDim.x) {
@@ -1053,22 +1100,32 @@ k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
     const int sg = n0 + g;
     const bool vg = sg < sb;
     const int sgc = vg ? sg : sa;
-    const int oyg = s_by[sgc] - ty0, oxg = s_bx[sgc] - tx0;
+    // padded sample slots get window offsets no tap reaches (all-zero B columns)
+    const int oyg = vg ? s_by[sgc] - ty0 : 64, oxg = vg ? s_bx[sgc] - tx0 : 64;
+    const double* wxg = s_wx + sgc * S;
+    const double* wyg = s_wy + sgc * S;
     double wb[6], yb[4], cb[4];
 #pragma unroll
     for (int ks = 0; ks < 6; ++ks) {
       const int d = ks * 4 + t - oxg;
-      const double v = s_wx[sgc * S + (d < 0 ? 0 : (d >= S ? S - 1 : d))];
-      wb[ks] = (vg && d >= 0 && d < S) ? v : 0.0;
+      double v = 0.0;
+      if ((unsigned)d < (unsigned)S) v = wxg[d];
+      wb[ks] = v;
     }
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
       const int d = band0 + ks * 4 + t - oyg;
-      const double v = s_wy[sgc * S + (d < 0 ? 0 : (d >= S ? S - 1 : d))];
-      yb[ks] = (vg && d >= 0 && d < S) ? v : 0.0;
-      const int j = (ks & 1) * 4 + t;
-      const cplx bj = (E > 0 && vg && j < E) ? s_ry[sgc * RR + 1 + (j < E ? j : 0)] : mk(0, 0);
-      cb[ks] = (ks >> 1) ? bj.y : bj.x;
+      double v = 0.0;
+      if ((unsigned)d < (unsigned)S) v = wyg[d];
+      yb[ks] = v;
+    }
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      const int j = kk * 4 + t;
+      cplx bj = mk(0, 0);
+      if (E > 0 && vg && j < E) bj = s_ry[sgc * RR + 1 + j];
+      cb[kk] = bj.x;
+      cb[kk + 2] = bj.y;
     }
     // products
     double h[6][2], uy[2][2], cbo[2][2];
@@ -1114,8 +1171,8 @@ k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
 #pragma unroll
       for (int mh = 0; mh < 2; ++mh) {
         const int d = band0 + mh * 8 + g - oyn;
-        const double wv = s_wy[snc * S + (d < 0 ? 0 : (d >= S ? S - 1 : d))];
-        const double w = (d >= 0 && d < S) ? wv : 0.0;
+        double w = 0.0;
+        if ((unsigned)d < (unsigned)S) w = s_wy[snc * S + d];
         rp = caxpy(rp, w, mk(h[mh][j], h[2 + mh][j]));
       }
       cplx part = cmul(cmul(Dx, Dy), rp);

@@ -31,3 +31,14 @@ for i in sorted(top)[:]:
     rs = sorted(((int(data[i][ci[h]]), h[6:]) for h in reasons), reverse=True)[:3]
     if int(data[i][S]) > 0.01 * tot:
         print(f"{i:5d} {data[i][1].strip()[:50]:50s} " + " ".join(f"{n}:{v}" for v, n in rs if v))
+# executed-instruction mix
+X = ci["Instructions Executed"]
+tx = sum(int(r[X] or 0) for r in data)
+mix = Counter()
+for r in data:
+    t = r[1].split()
+    if not t:
+        continue
+    op = t[1] if t[0].startswith("@") else t[0]
+    mix[op.split(".")[0]] += int(r[X] or 0)
+print("\nexecuted warp instructions", tx, "; mix:", ", ".join(f"{o} {100 * v / tx:.1f}%" for o, v in mix.most_common(18)))
