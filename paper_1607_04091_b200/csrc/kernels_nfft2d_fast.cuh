@@ -128,6 +128,26 @@ __device__ __forceinline__ unsigned char* bulk_stage(unsigned char* dst, const v
   return dst + (a - al);
 }
 
+// Debug-only CTA timeline (build with -DF_TIMELINE): per chunk, the SM id and
+// SM clock at entry, staging complete, compute complete (tools/timeline.py).
+#ifdef F_TIMELINE
+#define F_TL_MAX (1 << 16)
+__device__ unsigned long long g_tl[F_TL_MAX][4];
+__device__ __forceinline__ void tl_stamp(int64_t lin, int k) {
+  if (threadIdx.x == 0 && lin < F_TL_MAX) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_tl[lin][k] = (unsigned long long)clock64();
+    if (k == 0) g_tl[lin][3] = smid;
+  }
+}
+#define F_TL(k) tl_stamp(chunk, k)
+#define F_TL_SYNC() __syncthreads()
+#else
+#define F_TL(k)
+#define F_TL_SYNC()
+#endif
+
 // ------------------------------------------------------------------ interpolation
 // Work units of the interpolation: a chunk's samples are walked in sorted order
 // and consecutive samples in the same cell row whose columns differ by at most
@@ -995,6 +1015,7 @@ k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   const int prob = blockIdx.y, c = blockIdx.x;
   if (c >= ch_count[prob]) return;
   const int64_t chunk = (int64_t)prob * cap + c;
+  F_TL(0);
   const int tile = ch_tile[chunk], s0 = ch_s0[chunk], s1 = ch_s1[chunk];
   const int n = s1 - s0;
   const int ty = tile / Pp.nt, tx = tile - ty * Pp.nt;
@@ -1064,6 +1085,7 @@ k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   cp_async_wait_all();
   __syncthreads();  // barrier initialised, region / lines / corners landed
   bar_wait(&stage_bar, 0);
+  F_TL(1);
   if (threadIdx.x <= T) {  // row starts (samples are sorted by cell, row-major, in a tile)
     const int key = ty0 + threadIdx.x;
     int lo = 0, hi = n;
@@ -1192,4 +1214,6 @@ k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
       }
     }
   }
+  F_TL_SYNC();
+  F_TL(2);
 }
