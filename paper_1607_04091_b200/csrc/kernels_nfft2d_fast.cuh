@@ -992,6 +992,138 @@ struct FInterpM {
   static constexpr size_t bytes() { return END; }
 };
 
+// The forward products of one band of a staged chunk (k2f_interp_mma and the
+// persistent k2f_interp_pipe): sample tiles n0 = sa + 8 half, +8 SPLIT, ...
+template <int P, int SPLIT>
+__device__ __forceinline__ void f_interp_band(int band0, int half, int sa, int sb, int ty0, int tx0,
+                                              const double* __restrict__ s_wx, const double* __restrict__ s_wy,
+                                              const cplx* __restrict__ s_rx, const cplx* __restrict__ s_ry,
+                                              const int* __restrict__ s_bx, const int* __restrict__ s_by,
+                                              const double* __restrict__ gre, const double* __restrict__ gim,
+                                              const double* __restrict__ lxre, const double* __restrict__ lxim,
+                                              const cplx (*__restrict__ lys)[F_R], const cplx* __restrict__ cxs,
+                                              int64_t ybase, int64_t g0, int s0, const int* __restrict__ out_perm,
+                                              cplx* __restrict__ y) {
+  constexpr int S = F_S, R = F_R, RR = 1 + (P >= 2 ? 2 * P : 0), IMU = F_IMUNROLL;
+  constexpr int E = P >= 2 ? 2 * P : 0;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  // constant A operands: y-lines [LY_re; LY_im](g, band0 + 4 ks + t), corner block matrix
+  double lyA[2][4], crA[2][4];
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const int row = band0 + ks * 4 + t;
+    const cplx v = (E > 0 && g < E && row < R) ? lys[g < E ? g : 0][row < R ? row : 0] : mk(0, 0);
+    lyA[0][ks] = v.x;
+    lyA[1][ks] = v.y;
+    const int part = ks >> 1, j = (ks & 1) * 4 + t;  // K index = (re | im part of b, j)
+    cplx cij = mk(0, 0);
+    if (E > 0 && g < E && j < E) {
+      const int hi = g < P ? 0 : 1, ii = g - hi * P, hj = j < P ? 0 : 1, jj = j - hj * P;
+      cij = cxs[(2 * hi + hj) * P * P + ii * P + jj];
+    }
+    crA[0][ks] = part == 0 ? cij.x : -cij.y;  // row block re:  C_re b_re - C_im b_im
+    crA[1][ks] = part == 0 ? cij.y : cij.x;   // row block im:  C_im b_re + C_re b_im
+  }
+#pragma unroll IMU
+  for (int n0 = sa + 8 * half; n0 < sb; n0 += 8 * SPLIT) {
+    // B operands for sample column g
+    const int sg = n0 + g;
+    const bool vg = sg < sb;
+    const int sgc = vg ? sg : sa;
+    // padded sample slots get window offsets no tap reaches (all-zero B columns)
+    const int oyg = vg ? s_by[sgc] - ty0 : 64, oxg = vg ? s_bx[sgc] - tx0 : 64;
+    const double* wxg = s_wx + sgc * S;
+    const double* wyg = s_wy + sgc * S;
+    double wb[6], yb[4], cb[4];
+#pragma unroll
+    for (int ks = 0; ks < 6; ++ks) {
+      const int d = ks * 4 + t - oxg;
+      double v = 0.0;
+      if ((unsigned)d < (unsigned)S) v = wxg[d];
+      wb[ks] = v;
+    }
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      const int d = band0 + ks * 4 + t - oyg;
+      double v = 0.0;
+      if ((unsigned)d < (unsigned)S) v = wyg[d];
+      yb[ks] = v;
+    }
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      const int j = kk * 4 + t;
+      cplx bj = mk(0, 0);
+      if (E > 0 && vg && j < E) bj = s_ry[sgc * RR + 1 + j];
+      cb[kk] = bj.x;
+      cb[kk + 2] = bj.y;
+    }
+    // products
+    double h[6][2], uy[2][2], cbo[2][2];
+#pragma unroll
+    for (int mt = 0; mt < 6; ++mt) h[mt][0] = h[mt][1] = 0.0;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) uy[mt][0] = uy[mt][1] = cbo[mt][0] = cbo[mt][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < 6; ++ks) {
+      const int col = ks * 4 + t;
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const double* src = mt < 2 ? gre : gim;
+        const int row = band0 + (mt & 1) * 8 + g;
+        const double a = row < R ? src[row * F_GS + col] : 0.0;
+        dmma884(h[mt][0], h[mt][1], a, wb[ks]);
+      }
+      if (E > 0) {
+        dmma884(h[4][0], h[4][1], lxre[g * F_GS + col], wb[ks]);
+        dmma884(h[5][0], h[5][1], lxim[g * F_GS + col], wb[ks]);
+      }
+    }
+    if (E > 0) {
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          dmma884(uy[mt][0], uy[mt][1], lyA[mt][ks], yb[ks]);
+          dmma884(cbo[mt][0], cbo[mt][1], crA[mt][ks], cb[ks]);
+        }
+    }
+    // epilogue: lane (g, t) holds row g of every product for samples n0 + 2t + j
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int sn = n0 + 2 * t + j;
+      const bool vn = sn < sb;
+      const int snc = vn ? sn : sa;
+      const int oyn = s_by[snc] - ty0;
+      const cplx* rx = s_rx + snc * RR;
+      const cplx* ry = s_ry + snc * RR;
+      const cplx Dx = rx[0], Dy = ry[0];
+      cplx rp = mk(0, 0);
+#pragma unroll
+      for (int mh = 0; mh < 2; ++mh) {
+        const int d = band0 + mh * 8 + g - oyn;
+        double w = 0.0;
+        if ((unsigned)d < (unsigned)S) w = s_wy[snc * S + d];
+        rp = caxpy(rp, w, mk(h[mh][j], h[2 + mh][j]));
+      }
+      cplx part = cmul(cmul(Dx, Dy), rp);
+      if (E > 0 && g < E) {
+        const cplx ag = rx[1 + g], bg = ry[1 + g];
+        part = cadd(part, cmul(Dx, cmul(bg, mk(h[4][j], h[5][j]))));
+        part = cadd(part, cmul(ag, cadd(cmul(Dy, mk(uy[0][j], uy[1][j])), mk(cbo[0][j], cbo[1][j]))));
+      }
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        part.x += __shfl_xor_sync(0xffffffffu, part.x, o);
+        part.y += __shfl_xor_sync(0xffffffffu, part.y, o);
+      }
+      if (g == 0 && vn) {
+        const int64_t gs = g0 + sn;
+        y[ybase + (out_perm ? (int64_t)out_perm[gs] : (int64_t)(s0 + sn))] = part;
+      }
+    }
+  }
+}
+
 template <int P>
 __global__ void __launch_bounds__(32 * F_IWARPS * F_IMSPLIT, 2)
 k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ ch_s0, const int* __restrict__ ch_s1,
@@ -1099,121 +1231,9 @@ k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   __syncthreads();
   const int band0 = (warp % F_IWARPS) * BAND, half = warp / F_IWARPS;
   const int sa = rs[band0], sb = rs[band0 + BAND];
-  // constant A operands: y-lines [LY_re; LY_im](g, band0 + 4 ks + t), corner block matrix
-  double lyA[2][4], crA[2][4];
-#pragma unroll
-  for (int ks = 0; ks < 4; ++ks) {
-    const int row = band0 + ks * 4 + t;
-    const cplx v = (E > 0 && g < E && row < R) ? lys[g < E ? g : 0][row < R ? row : 0] : mk(0, 0);
-    lyA[0][ks] = v.x;
-    lyA[1][ks] = v.y;
-    const int part = ks >> 1, j = (ks & 1) * 4 + t;  // K index = (re | im part of b, j)
-    cplx cij = mk(0, 0);
-    if (E > 0 && g < E && j < E) {
-      const int hi = g < P ? 0 : 1, ii = g - hi * P, hj = j < P ? 0 : 1, jj = j - hj * P;
-      cij = cxs[(2 * hi + hj) * P * P + ii * P + jj];
-    }
-    crA[0][ks] = part == 0 ? cij.x : -cij.y;  // row block re:  C_re b_re - C_im b_im
-    crA[1][ks] = part == 0 ? cij.y : cij.x;   // row block im:  C_im b_re + C_re b_im
-  }
-#pragma unroll IMU
-  for (int n0 = sa + 8 * half; n0 < sb; n0 += 8 * F_IMSPLIT) {
-    // B operands for sample column g
-    const int sg = n0 + g;
-    const bool vg = sg < sb;
-    const int sgc = vg ? sg : sa;
-    // padded sample slots get window offsets no tap reaches (all-zero B columns)
-    const int oyg = vg ? s_by[sgc] - ty0 : 64, oxg = vg ? s_bx[sgc] - tx0 : 64;
-    const double* wxg = s_wx + sgc * S;
-    const double* wyg = s_wy + sgc * S;
-    double wb[6], yb[4], cb[4];
-#pragma unroll
-    for (int ks = 0; ks < 6; ++ks) {
-      const int d = ks * 4 + t - oxg;
-      double v = 0.0;
-      if ((unsigned)d < (unsigned)S) v = wxg[d];
-      wb[ks] = v;
-    }
-#pragma unroll
-    for (int ks = 0; ks < 4; ++ks) {
-      const int d = band0 + ks * 4 + t - oyg;
-      double v = 0.0;
-      if ((unsigned)d < (unsigned)S) v = wyg[d];
-      yb[ks] = v;
-    }
-#pragma unroll
-    for (int kk = 0; kk < 2; ++kk) {
-      const int j = kk * 4 + t;
-      cplx bj = mk(0, 0);
-      if (E > 0 && vg && j < E) bj = s_ry[sgc * RR + 1 + j];
-      cb[kk] = bj.x;
-      cb[kk + 2] = bj.y;
-    }
-    // products
-    double h[6][2], uy[2][2], cbo[2][2];
-#pragma unroll
-    for (int mt = 0; mt < 6; ++mt) h[mt][0] = h[mt][1] = 0.0;
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt) uy[mt][0] = uy[mt][1] = cbo[mt][0] = cbo[mt][1] = 0.0;
-#pragma unroll
-    for (int ks = 0; ks < 6; ++ks) {
-      const int col = ks * 4 + t;
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
-        const double* src = mt < 2 ? gre : gim;
-        const int row = band0 + (mt & 1) * 8 + g;
-        const double a = row < R ? src[row * F_GS + col] : 0.0;
-        dmma884(h[mt][0], h[mt][1], a, wb[ks]);
-      }
-      if (E > 0) {
-        dmma884(h[4][0], h[4][1], lxre[g * F_GS + col], wb[ks]);
-        dmma884(h[5][0], h[5][1], lxim[g * F_GS + col], wb[ks]);
-      }
-    }
-    if (E > 0) {
-#pragma unroll
-      for (int ks = 0; ks < 4; ++ks)
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          dmma884(uy[mt][0], uy[mt][1], lyA[mt][ks], yb[ks]);
-          dmma884(cbo[mt][0], cbo[mt][1], crA[mt][ks], cb[ks]);
-        }
-    }
-    // epilogue: lane (g, t) holds row g of every product for samples n0 + 2t + j
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int sn = n0 + 2 * t + j;
-      const bool vn = sn < sb;
-      const int snc = vn ? sn : sa;
-      const int oyn = s_by[snc] - ty0;
-      const cplx* rx = s_rx + snc * RR;
-      const cplx* ry = s_ry + snc * RR;
-      const cplx Dx = rx[0], Dy = ry[0];
-      cplx rp = mk(0, 0);
-#pragma unroll
-      for (int mh = 0; mh < 2; ++mh) {
-        const int d = band0 + mh * 8 + g - oyn;
-        double w = 0.0;
-        if ((unsigned)d < (unsigned)S) w = s_wy[snc * S + d];
-        rp = caxpy(rp, w, mk(h[mh][j], h[2 + mh][j]));
-      }
-      cplx part = cmul(cmul(Dx, Dy), rp);
-      if (E > 0 && g < E) {
-        const cplx ag = rx[1 + g], bg = ry[1 + g];
-        part = cadd(part, cmul(Dx, cmul(bg, mk(h[4][j], h[5][j]))));
-        part = cadd(part, cmul(ag, cadd(cmul(Dy, mk(uy[0][j], uy[1][j])), mk(cbo[0][j], cbo[1][j]))));
-      }
-#pragma unroll
-      for (int o = 4; o < 32; o <<= 1) {
-        part.x += __shfl_xor_sync(0xffffffffu, part.x, o);
-        part.y += __shfl_xor_sync(0xffffffffu, part.y, o);
-      }
-      if (g == 0 && vn) {
-        const int64_t gs = g0 + sn;
-        y[(int64_t)prob * Pp.M + (out_perm ? (int64_t)out_perm[gs] : (int64_t)(s0 + sn))] = part;
-      }
-    }
-  }
+  f_interp_band<P, F_IMSPLIT>(band0, half, sa, sb, ty0, tx0, s_wx, s_wy, s_rx, s_ry, s_bx, s_by, gre, gim, lxre, lxim,
+                              lys, cxs, (int64_t)prob * Pp.M, g0, s0, out_perm, y);
   F_TL_SYNC();
   F_TL(2);
 }
+
