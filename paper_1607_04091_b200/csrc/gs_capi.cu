@@ -573,6 +573,7 @@ gs_op* create(const gs_op_desc* dsc) {
     P.nt = (n_ov + P.T - 1) / P.T;
     P.CW = std::max(1, std::min(8, (int)((120 * 1024) / ((fpad_len(n_ov) + 1) * (int)sizeof(cplx)))));
     while (n_ov % P.CW) --P.CW;
+    P.RW = std::max(1, std::min(8, 2048 / n_ov));
     d_xi_x.upload(xi_x.data(), total, st);
     if (d.dim == 2) d_xi_y.upload(xi_y.data(), total, st);
     // 1. windows in the caller's order -> bin keys -> sort
@@ -772,7 +773,7 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
     }
     case GS_ROUTE_NFFT_2D: {
       const NfP& P = op->np;
-      k2_rows_embed_fft<<<dim3(P.n, B), 256, fpad_len(P.n_ov) * sizeof(cplx), st>>>(P, x, op->deconv.p, op->G.p, op->tw.p,
+      k2_rows_embed_fft<<<dim3((P.n + P.RW - 1) / P.RW, B), 256, (size_t)P.RW * (fpad_len(P.n_ov) + 1) * sizeof(cplx), st>>>(P, x, op->deconv.p, op->G.p, op->tw.p,
                                                                           op->logLmax);
       pmark("k2_rows_embed_fft", st);
       k2_cols_fft<<<dim3(P.n_ov / P.CW, B), 256, (size_t)P.CW * (fpad_len(P.n_ov) + 1) * sizeof(cplx), st>>>(P, op->G.p, op->tw.p,
@@ -886,7 +887,7 @@ void adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
       k2_cols_ifft<<<dim3(P.n_ov / P.CW, B), 256, (size_t)P.CW * (fpad_len(P.n_ov) + 1) * sizeof(cplx), st>>>(
           P, op->G.p, op->tw.p, op->logLmax);
       pmark("k2_cols_ifft", st);
-      k2_rows_ifft_crop<<<dim3(P.n, B), 256, fpad_len(P.n_ov) * sizeof(cplx), st>>>(P, op->G.p, op->deconv.p, z, op->tw.p,
+      k2_rows_ifft_crop<<<dim3((P.n + P.RW - 1) / P.RW, B), 256, (size_t)P.RW * (fpad_len(P.n_ov) + 1) * sizeof(cplx), st>>>(P, op->G.p, op->deconv.p, z, op->tw.p,
                                                                           op->logLmax);
       pmark("k2_rows_ifft_crop", st);
       if (P.edges) {

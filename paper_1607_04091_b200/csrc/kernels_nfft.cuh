@@ -24,6 +24,7 @@ struct NfP {
   // 2D tiling
   int T, R, nt; // tile edge, region edge = T + S - 1, tiles per axis
   int CW;       // columns per CTA in the column-FFT kernels
+  int RW;       // rows per CTA in the row-FFT kernels (n_ov * RW / 8 = one 8-point group per thread)
 };
 
 // ============================================================== 1D route
@@ -148,30 +149,28 @@ __global__ void k_n1_ifft_crop(NfP P, const cplx* __restrict__ line, const doubl
 // fastest (freq2wave.cpp:183-190).  Coefficients X(i, j) = x[j*n + i], i = x.
 
 // rows of the embedded interior block, deconvolved, FFT_{-} along x
-// (nufft.cpp:253-266 row part + freq2wave.cpp:246-254)
+// (nufft.cpp:253-266 row part + freq2wave.cpp:246-254); RW rows per CTA
 __global__ void k2_rows_embed_fft(NfP P, const cplx* __restrict__ x, const double* __restrict__ deconv,
                                   cplx* __restrict__ G, const cplx* __restrict__ tw, int logLmax) {
   extern __shared__ cplx sm[];
-  const int j = blockIdx.x, prob = blockIdx.y;
-  const int r = (j - P.n / 2 + P.n_ov) & (P.n_ov - 1);
-  cplx* grow = G + ((int64_t)prob * P.n_ov + r) * P.n_ov;
-  if (P.edges && (j < P.p || j >= P.n - P.p)) {
-    for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) grow[i] = mk(0, 0);
-    return;
-  }
-  const cplx* xr = x + (int64_t)prob * P.n * P.n + (int64_t)j * P.n;
-  for (int i = threadIdx.x; i < fpad_len(P.n_ov); i += blockDim.x) sm[i] = mk(0, 0);
+  const int j0 = blockIdx.x * P.RW, prob = blockIdx.y;
+  const int ls = fpad_len(P.n_ov) + 1, nr = min(P.RW, P.n - j0);
+  for (int i = threadIdx.x; i < P.RW * ls; i += blockDim.x) sm[i] = mk(0, 0);
   __syncthreads();
-  const double d0 = deconv[j];
-  for (int i = threadIdx.x; i < P.n; i += blockDim.x) {
-    cplx v = xr[i];
-    if (P.edges && (i < P.p || i >= P.n - P.p)) v = mk(0, 0);
-    int pos = (i - P.n / 2 + P.n_ov) & (P.n_ov - 1);
-    sm[fpad(bitrev(pos, P.log_nov))] = cscale(v, d0 * deconv[i]);
+  for (int t = threadIdx.x; t < nr * P.n; t += blockDim.x) {
+    const int rr = t / P.n, i = t - rr * P.n, j = j0 + rr;
+    if (P.edges && (j < P.p || j >= P.n - P.p || i < P.p || i >= P.n - P.p)) continue;  // edge rows / slots stay 0
+    const cplx v = x[(int64_t)prob * P.n * P.n + (int64_t)j * P.n + i];
+    const int pos = (i - P.n / 2 + P.n_ov) & (P.n_ov - 1);
+    sm[rr * ls + fpad(bitrev(pos, P.log_nov))] = cscale(v, deconv[j] * deconv[i]);
   }
   __syncthreads();
-  block_fft_padded(sm, P.log_nov, 1, 0, tw, logLmax, -1);
-  for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) grow[i] = sm[fpad(i)];
+  block_fft_padded(sm, P.log_nov, P.RW, ls, tw, logLmax, -1);
+  for (int t = threadIdx.x; t < nr * P.n_ov; t += blockDim.x) {
+    const int rr = t / P.n_ov, i = t - rr * P.n_ov;
+    const int r = (j0 + rr - P.n / 2 + P.n_ov) & (P.n_ov - 1);
+    G[((int64_t)prob * P.n_ov + r) * P.n_ov + i] = sm[rr * ls + fpad(i)];
+  }
 }
 
 // FFT_{-} along y of CW columns; only the n rows carrying data are loaded
@@ -476,22 +475,24 @@ __global__ void k2_cols_ifft(NfP P, cplx* __restrict__ G, const cplx* __restrict
 __global__ void k2_rows_ifft_crop(NfP P, const cplx* __restrict__ G, const double* __restrict__ deconv,
                                   cplx* __restrict__ z, const cplx* __restrict__ tw, int logLmax) {
   extern __shared__ cplx sm[];
-  const int j = blockIdx.x, prob = blockIdx.y;
-  cplx* zr = z + (int64_t)prob * P.n * P.n + (int64_t)j * P.n;
-  if (P.edges && (j < P.p || j >= P.n - P.p)) {
-    for (int i = threadIdx.x; i < P.n; i += blockDim.x) zr[i] = mk(0, 0);
-    return;
+  const int j0 = blockIdx.x * P.RW, prob = blockIdx.y;
+  const int ls = fpad_len(P.n_ov) + 1, nr = min(P.RW, P.n - j0);
+  for (int t = threadIdx.x; t < P.RW * P.n_ov; t += blockDim.x) {
+    const int rr = t / P.n_ov, i = t - rr * P.n_ov;
+    cplx v = mk(0, 0);
+    if (rr < nr) {
+      const int r = (j0 + rr - P.n / 2 + P.n_ov) & (P.n_ov - 1);
+      v = G[((int64_t)prob * P.n_ov + r) * P.n_ov + i];
+    }
+    sm[rr * ls + fpad(bitrev(i, P.log_nov))] = v;
   }
-  const int r = (j - P.n / 2 + P.n_ov) & (P.n_ov - 1);
-  const cplx* grow = G + ((int64_t)prob * P.n_ov + r) * P.n_ov;
-  for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) sm[fpad(bitrev(i, P.log_nov))] = grow[i];
   __syncthreads();
-  block_fft_padded(sm, P.log_nov, 1, 0, tw, logLmax, +1);
-  const double d0 = deconv[j];
-  for (int i = threadIdx.x; i < P.n; i += blockDim.x) {
-    cplx v = cscale(sm[fpad((i - P.n / 2 + P.n_ov) & (P.n_ov - 1))], d0 * deconv[i]);
-    if (P.edges && (i < P.p || i >= P.n - P.p)) v = mk(0, 0);
-    zr[i] = v;
+  block_fft_padded(sm, P.log_nov, P.RW, ls, tw, logLmax, +1);
+  for (int t = threadIdx.x; t < nr * P.n; t += blockDim.x) {
+    const int rr = t / P.n, i = t - rr * P.n, j = j0 + rr;
+    cplx v = cscale(sm[rr * ls + fpad((i - P.n / 2 + P.n_ov) & (P.n_ov - 1))], deconv[j] * deconv[i]);
+    if (P.edges && (j < P.p || j >= P.n - P.p || i < P.p || i >= P.n - P.p)) v = mk(0, 0);
+    z[(int64_t)prob * P.n * P.n + (int64_t)j * P.n + i] = v;
   }
 }
 
