@@ -212,6 +212,8 @@ struct gs_op {
   bool fast2d = false;  // kernels_nfft2d_fast.cuh path (w = 6, p <= 4)
   int cap = 1;          // chunk capacity per problem (2D work list)
   DBuf<int> ch_tile, ch_s0, ch_s1, ch_count, tcs;
+  DBuf<int> fs_start;  // per (problem, tile): range of fold sources (k2_fold_src)
+  DBuf<int4> fsrc;
   DBuf<int2> cov;        // per grid coordinate: (tile, offset) of the regions covering it
   DBuf<int> covn;
   DBuf<unsigned> units;  // fast 2D interpolation work units (k2f_build_units)
@@ -387,6 +389,7 @@ void attach_phases(UniP& P, DBuf<cplx>& buf, cudaStream_t st) {
 size_t uni_smem(const UniP& P) { return (size_t)(P.logN2 >= 0 ? fpad_len(P.N2) : 2 * P.N2) * sizeof(cplx); }
 
 bool interp_mma();  // kernel variant selectors (defined with the launch code)
+bool fold_src();
 
 // ------------------------------------------------------------------ construction
 gs_op* create(const gs_op_desc* dsc) {
@@ -657,6 +660,45 @@ gs_op* create(const gs_op_desc* dsc) {
       op->ch_s1.upload(h_1.data(), h_1.size(), st);
       op->ch_count.upload(h_n.data(), h_n.size(), st);
       op->tcs.upload(tcs.data(), tcs.size(), st);
+      if (op->fast2d) {  // fold sources per tile (k2_fold_src): same order as k2_fold_tiles' coverage loops
+        std::vector<int> fst((size_t)B * (ntiles + 1));
+        std::vector<int4> fs;
+        const int dmax = (P.R + P.T - 1) / P.T;
+        std::vector<int> ct_t, ct_o;  // covering tiles / offsets of a tile's rows (same for columns)
+        for (int64_t b = 0; b < B; ++b) {
+          const int* tb = tcs.data() + b * (ntiles + 1);
+          for (int tyy = 0; tyy < P.nt; ++tyy)
+            for (int txx = 0; txx < P.nt; ++txx) {
+              fst[b * (ntiles + 1) + tyy * P.nt + txx] = (int)fs.size();
+              auto covers = [&](int t0, std::vector<int>& tt, std::vector<int>& oo) {
+                tt.clear();
+                oo.clear();
+                for (int d = 0; d <= dmax && d < P.nt; ++d) {
+                  const int t = ((t0 - d) % P.nt + P.nt) % P.nt;
+                  const int o = ((t0 * P.T - t * P.T) % n_ov + n_ov) % n_ov;
+                  bool any = false;
+                  for (int a = 0; a < P.T && t0 * P.T + a < n_ov; ++a) any |= (o + a) % n_ov < P.R;
+                  if (any) {
+                    tt.push_back(t);
+                    oo.push_back(o);
+                  }
+                }
+              };
+              std::vector<int> ry_t, ry_o, rx_t, rx_o;
+              covers(tyy, ry_t, ry_o);
+              covers(txx, rx_t, rx_o);
+              for (size_t i = 0; i < ry_t.size(); ++i)
+                for (size_t j = 0; j < rx_t.size(); ++j) {
+                  const int tl = ry_t[i] * P.nt + rx_t[j];
+                  for (int ch = tb[tl]; ch < tb[tl + 1]; ++ch) fs.push_back(int4{ch, ry_o[i], rx_o[j], 0});
+                }
+            }
+          fst[b * (ntiles + 1) + ntiles] = (int)fs.size();
+        }
+        op->fs_start.upload(fst.data(), fst.size(), st);
+        op->fsrc.upload(fs.data(), fs.size(), st);
+        CK(cudaStreamSynchronize(st));
+      }
       {  // coverage of each grid coordinate by tile regions (k2_fold_tiles)
         std::vector<int2> hc((size_t)n_ov * MAX_COVER, int2{0, 0});
         std::vector<int> hn(n_ov);
@@ -714,6 +756,13 @@ bool interp_mma() {
   static const bool on = [] {
     const char* e = std::getenv("GS_B200_INTERP");
     return !(e && std::string(e) == "dfma");
+  }();
+  return on;
+}
+bool fold_src() {
+  static const bool on = [] {
+    const char* e = std::getenv("GS_B200_FOLD");
+    return !(e && std::string(e) == "cover");
   }();
   return on;
 }
@@ -881,8 +930,12 @@ void adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
             perm_io ? op->perm.p : nullptr, op->TB.p, op->TL.p, op->TC.p);
         pmark("k2_spread", st);
       }
-      k2_fold_tiles<<<dim3(P.nt * P.nt, B), (P.T * P.T + 31) / 32 * 32, 0, st>>>(P, op->TB.p, op->tcs.p, op->cap,
-                                                                                op->cov.p, op->covn.p, op->G.p);
+      if (op->fast2d && fold_src())
+        k2_fold_src<<<dim3(P.nt * P.nt, B), (P.T * P.T + 31) / 32 * 32, 0, st>>>(P, op->TB.p, op->fs_start.p,
+                                                                               op->fsrc.p, op->cap, op->G.p);
+      else
+        k2_fold_tiles<<<dim3(P.nt * P.nt, B), (P.T * P.T + 31) / 32 * 32, 0, st>>>(P, op->TB.p, op->tcs.p, op->cap,
+                                                                                  op->cov.p, op->covn.p, op->G.p);
       pmark("k2_fold_tiles", st);
       k2_cols_ifft<<<dim3(P.n_ov / P.CW, B), 256, (size_t)P.CW * (fpad_len(P.n_ov) + 1) * sizeof(cplx), st>>>(
           P, op->G.p, op->tw.p, op->logLmax);

@@ -452,6 +452,51 @@ __global__ void k2_fold_tiles(NfP P, const cplx* __restrict__ TB, const int* __r
 }
 
 // FFT_{+} along y for CW columns of G; only the rows the crop keeps are written
+// Same fold, driven by a per-tile source list built at construction
+// (gs_capi.cu): entry (chunk, oy, ox) adds partial chunk[(oy + a) mod n_ov]
+// [(ox + b) mod n_ov] to core cell (a, b) where that lies inside the chunk's
+// region, in the order k2_fold_tiles sums them (row cover, column cover,
+// chunk).  The list sits in shared memory, so each thread's partial loads are
+// independent and issue back to back instead of behind the coverage lookups.
+#define K2_FOLD_SRC 64
+__global__ void k2_fold_src(NfP P, const cplx* __restrict__ TB, const int* __restrict__ fs_start,
+                            const int4* __restrict__ fsrc, int cap, cplx* __restrict__ G) {
+  __shared__ int4 src[K2_FOLD_SRC];
+  const int tile = blockIdx.x, prob = blockIdx.y, ntl = P.nt * P.nt;
+  const int ty = tile / P.nt, tx = tile - ty * P.nt;
+  const cplx* TBp = TB + (int64_t)prob * cap * P.R * P.R;
+  const int f0 = fs_start[(int64_t)prob * (ntl + 1) + tile], f1 = fs_start[(int64_t)prob * (ntl + 1) + tile + 1];
+  const int q = threadIdx.x, a = q / P.T, b = q - (q / P.T) * P.T;
+  const int r = ty * P.T + a, c = tx * P.T + b;
+  const bool live = q < P.T * P.T && r < P.n_ov && c < P.n_ov;
+  cplx acc = mk(0, 0);
+  for (int base = f0; base < f1; base += K2_FOLD_SRC) {
+    const int ns = min(K2_FOLD_SRC, f1 - base);
+    __syncthreads();
+    for (int i = threadIdx.x; i < ns; i += blockDim.x) src[i] = fsrc[base + i];
+    __syncthreads();
+    if (!live) continue;
+    for (int i0 = 0; i0 < ns; i0 += 4) {
+      cplx v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        v[k] = mk(0, 0);
+        if (i0 + k < ns) {
+          const int4 e = src[i0 + k];
+          int la = e.y + a, lb = e.z + b;
+          if (la >= P.n_ov) la -= P.n_ov;
+          if (lb >= P.n_ov) lb -= P.n_ov;
+          if (la < P.R && lb < P.R) v[k] = ldg2(TBp + ((int64_t)e.x * P.R + la) * P.R + lb);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (i0 + k < ns) acc = cadd(acc, v[k]);
+    }
+  }
+  if (live) G[((int64_t)prob * P.n_ov + r) * P.n_ov + c] = acc;
+}
+
 __global__ void k2_cols_ifft(NfP P, cplx* __restrict__ G, const cplx* __restrict__ tw, int logLmax) {
   extern __shared__ cplx sm[];
   const int c0 = blockIdx.x * P.CW, prob = blockIdx.y;
