@@ -1520,10 +1520,10 @@ int gs_weval(int dim, int family_p, int J, int R, const double* coeffs, int64_t 
 // debug builds only: copy the CTA timeline of the last fast-path launch (kernels_nfft2d_fast.cuh)
 int gs_debug_timeline(unsigned long long* host, int64_t rows) {
   const int64_t n = rows < F_TL_MAX ? rows : F_TL_MAX;
-  return cudaMemcpyFromSymbol(host, g_tl, sizeof(unsigned long long) * 4 * n) == cudaSuccess ? 0 : 7;
+  return cudaMemcpyFromSymbol(host, g_tl, sizeof(unsigned long long) * 5 * n) == cudaSuccess ? 0 : 7;
 }
 int gs_debug_timeline_clear() {
-  static unsigned long long zero[F_TL_MAX][4];
+  static unsigned long long zero[F_TL_MAX][5];
   return cudaMemcpyToSymbol(g_tl, zero, sizeof(zero)) == cudaSuccess ? 0 : 7;
 }
 #endif

@@ -132,7 +132,7 @@ __device__ __forceinline__ unsigned char* bulk_stage(unsigned char* dst, const v
 // SM clock at entry, staging complete, compute complete (tools/timeline.py).
 #ifdef F_TIMELINE
 #define F_TL_MAX (1 << 16)
-__device__ unsigned long long g_tl[F_TL_MAX][4];
+__device__ unsigned long long g_tl[F_TL_MAX][5];  // entry, staged, computed, SM id, exit
 __device__ __forceinline__ void tl_stamp(int64_t lin, int k) {
   if (threadIdx.x == 0 && lin < F_TL_MAX) {
     unsigned smid;
@@ -141,11 +141,23 @@ __device__ __forceinline__ void tl_stamp(int64_t lin, int k) {
     if (k == 0) g_tl[lin][3] = smid;
   }
 }
+// F_TIMELINE=1 (or bare -DF_TIMELINE): the interpolation records; 2: the spreading
+#if F_TIMELINE + 0 == 2
+#define F_TLS(k) tl_stamp((int64_t)prob * cap + c, k)
+#define F_TLS_SYNC() __syncthreads()
+#define F_TL(k)
+#define F_TL_SYNC()
+#else
 #define F_TL(k) tl_stamp(chunk, k)
 #define F_TL_SYNC() __syncthreads()
+#define F_TLS(k)
+#define F_TLS_SYNC()
+#endif
 #else
 #define F_TL(k)
 #define F_TL_SYNC()
+#define F_TLS(k)
+#define F_TLS_SYNC()
 #endif
 
 // ------------------------------------------------------------------ interpolation
@@ -742,6 +754,7 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   __shared__ int rs[T + 1];
   const int prob = blockIdx.y, c = blockIdx.x;
   if (c >= ch_count[prob]) return;
+  F_TLS(0);
   const int tile = ch_tile[prob * cap + c], s0 = ch_s0[prob * cap + c], s1 = ch_s1[prob * cap + c];
   const int n = s1 - s0;
   const int ty = tile / Pp.nt, tx = tile - ty * Pp.nt;
@@ -783,6 +796,7 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
     for (int i = threadIdx.x; i < n; i += blockDim.x) s_ys[i] = ldg2(yin + (int64_t)prob * Pp.M + in_perm[g0 + i]);
   __syncthreads();  // barrier initialised, samples staged
   bar_wait(&stage_bar, 0);
+  F_TLS(1);
   const int ty0 = ty * T, tx0 = tx * T;
   if (threadIdx.x <= T) {  // row starts (samples are sorted by cell, row-major, in a tile)
     const int key = ty0 + threadIdx.x;
@@ -871,6 +885,8 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
       }
     }
   }
+  F_TLS_SYNC();
+  F_TLS(2);
   __syncthreads();  // the fold buffer aliases the staging area
   cplx* buf = reinterpret_cast<cplx*>(fsm_raw);
   cplx* mine = buf + band * FM::PER_WARP;  // one record per band; the K-step halves add in turn
@@ -949,6 +965,8 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
       tc[q] = mk(re, im);
     }
   }
+  F_TLS_SYNC();
+  F_TLS(4);
 }
 
 // ------------------------------------------------------------------ interpolation on the FP64 tensor cores

@@ -1,6 +1,6 @@
 #!/usr/bin/env python3
-"""CTA timeline of the fast-path interpolation kernel (debug build with
--DF_TIMELINE: tools/build_variant.sh tl -DF_TIMELINE, then
+"""CTA timeline of the fast-path interpolation (debug build with -DF_TIMELINE)
+or spreading (-DF_TIMELINE=2) kernel: tools/build_variant.sh tl -DF_TIMELINE, then
 GS_B200_LIB=ablibs/tl.so python tools/timeline.py).  Per chunk: SM clock at
 entry, staging complete, compute complete; prints phase lengths and, per SM,
 how much of the kernel span had 0 / 1 / 2+ CTAs in their compute phase."""
@@ -36,18 +36,19 @@ sess.step(1)  # the interpolation launch of this iteration is recorded
 torch.cuda.synchronize()
 sess.close()
 rows = 1 << 16
-buf = np.zeros((rows, 4), dtype=np.uint64)
+buf = np.zeros((rows, 5), dtype=np.uint64)
 assert L.gs_debug_timeline(buf.ctypes.data_as(C.c_void_p), C.c_int64(rows)) == 0
 buf = buf[buf[:, 0] != 0].astype(np.int64)
 t0, t1, t2, sm = buf[:, 0], buf[:, 1], buf[:, 2], buf[:, 3]
 print(f"chunks {len(buf)}; cycles per CTA: staging median {np.median(t1 - t0):.0f} (p90 {np.percentile(t1 - t0, 90):.0f}),"
-      f" compute median {np.median(t2 - t1):.0f} (p90 {np.percentile(t2 - t1, 90):.0f})")
+      f" compute median {np.median(t2 - t1):.0f} (p90 {np.percentile(t2 - t1, 90):.0f})"
+      + (f", fold+write median {np.median(buf[:, 4] - t2):.0f}" if buf[:, 4].any() else ""))
 occ = np.zeros(4)
 spans = []
 for s in np.unique(sm):
     m = sm == s
     a0, a1, a2 = t0[m], t1[m], t2[m]
-    lo, hi = a0.min(), a2.max()
+    lo, hi = a0.min(), max(a2.max(), buf[m, 4].max())
     spans.append(hi - lo)
     ev = sorted([(x, 1) for x in a1] + [(x, -1) for x in a2])
     cur, last = 0, lo
