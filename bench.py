@@ -100,6 +100,8 @@ class ProductGen:
 
 # ------------------------------------------------------------------ roofline bookkeeping
 E2E_CALLS = 3
+# CGLS iterations each config specifies (BASELINE.json configs): one e2e call = one such solve
+CONFIG_ITERS = {"c1": 50, "c2": 100, "c3": 100, "c4": 200, "c5": 100}
 
 
 def algorithmic_bytes(kernel, dim, p, M, Nc, uaxis=None):
@@ -332,16 +334,19 @@ def run_gpu(args):
     # once per operator), then the mean of E2E_CALLS timed calls
     b_host = data.cpu().pin_memory()
     x_host = torch.empty(B * Nc, dtype=torch.complex128).pin_memory()
-    gs_solve_host(op, b_host, x_host, args.steps)
+    e2e_iters = CONFIG_ITERS[args.workload]
+    gs_solve_host(op, b_host, x_host, e2e_iters)
     barrier(world)
     t_e = time.perf_counter()
     for _ in range(E2E_CALLS):
-        xr, stats = gs_solve_host(op, b_host, x_host, args.steps)
+        xr, stats = gs_solve_host(op, b_host, x_host, e2e_iters)
     t_e = (time.perf_counter() - t_e) / E2E_CALLS
     t_e = allreduce_max(t_e, world, dev)
-    e2e_value = P * args.steps / t_e
-    h2d = int(b_host.numel() * 16)
-    d2h = int(x_host.numel() * 16)
+    e2e_value = P * e2e_iters / t_e
+    h2d_call = int(b_host.numel() * 16)
+    import ctypes as C
+    d2h_call = int(x_host.numel() * 16 + B * C.sizeof(gs._Stats))  # solution + per-problem solve stats
+    h2d, d2h = h2d_call // e2e_iters, d2h_call // e2e_iters
 
     out = None
     if rank == 0:
@@ -365,9 +370,12 @@ def run_gpu(args):
             "roofline": roofline, "roofline_iteration": roof_iter,
             "kernel_ms_per_pair": {k: round(v, 4) for k, v in prof.items()},
             "e2e": {"value": round(e2e_value, 3), "unit": "problem-iterations/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "steps_per_call": args.steps, "calls_timed": E2E_CALLS,
-                    "note": "gs_solve_least_squares calls (preamble + steps each) from pinned host memory, "
-                            "after one untimed call; wall clock per call"},
+                    "d2h_bytes_per_step": d2h, "h2d_bytes_per_call": h2d_call, "d2h_bytes_per_call": d2h_call,
+                    "steps_per_call": e2e_iters, "calls_timed": E2E_CALLS,
+                    "note": "one call = the config's whole solve: gs_solve_least_squares (preamble + "
+                            f"{e2e_iters} CGLS iterations, the config's count) from pinned host memory, data in and "
+                            "solution + solve stats out inside the timed region; mean of the timed calls "
+                            "after one untimed call; wall clock per call; per-step bytes = per-call / steps"},
             "clocks": clk, "cpu_baseline": cpu, "build_seconds": round(build_s, 1),
             "final_residual_problem0": st[0].residual,
         }
