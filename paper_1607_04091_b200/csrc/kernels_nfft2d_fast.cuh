@@ -24,7 +24,13 @@
 #define F_S 13
 #define F_T 12
 #define F_R 24
-#define F_CHUNK 160  // samples per work item (chunks of a tile are staged in shared memory)
+#ifndef F_CHUNK
+// samples per work item (chunks of a tile are staged in shared memory): one
+// sample per grid cell fills a 12 x 12 tile exactly, and 144 keeps a spreading
+// CTA's staging under 75 KB so 3 of them fit an SM (C5: 160 -> 144 took the
+// spreading from 12.2 to 10.1 ms per 256 problems)
+#define F_CHUNK 144
+#endif
 
 // cooperative 16-byte copy of [src, src + bytes) global -> shared; the copy starts
 // at the aligned address below src, the returned pointer is src's image
@@ -739,8 +745,11 @@ struct FSpreadM {
   static constexpr size_t bytes() { return (MAIN + 15) / 16 * 16; }
 };
 
+#ifndef F_SBLOCKS
+#define F_SBLOCKS 3  // resident spreading CTAs per SM the register budget is sized for (smem allows 3 at F_CHUNK 144)
+#endif
 template <int P>
-__global__ void __launch_bounds__(32 * F_MWARPS, 2)
+__global__ void __launch_bounds__(32 * F_MWARPS, F_SBLOCKS)
 k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ ch_s0, const int* __restrict__ ch_s1,
                const int* __restrict__ ch_count, int cap, const int* __restrict__ base_x,
                const int* __restrict__ base_y, const double* __restrict__ wx_all, const double* __restrict__ wy_all,
