@@ -994,8 +994,22 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
 #ifndef F_IMUNROLL
 #define F_IMUNROLL 8  // sample tiles per loop trip: a whole band in one trip (DMMAs of one tile overlap the epilogue of another)
 #endif
+#ifndef F_ICONST_RELOAD
+#define F_ICONST_RELOAD 0
+#endif
+// DMMA interpolation CTA shape (measured on C5, 256 problems): 4 warps (bands
+// of 3 sample rows), the factor records read from global memory after an L2
+// prefetch instead of staged, so a CTA needs ~50 KB of shared memory and 4 CTAs
+// (16 warps, 128 registers, a few spills) share an SM: 11.6 ms per apply,
+// against 12.4 ms for 2 CTAs of 6 warps with staged records
+#ifndef F_IREC_GLOBAL
+#define F_IREC_GLOBAL 1  // 1: factor records read from global (L2-prefetched), not staged in shared memory
+#endif
+#ifndef F_IBLOCKS_M
+#define F_IBLOCKS_M 4  // resident DMMA interpolation CTAs per SM the register budget is sized for
+#endif
 #ifndef F_IWARPS
-#define F_IWARPS 6  // warps (bands of F_T / F_IWARPS sample rows) of the DMMA interpolation CTA
+#define F_IWARPS 4  // warps (bands of F_T / F_IWARPS sample rows) of the DMMA interpolation CTA
 #endif
 #ifndef F_IMSPLIT
 #define F_IMSPLIT 1  // warps per band (alternate sample tiles)
@@ -1008,8 +1022,8 @@ struct FInterpM {
   static constexpr size_t WY = 0;
   static constexpr size_t WX = WY + sizeof(double) * F_CHUNK * F_S + 32;
   static constexpr size_t RX = WX + sizeof(double) * F_CHUNK * F_S + 32;
-  static constexpr size_t RY = RX + sizeof(cplx) * F_CHUNK * RR + 16;
-  static constexpr size_t GRE = RY + sizeof(cplx) * F_CHUNK * RR + 16;
+  static constexpr size_t RY = RX + (F_IREC_GLOBAL ? 0 : sizeof(cplx) * F_CHUNK * RR + 16);
+  static constexpr size_t GRE = RY + (F_IREC_GLOBAL ? 0 : sizeof(cplx) * F_CHUNK * RR + 16);
   static constexpr size_t GIM = GRE + sizeof(double) * F_R * F_GS;
   static constexpr size_t LXRE = GIM + sizeof(double) * F_R * F_GS;
   static constexpr size_t LXIM = LXRE + sizeof(double) * 8 * F_GS;
@@ -1035,9 +1049,26 @@ __device__ __forceinline__ void f_interp_band(int band0, int half, int sa, int s
   constexpr int E = P >= 2 ? 2 * P : 0;
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   // constant A operands: y-lines [LY_re; LY_im](g, band0 + 4 ks + t), corner block matrix
+  // (F_ICONST_RELOAD: re-read from shared memory at each use instead of held in 32 registers)
+  auto ly_op = [&](int ks, double* out2) {
+    const int row = band0 + ks * 4 + t;
+    const cplx v = (E > 0 && g < E && row < R) ? lys[g < E ? g : 0][row < R ? row : 0] : mk(0, 0);
+    out2[0] = v.x;
+    out2[1] = v.y;
+  };
+  auto cr_op = [&](int ks, double* out2) {
+    const int part = ks >> 1, j = (ks & 1) * 4 + t;
+    cplx cij = mk(0, 0);
+    if (E > 0 && g < E && j < E) {
+      const int hi = g < P ? 0 : 1, ii = g - hi * P, hj = j < P ? 0 : 1, jj = j - hj * P;
+      cij = cxs[(2 * hi + hj) * P * P + ii * P + jj];
+    }
+    out2[0] = part == 0 ? cij.x : -cij.y;
+    out2[1] = part == 0 ? cij.y : cij.x;
+  };
   double lyA[2][4], crA[2][4];
 #pragma unroll
-  for (int ks = 0; ks < 4; ++ks) {
+  for (int ks = 0; ks < (F_ICONST_RELOAD ? 0 : 4); ++ks) {
     const int row = band0 + ks * 4 + t;
     const cplx v = (E > 0 && g < E && row < R) ? lys[g < E ? g : 0][row < R ? row : 0] : mk(0, 0);
     lyA[0][ks] = v.x;
@@ -1110,8 +1141,16 @@ __device__ __forceinline__ void f_interp_band(int band0, int half, int sa, int s
       for (int ks = 0; ks < 4; ++ks)
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt) {
-          dmma884(uy[mt][0], uy[mt][1], lyA[mt][ks], yb[ks]);
-          dmma884(cbo[mt][0], cbo[mt][1], crA[mt][ks], cb[ks]);
+          if (F_ICONST_RELOAD) {
+            double la[2], ca[2];
+            ly_op(ks, la);
+            cr_op(ks, ca);
+            dmma884(uy[mt][0], uy[mt][1], la[mt], yb[ks]);
+            dmma884(cbo[mt][0], cbo[mt][1], ca[mt], cb[ks]);
+          } else {
+            dmma884(uy[mt][0], uy[mt][1], lyA[mt][ks], yb[ks]);
+            dmma884(cbo[mt][0], cbo[mt][1], crA[mt][ks], cb[ks]);
+          }
         }
     }
     // epilogue: lane (g, t) holds row g of every product for samples n0 + 2t + j
@@ -1152,7 +1191,7 @@ __device__ __forceinline__ void f_interp_band(int band0, int half, int sa, int s
 }
 
 template <int P>
-__global__ void __launch_bounds__(32 * F_IWARPS * F_IMSPLIT, 2)
+__global__ void __launch_bounds__(32 * F_IWARPS * F_IMSPLIT, F_IBLOCKS_M)
 k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ ch_s0, const int* __restrict__ ch_s1,
                const int* __restrict__ ch_count, int cap, const int* __restrict__ base_x,
                const int* __restrict__ base_y, const double* __restrict__ wx_all, const double* __restrict__ wy_all,
@@ -1192,19 +1231,31 @@ k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   const cplx* ry_src = recy_all + g0 * RR;
   const double* s_wy = reinterpret_cast<const double*>(fim_raw + FI::WY + (reinterpret_cast<uintptr_t>(wy_src) & 15));
   const double* s_wx = reinterpret_cast<const double*>(fim_raw + FI::WX + (reinterpret_cast<uintptr_t>(wx_src) & 15));
+#if F_IREC_GLOBAL
+  const cplx* s_rx = rx_src;
+  const cplx* s_ry = ry_src;
+#else
   const cplx* s_rx = reinterpret_cast<const cplx*>(fim_raw + FI::RX + (reinterpret_cast<uintptr_t>(rx_src) & 15));
   const cplx* s_ry = reinterpret_cast<const cplx*>(fim_raw + FI::RY + (reinterpret_cast<uintptr_t>(ry_src) & 15));
+#endif
   const int* s_bx = reinterpret_cast<const int*>(fim_raw + FI::BX + (reinterpret_cast<uintptr_t>(base_x + g0) & 15));
   const int* s_by = reinterpret_cast<const int*>(fim_raw + FI::BY + (reinterpret_cast<uintptr_t>(base_y + g0) & 15));
   if (threadIdx.x == 0) {
     bar_init(&stage_bar);
     bar_expect(&stage_bar, bulk_bytes(wy_src, sizeof(double) * S * n) + bulk_bytes(wx_src, sizeof(double) * S * n) +
-                               bulk_bytes(rx_src, sizeof(cplx) * RR * n) + bulk_bytes(ry_src, sizeof(cplx) * RR * n) +
+                               (F_IREC_GLOBAL ? 0u : bulk_bytes(rx_src, sizeof(cplx) * RR * n) +
+                                                         bulk_bytes(ry_src, sizeof(cplx) * RR * n)) +
                                bulk_bytes(base_x + g0, sizeof(int) * n) + bulk_bytes(base_y + g0, sizeof(int) * n));
+#if F_IREC_GLOBAL
+    l2_prefetch(rx_src, sizeof(cplx) * RR * n);
+    l2_prefetch(ry_src, sizeof(cplx) * RR * n);
+#endif
     bulk_stage(fim_raw + FI::WY, wy_src, sizeof(double) * S * n, &stage_bar);
     bulk_stage(fim_raw + FI::WX, wx_src, sizeof(double) * S * n, &stage_bar);
+#if !F_IREC_GLOBAL
     bulk_stage(fim_raw + FI::RX, rx_src, sizeof(cplx) * RR * n, &stage_bar);
     bulk_stage(fim_raw + FI::RY, ry_src, sizeof(cplx) * RR * n, &stage_bar);
+#endif
     bulk_stage(fim_raw + FI::BX, base_x + g0, sizeof(int) * n, &stage_bar);
     bulk_stage(fim_raw + FI::BY, base_y + g0, sizeof(int) * n, &stage_bar);
   }
