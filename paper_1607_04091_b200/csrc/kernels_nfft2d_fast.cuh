@@ -734,6 +734,9 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 #define F_MUNROLL 2  // K steps per loop trip: the next step's fragments load under this step's DMMAs
 #endif
 
+#ifndef F_SREC_GLOBAL
+#define F_SREC_GLOBAL 0  // 1: factor records read from global (L2-prefetched), not staged in shared memory
+#endif
 template <int P>
 struct FSpreadM {
   static constexpr int E = P >= 2 ? 2 * P : 0;
@@ -741,7 +744,18 @@ struct FSpreadM {
   static constexpr int REG = 16 * F_R, LYN = 8 * 16, LXN = 8 * F_R, PN = 16 * 16 / 2;  // in complex units
   static constexpr int PER_WARP = REG + LYN + LXN + PN;
   static constexpr size_t FOLD = sizeof(cplx) * F_WARPS * PER_WARP;  // one record per band
-  static constexpr size_t MAIN = (FSpread<P>::STG_END > FOLD ? FSpread<P>::STG_END : FOLD);
+  // staging (structure of arrays, sample order; 16 B of slack each); the factor
+  // records only when F_SREC_GLOBAL is 0
+  static constexpr int RR = FSpread<P>::RR;
+  static constexpr size_t WY = 0;
+  static constexpr size_t WX = WY + sizeof(double) * F_CHUNK * F_S + 32;
+  static constexpr size_t YS = WX + sizeof(double) * F_CHUNK * F_S + 32;
+  static constexpr size_t OX = YS + sizeof(cplx) * F_CHUNK;
+  static constexpr size_t BY = OX + sizeof(int) * F_CHUNK + 16;
+  static constexpr size_t RX = BY + sizeof(int) * F_CHUNK + 16;
+  static constexpr size_t RY = RX + (F_SREC_GLOBAL ? 0 : sizeof(cplx) * F_CHUNK * RR + 16);
+  static constexpr size_t STG_END = RY + (F_SREC_GLOBAL ? 0 : sizeof(cplx) * F_CHUNK * RR + 16);
+  static constexpr size_t MAIN = (STG_END > FOLD ? STG_END : FOLD);
   static constexpr size_t bytes() { return (MAIN + 15) / 16 * 16; }
 };
 
@@ -759,7 +773,7 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   using FM = FSpreadM<P>;
   constexpr int S = F_S, T = F_T, R = F_R, BAND = F_BAND, E = F::E, RR = F::RR, NCE = F::NCE, MU = F_MUNROLL;
   extern __shared__ __align__(16) unsigned char fsm_raw[];
-  cplx* s_ys = reinterpret_cast<cplx*>(fsm_raw + F::STG_YS);
+  cplx* s_ys = reinterpret_cast<cplx*>(fsm_raw + FM::YS);
   __shared__ int rs[T + 1];
   const int prob = blockIdx.y, c = blockIdx.x;
   if (c >= ch_count[prob]) return;
@@ -776,27 +790,38 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   const double* wx_src = wx_all + g0 * S;
   const cplx* rx_src = recx_all + g0 * RR;
   const cplx* ry_src = recy_all + g0 * RR;
-  const double* s_wy = reinterpret_cast<const double*>(fsm_raw + F::STG_WY + (reinterpret_cast<uintptr_t>(wy_src) & 15));
-  const double* s_wx = reinterpret_cast<const double*>(fsm_raw + F::STG_WX + (reinterpret_cast<uintptr_t>(wx_src) & 15));
-  const cplx* s_rx = reinterpret_cast<const cplx*>(fsm_raw + F::STG_RX + (reinterpret_cast<uintptr_t>(rx_src) & 15));
-  const cplx* s_ry = reinterpret_cast<const cplx*>(fsm_raw + F::STG_RY + (reinterpret_cast<uintptr_t>(ry_src) & 15));
+  const double* s_wy = reinterpret_cast<const double*>(fsm_raw + FM::WY + (reinterpret_cast<uintptr_t>(wy_src) & 15));
+  const double* s_wx = reinterpret_cast<const double*>(fsm_raw + FM::WX + (reinterpret_cast<uintptr_t>(wx_src) & 15));
+#if F_SREC_GLOBAL
+  const cplx* s_rx = rx_src;
+  const cplx* s_ry = ry_src;
+#else
+  const cplx* s_rx = reinterpret_cast<const cplx*>(fsm_raw + FM::RX + (reinterpret_cast<uintptr_t>(rx_src) & 15));
+  const cplx* s_ry = reinterpret_cast<const cplx*>(fsm_raw + FM::RY + (reinterpret_cast<uintptr_t>(ry_src) & 15));
+#endif
   // window origins and (sorted-order input) samples ride the same TMA transaction
   const cplx* ys_src = yin + g0;
-  const int* s_bx = reinterpret_cast<const int*>(fsm_raw + F::STG_OX + (reinterpret_cast<uintptr_t>(base_x + g0) & 15));
-  const int* s_by = reinterpret_cast<const int*>(fsm_raw + F::STG_BY + (reinterpret_cast<uintptr_t>(base_y + g0) & 15));
+  const int* s_bx = reinterpret_cast<const int*>(fsm_raw + FM::OX + (reinterpret_cast<uintptr_t>(base_x + g0) & 15));
+  const int* s_by = reinterpret_cast<const int*>(fsm_raw + FM::BY + (reinterpret_cast<uintptr_t>(base_y + g0) & 15));
   if (threadIdx.x == 0) {
     bar_init(&stage_bar);
     bar_expect(&stage_bar, bulk_bytes(wy_src, sizeof(double) * S * n) + bulk_bytes(wx_src, sizeof(double) * S * n) +
-                               bulk_bytes(rx_src, sizeof(cplx) * RR * n) + bulk_bytes(ry_src, sizeof(cplx) * RR * n) +
+                               (F_SREC_GLOBAL ? 0u : bulk_bytes(rx_src, sizeof(cplx) * RR * n) +
+                                                         bulk_bytes(ry_src, sizeof(cplx) * RR * n)) +
                                bulk_bytes(base_x + g0, sizeof(int) * n) + bulk_bytes(base_y + g0, sizeof(int) * n) +
                                (in_perm ? 0u : bulk_bytes(ys_src, sizeof(cplx) * n)));
-    bulk_stage(fsm_raw + F::STG_WY, wy_src, sizeof(double) * S * n, &stage_bar);
-    bulk_stage(fsm_raw + F::STG_WX, wx_src, sizeof(double) * S * n, &stage_bar);
-    bulk_stage(fsm_raw + F::STG_RX, rx_src, sizeof(cplx) * RR * n, &stage_bar);
-    bulk_stage(fsm_raw + F::STG_RY, ry_src, sizeof(cplx) * RR * n, &stage_bar);
-    bulk_stage(fsm_raw + F::STG_OX, base_x + g0, sizeof(int) * n, &stage_bar);
-    bulk_stage(fsm_raw + F::STG_BY, base_y + g0, sizeof(int) * n, &stage_bar);
-    if (!in_perm) bulk_stage(fsm_raw + F::STG_YS, ys_src, sizeof(cplx) * n, &stage_bar);
+#if F_SREC_GLOBAL
+    l2_prefetch(rx_src, sizeof(cplx) * RR * n);
+    l2_prefetch(ry_src, sizeof(cplx) * RR * n);
+#else
+    bulk_stage(fsm_raw + FM::RX, rx_src, sizeof(cplx) * RR * n, &stage_bar);
+    bulk_stage(fsm_raw + FM::RY, ry_src, sizeof(cplx) * RR * n, &stage_bar);
+#endif
+    bulk_stage(fsm_raw + FM::WY, wy_src, sizeof(double) * S * n, &stage_bar);
+    bulk_stage(fsm_raw + FM::WX, wx_src, sizeof(double) * S * n, &stage_bar);
+    bulk_stage(fsm_raw + FM::OX, base_x + g0, sizeof(int) * n, &stage_bar);
+    bulk_stage(fsm_raw + FM::BY, base_y + g0, sizeof(int) * n, &stage_bar);
+    if (!in_perm) bulk_stage(fsm_raw + FM::YS, ys_src, sizeof(cplx) * n, &stage_bar);
   }
   if (threadIdx.x == 32)
     prefetch_chunk_ahead<RR, F_PF_SPREAD>(prob, c, cap, gridDim.y, Pp.M, ch_s0, ch_s1, base_x, base_y, wx_all, wy_all,
