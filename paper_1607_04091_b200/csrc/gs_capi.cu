@@ -298,14 +298,20 @@ __global__ void k_gather_d(const double* __restrict__ src, const int* __restrict
   dst[i] = src[(i / M) * M + perm[i]];
 }
 __global__ void k_keys(const int* __restrict__ by, const int* __restrict__ bx, int64_t M, int64_t total, int T, int nt,
-                       unsigned long long* __restrict__ keys, int* __restrict__ vals) {
+                       int band, unsigned long long* __restrict__ keys, int* __restrict__ vals) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= total) return;
   unsigned long long prob = (unsigned long long)(i / M);
-  // 2D: tile-major, then cell (row-major) inside the tile; 1D: cell
-  unsigned long long bin =
-      by ? (unsigned long long)(((by[i] / T) * nt + bx[i] / T) * T * T + (by[i] % T) * T + bx[i] % T)
-         : (unsigned long long)bx[i];
+  // 2D: tile-major, then inside the tile either the cell row-major (band = 0) or
+  // band-major with bands of `band` rows, column-major inside a band (the DMMA
+  // kernels: a warp's 4- / 8-sample K steps then span ~band columns instead of
+  // a row stretch, so fewer column tiles are reached); 1D: cell
+  unsigned long long bin = (unsigned long long)bx[i];
+  if (by) {
+    const int r = by[i] % T, c = bx[i] % T;
+    const int in_tile = band > 0 ? (r / band) * (band * T) + c * band + r % band : r * T + c;
+    bin = (unsigned long long)(((by[i] / T) * nt + bx[i] / T) * T * T + in_tile);
+  }
   keys[i] = (prob << 32) | bin;
   vals[i] = (int)(i - (int64_t)prob * M);
 }
@@ -326,7 +332,7 @@ __global__ void k_bin_starts(const unsigned long long* __restrict__ keys, int64_
 }
 
 // sort the samples of every problem by bin; perm[s] = original index
-void sort_bins(gs_op* op, const int* by, const int* bx, int nbins, int T, int nt, cudaStream_t st) {
+void sort_bins(gs_op* op, const int* by, const int* bx, int nbins, int T, int nt, int band, cudaStream_t st) {
   const int64_t total = op->M * op->B;
   DBuf<unsigned long long> k_in, k_out;
   DBuf<int> v_in;
@@ -334,7 +340,7 @@ void sort_bins(gs_op* op, const int* by, const int* bx, int nbins, int T, int nt
   k_out.alloc(total);
   v_in.alloc(total);
   op->perm.alloc(total);
-  k_keys<<<nblk(total, 256), 256, 0, st>>>(by, bx, op->M, total, T, nt, k_in.p, v_in.p);
+  k_keys<<<nblk(total, 256), 256, 0, st>>>(by, bx, op->M, total, T, nt, band, k_in.p, v_in.p);
   CKL();
   size_t tmp = 0;
   int end_bit = 32 + std::max(1, ilog2(op->B + 1));
@@ -389,6 +395,8 @@ void attach_phases(UniP& P, DBuf<cplx>& buf, cudaStream_t st) {
 size_t uni_smem(const UniP& P) { return (size_t)(P.logN2 >= 0 ? fpad_len(P.N2) : 2 * P.N2) * sizeof(cplx); }
 
 bool interp_mma();  // kernel variant selectors (defined with the launch code)
+bool spread_mma();
+static_assert(F_T / F_WARPS == F_T / F_IWARPS, "the DMMA kernels share the in-tile band order");
 bool fold_src();
 
 // ------------------------------------------------------------------ construction
@@ -588,9 +596,12 @@ gs_op* create(const gs_op_desc* dsc) {
       by0.alloc(total);
       k_kb_window<<<nblk(total, 256), 256, 0, st>>>(d_xi_y.p, total, d.J, n_ov, w, op->beta, by0.p, nullptr);
       CKL();
-      sort_bins(op.get(), by0.p, bx0.p, P.nt * P.nt, P.T, P.nt, st);
+      // band-major order inside tiles for the DMMA kernels (their bands are F_T / F_WARPS rows);
+      // the DFMA A/B variants walk rows and keep the row-major order
+      const int band = (op->fast2d && interp_mma() && spread_mma()) ? F_T / F_WARPS : 0;
+      sort_bins(op.get(), by0.p, bx0.p, P.nt * P.nt, P.T, P.nt, band, st);
     } else {
-      sort_bins(op.get(), nullptr, bx0.p, n_ov, 1, 1, st);
+      sort_bins(op.get(), nullptr, bx0.p, n_ov, 1, 1, 0, st);
     }
     // 2. sorted coordinates -> windows and factors in sorted order
     DBuf<double> sx, sy, ssw;

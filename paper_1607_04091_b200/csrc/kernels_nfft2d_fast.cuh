@@ -1146,8 +1146,13 @@ __device__ __forceinline__ void f_interp_band(int band0, int half, int sa, int s
     for (int mt = 0; mt < 6; ++mt) h[mt][0] = h[mt][1] = 0.0;
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) uy[mt][0] = uy[mt][1] = cbo[mt][0] = cbo[mt][1] = 0.0;
+    // column blocks no sample of the tile reaches are all-zero: skip them (warp-uniform vote)
+    bool hk[6];
+#pragma unroll
+    for (int ks = 0; ks < 6; ++ks) hk[ks] = __any_sync(0xffffffffu, wb[ks] != 0.0);
 #pragma unroll
     for (int ks = 0; ks < 6; ++ks) {
+      if (!hk[ks]) continue;
       const int col = ks * 4 + t;
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) {
