@@ -1184,11 +1184,12 @@ __device__ __forceinline__ void f_interp_band(int band0, int half, int sa, int s
         }
     }
     // epilogue: lane (g, t) holds row g of every product for samples n0 + 2t + j
+    // part = Dx (Dy rp + b_g hx_g) + a_g (Dy uy_g + (C b)_g), then the sum over g
+    cplx pj[2];
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int sn = n0 + 2 * t + j;
-      const bool vn = sn < sb;
-      const int snc = vn ? sn : sa;
+      const int snc = sn < sb ? sn : sa;
       const int oyn = s_by[snc] - ty0;
       const cplx* rx = s_rx + snc * RR;
       const cplx* ry = s_ry + snc * RR;
@@ -1201,21 +1202,33 @@ __device__ __forceinline__ void f_interp_band(int band0, int half, int sa, int s
         if ((unsigned)d < (unsigned)S) w = s_wy[snc * S + d];
         rp = caxpy(rp, w, mk(h[mh][j], h[2 + mh][j]));
       }
-      cplx part = cmul(cmul(Dx, Dy), rp);
+      cplx part;
       if (E > 0 && g < E) {
         const cplx ag = rx[1 + g], bg = ry[1 + g];
-        part = cadd(part, cmul(Dx, cmul(bg, mk(h[4][j], h[5][j]))));
+        part = cmul(Dx, cadd(cmul(Dy, rp), cmul(bg, mk(h[4][j], h[5][j]))));
         part = cadd(part, cmul(ag, cadd(cmul(Dy, mk(uy[0][j], uy[1][j])), mk(cbo[0][j], cbo[1][j]))));
+      } else {
+        part = cmul(Dx, cmul(Dy, rp));
       }
+      pj[j] = part;
+    }
+    // transposing reduction over the 8 lanes of a sample column: the first
+    // exchange leaves lane g with sample 2t + (g & 1) only, so the two later
+    // steps move and add one complex per lane instead of two
+    const int jj = g & 1;
+    const cplx send = jj ? pj[0] : pj[1];
+    cplx acc = jj ? pj[1] : pj[0];
+    acc.x += __shfl_xor_sync(0xffffffffu, send.x, 4);
+    acc.y += __shfl_xor_sync(0xffffffffu, send.y, 4);
 #pragma unroll
-      for (int o = 4; o < 32; o <<= 1) {
-        part.x += __shfl_xor_sync(0xffffffffu, part.x, o);
-        part.y += __shfl_xor_sync(0xffffffffu, part.y, o);
-      }
-      if (g == 0 && vn) {
-        const int64_t gs = g0 + sn;
-        y[ybase + (out_perm ? (int64_t)out_perm[gs] : (int64_t)(s0 + sn))] = part;
-      }
+    for (int o = 8; o < 32; o <<= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    const int sn = n0 + 2 * t + jj;
+    if (g < 2 && sn < sb) {
+      const int64_t gs = g0 + sn;
+      y[ybase + (out_perm ? (int64_t)out_perm[gs] : (int64_t)(s0 + sn))] = acc;
     }
   }
 }
