@@ -258,6 +258,8 @@ void set_smem_attrs() {
   allow_big_smem(k2_lines_fft);
   allow_big_smem(k2_spread);
   allow_big_smem(k2_cols_ifft);
+  allow_big_smem(k2_cols_fft8<true>);
+  allow_big_smem(k2_cols_fft8<false>);
   allow_big_smem(k2_rows_ifft_crop);
   allow_big_smem(k2_edges);
   allow_big_smem(k2f_interp<1>);
@@ -395,6 +397,7 @@ void attach_phases(UniP& P, DBuf<cplx>& buf, cudaStream_t st) {
 size_t uni_smem(const UniP& P) { return (size_t)(P.logN2 >= 0 ? fpad_len(P.N2) : 2 * P.N2) * sizeof(cplx); }
 
 bool interp_mma();  // kernel variant selectors (defined with the launch code)
+bool cols_fft8();
 bool spread_mma();
 static_assert(F_T / F_WARPS == F_T / F_IWARPS, "the DMMA kernels share the in-tile band order");
 bool fold_src();
@@ -582,7 +585,10 @@ gs_op* create(const gs_op_desc* dsc) {
     P.T = op->fast2d ? F_T : std::min(16, n_ov);
     P.R = P.T + P.S - 1;
     P.nt = (n_ov + P.T - 1) / P.T;
-    P.CW = std::max(1, std::min(8, (int)((120 * 1024) / ((fpad_len(n_ov) + 1) * (int)sizeof(cplx)))));
+#ifndef F_CWMAX
+#define F_CWMAX 8
+#endif
+    P.CW = std::max(1, std::min(F_CWMAX, (int)((120 * 1024) / ((fpad_len(n_ov) + 1) * (int)sizeof(cplx)))));
     while (n_ov % P.CW) --P.CW;
     P.RW = std::max(1, std::min(8, 2048 / n_ov));
     d_xi_x.upload(xi_x.data(), total, st);
@@ -777,6 +783,13 @@ bool fold_src() {
   }();
   return on;
 }
+bool cols_fft8() {  // radix-8 column FFTs with global I/O in the first / last pass (default for n_ov = 8^k)
+  static const bool on = [] {
+    const char* e = std::getenv("GS_B200_COLFFT");
+    return !(e && std::string(e) == "smem");
+  }();
+  return on;
+}
 bool spread_mma() {
   static const bool on = [] {
     const char* e = std::getenv("GS_B200_SPREAD");
@@ -836,8 +849,13 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
       k2_rows_embed_fft<<<dim3((P.n + P.RW - 1) / P.RW, B), 256, (size_t)P.RW * (fpad_len(P.n_ov) + 1) * sizeof(cplx), st>>>(P, x, op->deconv.p, op->G.p, op->tw.p,
                                                                           op->logLmax);
       pmark("k2_rows_embed_fft", st);
-      k2_cols_fft<<<dim3(P.n_ov / P.CW, B), 256, (size_t)P.CW * (fpad_len(P.n_ov) + 1) * sizeof(cplx), st>>>(P, op->G.p, op->tw.p,
-                                                                                                   op->logLmax);
+      if (P.log_nov % 3 == 0 && op->logLmax == P.log_nov && cols_fft8())
+        k2_cols_fft8<true><<<dim3(P.n_ov / P.CW, B), 256,
+                              ((size_t)P.CW * (fpad_len(P.n_ov) + 1) + P.n_ov / 2) * sizeof(cplx), st>>>(P, op->G.p,
+                                                                                                        op->tw.p);
+      else
+        k2_cols_fft<<<dim3(P.n_ov / P.CW, B), 256, (size_t)P.CW * (fpad_len(P.n_ov) + 1) * sizeof(cplx), st>>>(
+            P, op->G.p, op->tw.p, op->logLmax);
       pmark("k2_cols_fft", st);
       if (P.edges) {
         k2_lines_fft<<<dim3(4 * P.p, B), 256, fpad_len(P.n_ov) * sizeof(cplx), st>>>(P, x, op->deconv.p, op->lines.p, op->tw.p,
@@ -948,7 +966,12 @@ void adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
         k2_fold_tiles<<<dim3(P.nt * P.nt, B), (P.T * P.T + 31) / 32 * 32, 0, st>>>(P, op->TB.p, op->tcs.p, op->cap,
                                                                                   op->cov.p, op->covn.p, op->G.p);
       pmark("k2_fold_tiles", st);
-      k2_cols_ifft<<<dim3(P.n_ov / P.CW, B), 256, (size_t)P.CW * (fpad_len(P.n_ov) + 1) * sizeof(cplx), st>>>(
+      if (P.log_nov % 3 == 0 && op->logLmax == P.log_nov && cols_fft8())
+        k2_cols_fft8<false><<<dim3(P.n_ov / P.CW, B), 256,
+                               ((size_t)P.CW * (fpad_len(P.n_ov) + 1) + P.n_ov / 2) * sizeof(cplx), st>>>(P, op->G.p,
+                                                                                                         op->tw.p);
+      else
+        k2_cols_ifft<<<dim3(P.n_ov / P.CW, B), 256, (size_t)P.CW * (fpad_len(P.n_ov) + 1) * sizeof(cplx), st>>>(
           P, op->G.p, op->tw.p, op->logLmax);
       pmark("k2_cols_ifft", st);
       k2_rows_ifft_crop<<<dim3((P.n + P.RW - 1) / P.RW, B), 256, (size_t)P.RW * (fpad_len(P.n_ov) + 1) * sizeof(cplx), st>>>(P, op->G.p, op->deconv.p, z, op->tw.p,

@@ -628,3 +628,79 @@ __global__ void k2_edges(NfP P, const cplx* __restrict__ TLF, const cplx* __rest
     else Z[(int64_t)fixed * n + v] = val;        // Z(i, j_e)
   }
 }
+
+// ------------------------------------------------------------------ column FFTs, radix-8 passes with global I/O
+// Same transform as k2_cols_fft / k2_cols_ifft (radix-2 DIT on bit-reversed
+// input, three stages fused per pass) for n_ov = 8^k: the first pass gathers
+// its 8 bit-reversed rows straight from global memory into registers and the
+// last pass stores its 8 rows straight back, so a 512-point column costs two
+// shared-memory round trips instead of four plus the load / store copies; the
+// twiddles sit in shared memory.  Thread (j, cc): column c0 + cc, lanes run
+// along the CW columns so every row access is a CW x 16 B segment.
+// FWD: forward (FFT_-), only the n rows carrying data are read (the zero rows
+// of the embedded block are skipped); else inverse (FFT_+), only the n rows
+// the crop keeps are stored.
+template <bool FWD>
+__device__ __forceinline__ void r8_pass(cplx* v, int jh, int h, const cplx* __restrict__ tws, int L, int s) {
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      if ((m >> q) & 1) continue;
+      const int k = jh + (m & ((1 << q) - 1)) * h;
+      cplx w = tws[k << (L - (s + q))];
+      if (!FWD) w.y = -w.y;
+      const cplx u = v[m], x = cmul(v[m + (1 << q)], w);
+      v[m] = cadd(u, x);
+      v[m + (1 << q)] = csub(u, x);
+    }
+  }
+}
+
+template <bool FWD>
+__global__ void k2_cols_fft8(NfP P, cplx* __restrict__ G, const cplx* __restrict__ tw) {
+  extern __shared__ cplx sm[];
+  const int L = P.log_nov, N = P.n_ov, CW = P.CW;
+  const int ls = fpad_len(N) + 1;
+  cplx* tws = sm + CW * ls;  // N / 2 twiddles
+  const int c0 = blockIdx.x * CW, prob = blockIdx.y;
+  cplx* g = G + (int64_t)prob * N * N;
+  for (int i = threadIdx.x; i < N / 2; i += blockDim.x) tws[i] = tw[i];
+  __syncthreads();
+  const int groups = N / 8, nthr = groups * CW;
+  const int half = P.n / 2;
+  int s = 1;
+  for (int pass = 0; 3 * pass < L; ++pass, s += 3) {
+    const int h = 1 << (s - 1);
+    const bool first = pass == 0, last = s + 3 > L;
+    for (int tix = threadIdx.x; tix < nthr; tix += blockDim.x) {
+      const int cc = tix % CW, j = tix / CW;
+      const int jh = j & (h - 1);
+      const int i0 = (j >> (s - 1)) * (8 * h) + jh;
+      cplx* base = sm + cc * ls;
+      cplx v[8];
+      if (first) {
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          const int r = bitrev(i0 + m, L);  // input row of bit-reversed position i0 + m
+          v[m] = (!FWD || r < half || r >= N - half) ? g[(int64_t)r * N + c0 + cc] : mk(0, 0);
+        }
+      } else {
+#pragma unroll
+        for (int m = 0; m < 8; ++m) v[m] = base[fpad(i0 + m * h)];
+      }
+      r8_pass<FWD>(v, jh, h, tws, L, s);
+      if (last) {
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          const int r = i0 + m * h;
+          if (FWD || r < half || r >= N - half) g[(int64_t)r * N + c0 + cc] = v[m];
+        }
+      } else {
+#pragma unroll
+        for (int m = 0; m < 8; ++m) base[fpad(i0 + m * h)] = v[m];
+      }
+    }
+    __syncthreads();
+  }
+}
