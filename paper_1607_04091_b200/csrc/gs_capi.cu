@@ -849,7 +849,7 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
       k2_rows_embed_fft<<<dim3((P.n + P.RW - 1) / P.RW, B), 256, (size_t)P.RW * (fpad_len(P.n_ov) + 1) * sizeof(cplx), st>>>(P, x, op->deconv.p, op->G.p, op->tw.p,
                                                                           op->logLmax);
       pmark("k2_rows_embed_fft", st);
-      if (P.log_nov % 3 == 0 && op->logLmax == P.log_nov && cols_fft8())
+      if (op->logLmax == P.log_nov && cols_fft8())
         k2_cols_fft8<true><<<dim3(P.n_ov / P.CW, B), 256,
                               ((size_t)P.CW * (fpad_len(P.n_ov) + 1) + P.n_ov / 2) * sizeof(cplx), st>>>(P, op->G.p,
                                                                                                         op->tw.p);
@@ -966,7 +966,7 @@ void adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
         k2_fold_tiles<<<dim3(P.nt * P.nt, B), (P.T * P.T + 31) / 32 * 32, 0, st>>>(P, op->TB.p, op->tcs.p, op->cap,
                                                                                   op->cov.p, op->covn.p, op->G.p);
       pmark("k2_fold_tiles", st);
-      if (P.log_nov % 3 == 0 && op->logLmax == P.log_nov && cols_fft8())
+      if (op->logLmax == P.log_nov && cols_fft8())
         k2_cols_fft8<false><<<dim3(P.n_ov / P.CW, B), 256,
                                ((size_t)P.CW * (fpad_len(P.n_ov) + 1) + P.n_ov / 2) * sizeof(cplx), st>>>(P, op->G.p,
                                                                                                          op->tw.p);

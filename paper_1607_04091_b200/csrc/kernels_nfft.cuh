@@ -640,12 +640,13 @@ __global__ void k2_edges(NfP P, const cplx* __restrict__ TLF, const cplx* __rest
 // FWD: forward (FFT_-), only the n rows carrying data are read (the zero rows
 // of the embedded block are skipped); else inverse (FFT_+), only the n rows
 // the crop keeps are stored.
-template <bool FWD>
+template <bool FWD, int NST>
 __device__ __forceinline__ void r8_pass(cplx* v, int jh, int h, const cplx* __restrict__ tws, int L, int s) {
+  constexpr int GN = 1 << NST;
 #pragma unroll
-  for (int q = 0; q < 3; ++q) {
+  for (int q = 0; q < NST; ++q) {
 #pragma unroll
-    for (int m = 0; m < 8; ++m) {
+    for (int m = 0; m < GN; ++m) {
       if ((m >> q) & 1) continue;
       const int k = jh + (m & ((1 << q) - 1)) * h;
       cplx w = tws[k << (L - (s + q))];
@@ -653,6 +654,44 @@ __device__ __forceinline__ void r8_pass(cplx* v, int jh, int h, const cplx* __re
       const cplx u = v[m], x = cmul(v[m + (1 << q)], w);
       v[m] = cadd(u, x);
       v[m + (1 << q)] = csub(u, x);
+    }
+  }
+}
+
+// one pass of NST fused stages starting at stage s over the CTA's CW columns
+template <bool FWD, int NST>
+__device__ __forceinline__ void cols_pass(const NfP& P, cplx* __restrict__ g, cplx* sm, const cplx* __restrict__ tws,
+                                          int ls, int c0, int s, bool first, bool last) {
+  constexpr int GN = 1 << NST;
+  const int L = P.log_nov, N = P.n_ov, CW = P.CW, half = P.n / 2;
+  const int h = 1 << (s - 1);
+  const int nthr = (N / GN) * CW;
+  for (int tix = threadIdx.x; tix < nthr; tix += blockDim.x) {
+    const int cc = tix % CW, j = tix / CW;
+    const int jh = j & (h - 1);
+    const int i0 = (j >> (s - 1)) * (GN * h) + jh;
+    cplx* base = sm + cc * ls;
+    cplx v[GN];
+    if (first) {
+#pragma unroll
+      for (int m = 0; m < GN; ++m) {
+        const int r = bitrev(i0 + m, L);  // input row of bit-reversed position i0 + m
+        v[m] = (!FWD || r < half || r >= N - half) ? g[(int64_t)r * N + c0 + cc] : mk(0, 0);
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < GN; ++m) v[m] = base[fpad(i0 + m * h)];
+    }
+    r8_pass<FWD, NST>(v, jh, h, tws, L, s);
+    if (last) {
+#pragma unroll
+      for (int m = 0; m < GN; ++m) {
+        const int r = i0 + m * h;
+        if (FWD || r < half || r >= N - half) g[(int64_t)r * N + c0 + cc] = v[m];
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < GN; ++m) base[fpad(i0 + m * h)] = v[m];
     }
   }
 }
@@ -667,40 +706,13 @@ __global__ void k2_cols_fft8(NfP P, cplx* __restrict__ G, const cplx* __restrict
   cplx* g = G + (int64_t)prob * N * N;
   for (int i = threadIdx.x; i < N / 2; i += blockDim.x) tws[i] = tw[i];
   __syncthreads();
-  const int groups = N / 8, nthr = groups * CW;
-  const int half = P.n / 2;
-  int s = 1;
-  for (int pass = 0; 3 * pass < L; ++pass, s += 3) {
-    const int h = 1 << (s - 1);
-    const bool first = pass == 0, last = s + 3 > L;
-    for (int tix = threadIdx.x; tix < nthr; tix += blockDim.x) {
-      const int cc = tix % CW, j = tix / CW;
-      const int jh = j & (h - 1);
-      const int i0 = (j >> (s - 1)) * (8 * h) + jh;
-      cplx* base = sm + cc * ls;
-      cplx v[8];
-      if (first) {
-#pragma unroll
-        for (int m = 0; m < 8; ++m) {
-          const int r = bitrev(i0 + m, L);  // input row of bit-reversed position i0 + m
-          v[m] = (!FWD || r < half || r >= N - half) ? g[(int64_t)r * N + c0 + cc] : mk(0, 0);
-        }
-      } else {
-#pragma unroll
-        for (int m = 0; m < 8; ++m) v[m] = base[fpad(i0 + m * h)];
-      }
-      r8_pass<FWD>(v, jh, h, tws, L, s);
-      if (last) {
-#pragma unroll
-        for (int m = 0; m < 8; ++m) {
-          const int r = i0 + m * h;
-          if (FWD || r < half || r >= N - half) g[(int64_t)r * N + c0 + cc] = v[m];
-        }
-      } else {
-#pragma unroll
-        for (int m = 0; m < 8; ++m) base[fpad(i0 + m * h)] = v[m];
-      }
-    }
+  for (int s = 1; s <= L;) {
+    const int nst = L - s + 1 >= 3 ? 3 : L - s + 1;
+    const bool first = s == 1, last = s + nst > L;
+    if (nst == 3) cols_pass<FWD, 3>(P, g, sm, tws, ls, c0, s, first, last);
+    else if (nst == 2) cols_pass<FWD, 2>(P, g, sm, tws, ls, c0, s, first, last);
+    else cols_pass<FWD, 1>(P, g, sm, tws, ls, c0, s, first, last);
     __syncthreads();
+    s += nst;
   }
 }
