@@ -259,6 +259,8 @@ void set_smem_attrs() {
   allow_big_smem(k2_spread);
   allow_big_smem(k2_cols_ifft);
   allow_big_smem(k2_cols_fft8<true>);
+  allow_big_smem(k2_rows_fft8<true>);
+  allow_big_smem(k2_rows_fft8<false>);
   allow_big_smem(k2_cols_fft8<false>);
   allow_big_smem(k2_rows_ifft_crop);
   allow_big_smem(k2_edges);
@@ -398,6 +400,7 @@ size_t uni_smem(const UniP& P) { return (size_t)(P.logN2 >= 0 ? fpad_len(P.N2) :
 
 bool interp_mma();  // kernel variant selectors (defined with the launch code)
 bool cols_fft8();
+bool rows_fft8();
 bool spread_mma();
 static_assert(F_T / F_WARPS == F_T / F_IWARPS, "the DMMA kernels share the in-tile band order");
 bool fold_src();
@@ -790,6 +793,13 @@ bool cols_fft8() {  // radix-8 column FFTs with global I/O in the first / last p
   }();
   return on;
 }
+bool rows_fft8() {  // row FFTs with global I/O in the first / last pass (default)
+  static const bool on = [] {
+    const char* e = std::getenv("GS_B200_ROWFFT");
+    return !(e && std::string(e) == "smem");
+  }();
+  return on;
+}
 bool spread_mma() {
   static const bool on = [] {
     const char* e = std::getenv("GS_B200_SPREAD");
@@ -846,7 +856,12 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
     }
     case GS_ROUTE_NFFT_2D: {
       const NfP& P = op->np;
-      k2_rows_embed_fft<<<dim3((P.n + P.RW - 1) / P.RW, B), 256, (size_t)P.RW * (fpad_len(P.n_ov) + 1) * sizeof(cplx), st>>>(P, x, op->deconv.p, op->G.p, op->tw.p,
+      if (op->logLmax == P.log_nov && rows_fft8())
+        k2_rows_fft8<true><<<dim3((P.n + P.RW - 1) / P.RW, B), 256,
+                              ((size_t)P.RW * (fpad_len(P.n_ov) + 1) + P.n_ov / 2) * sizeof(cplx), st>>>(
+            P, x, op->deconv.p, op->G.p, op->tw.p);
+      else
+        k2_rows_embed_fft<<<dim3((P.n + P.RW - 1) / P.RW, B), 256, (size_t)P.RW * (fpad_len(P.n_ov) + 1) * sizeof(cplx), st>>>(P, x, op->deconv.p, op->G.p, op->tw.p,
                                                                           op->logLmax);
       pmark("k2_rows_embed_fft", st);
       if (op->logLmax == P.log_nov && cols_fft8())
@@ -974,7 +989,12 @@ void adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
         k2_cols_ifft<<<dim3(P.n_ov / P.CW, B), 256, (size_t)P.CW * (fpad_len(P.n_ov) + 1) * sizeof(cplx), st>>>(
           P, op->G.p, op->tw.p, op->logLmax);
       pmark("k2_cols_ifft", st);
-      k2_rows_ifft_crop<<<dim3((P.n + P.RW - 1) / P.RW, B), 256, (size_t)P.RW * (fpad_len(P.n_ov) + 1) * sizeof(cplx), st>>>(P, op->G.p, op->deconv.p, z, op->tw.p,
+      if (op->logLmax == P.log_nov && rows_fft8())
+        k2_rows_fft8<false><<<dim3((P.n + P.RW - 1) / P.RW, B), 256,
+                               ((size_t)P.RW * (fpad_len(P.n_ov) + 1) + P.n_ov / 2) * sizeof(cplx), st>>>(
+            P, op->G.p, op->deconv.p, z, op->tw.p);
+      else
+        k2_rows_ifft_crop<<<dim3((P.n + P.RW - 1) / P.RW, B), 256, (size_t)P.RW * (fpad_len(P.n_ov) + 1) * sizeof(cplx), st>>>(P, op->G.p, op->deconv.p, z, op->tw.p,
                                                                           op->logLmax);
       pmark("k2_rows_ifft_crop", st);
       if (P.edges) {

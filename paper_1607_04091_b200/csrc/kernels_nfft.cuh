@@ -716,3 +716,92 @@ __global__ void k2_cols_fft8(NfP P, cplx* __restrict__ G, const cplx* __restrict
     s += nst;
   }
 }
+
+// ------------------------------------------------------------------ row FFTs with global I/O in the first / last pass
+// k2_rows_embed_fft / k2_rows_ifft_crop restated the same way as k2_cols_fft8:
+// the first pass gathers its bit-reversed inputs from global memory (the
+// embedded, deconvolved row of X for the forward; the row of G for the
+// inverse) and the last pass writes its outputs (the whole row of G; the
+// cropped, deconvolved row of Z), twiddles in shared memory.
+template <bool FWD, int NST>
+__device__ __forceinline__ void rows_pass(const NfP& P, const cplx* __restrict__ src, cplx* __restrict__ dst,
+                                          const double* __restrict__ deconv, cplx* sm, const cplx* __restrict__ tws,
+                                          int ls, int j0, int nr, int s, bool first, bool last) {
+  constexpr int GN = 1 << NST;
+  const int L = P.log_nov, N = P.n_ov, n = P.n, half = n / 2;
+  const int h = 1 << (s - 1);
+  const int groups = N / GN, nthr = groups * P.RW;
+  for (int tix = threadIdx.x; tix < nthr; tix += blockDim.x) {
+    const int rr = tix / groups, j = tix - rr * groups;
+    const int jy = j0 + rr;  // coefficient row (y index) of this line
+    const int jh = j & (h - 1);
+    const int i0 = (j >> (s - 1)) * (GN * h) + jh;
+    cplx* base = sm + rr * ls;
+    cplx v[GN];
+    if (first) {
+#pragma unroll
+      for (int m = 0; m < GN; ++m) {
+        const int pos = bitrev(i0 + m, L);  // grid column held by bit-reversed position i0 + m
+        cplx a = mk(0, 0);
+        if (rr < nr) {
+          if (FWD) {  // embedded X(i, jy) deconvolved, edge rows / slots zero
+            const int i = (pos + half) & (N - 1);
+            if (i < n && !(P.edges && (jy < P.p || jy >= n - P.p || i < P.p || i >= n - P.p)))
+              a = cscale(src[(int64_t)jy * n + i], deconv[jy] * deconv[i]);
+          } else {
+            a = src[(int64_t)((jy - half + N) & (N - 1)) * N + pos];
+          }
+        }
+        v[m] = a;
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < GN; ++m) v[m] = base[fpad(i0 + m * h)];
+    }
+    r8_pass<FWD, NST>(v, jh, h, tws, L, s);
+    if (last) {
+      if (rr < nr) {
+#pragma unroll
+        for (int m = 0; m < GN; ++m) {
+          const int pos = i0 + m * h;
+          if (FWD) {
+            dst[(int64_t)((jy - half + N) & (N - 1)) * N + pos] = v[m];
+          } else {
+            const int i = (pos + half) & (N - 1);  // crop: grid column pos -> coefficient index i
+            if (i < n) {
+              cplx z = cscale(v[m], deconv[jy] * deconv[i]);
+              if (P.edges && (jy < P.p || jy >= n - P.p || i < P.p || i >= n - P.p)) z = mk(0, 0);
+              dst[(int64_t)jy * n + i] = z;
+            }
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < GN; ++m) base[fpad(i0 + m * h)] = v[m];
+    }
+  }
+}
+
+template <bool FWD>
+__global__ void k2_rows_fft8(NfP P, const cplx* __restrict__ src, const double* __restrict__ deconv,
+                             cplx* __restrict__ dst, const cplx* __restrict__ tw) {
+  extern __shared__ cplx sm[];
+  const int L = P.log_nov, N = P.n_ov;
+  const int ls = fpad_len(N) + 1;
+  cplx* tws = sm + P.RW * ls;
+  const int j0 = blockIdx.x * P.RW, prob = blockIdx.y, nr = min(P.RW, P.n - j0);
+  const cplx* s = FWD ? src + (int64_t)prob * P.n * P.n : src + (int64_t)prob * N * N;
+  cplx* d = FWD ? dst + (int64_t)prob * N * N : dst + (int64_t)prob * P.n * P.n;
+  for (int i = threadIdx.x; i < N / 2; i += blockDim.x) tws[i] = tw[i];
+  __syncthreads();
+  for (int st = 1; st <= L;) {
+    const int nst = L - st + 1 >= 3 ? 3 : L - st + 1;
+    const bool first = st == 1, last = st + nst > L;
+    if (nst == 3) rows_pass<FWD, 3>(P, s, d, deconv, sm, tws, ls, j0, nr, st, first, last);
+    else if (nst == 2) rows_pass<FWD, 2>(P, s, d, deconv, sm, tws, ls, j0, nr, st, first, last);
+    else rows_pass<FWD, 1>(P, s, d, deconv, sm, tws, ls, j0, nr, st, first, last);
+    __syncthreads();
+    st += nst;
+  }
+}
