@@ -212,6 +212,7 @@ struct gs_op {
   bool fast2d = false;  // kernels_nfft2d_fast.cuh path (w = 6, p <= 4)
   int cap = 1;          // chunk capacity per problem (2D work list)
   DBuf<int> ch_tile, ch_s0, ch_s1, ch_count, tcs;
+  DBuf<uint4> ch_rows;  // per chunk: row starts (k2f_chunk_rows)
   DBuf<int> fs_start;  // per (problem, tile): range of fold sources (k2_fold_src)
   DBuf<int4> fsrc;
   DBuf<int2> cov;        // per grid coordinate: (tile, offset) of the regions covering it
@@ -680,6 +681,13 @@ gs_op* create(const gs_op_desc* dsc) {
       op->ch_s1.upload(h_1.data(), h_1.size(), st);
       op->ch_count.upload(h_n.data(), h_n.size(), st);
       op->tcs.upload(tcs.data(), tcs.size(), st);
+      if (op->fast2d) {
+        op->ch_rows.alloc((size_t)B * cap);
+        k2f_chunk_rows<<<nblk((int64_t)B * cap, 128), 128, 0, st>>>(op->ch_tile.p, op->ch_s0.p, op->ch_s1.p,
+                                                                   (int64_t)B * cap, cap, M, P.nt, op->base_y.p,
+                                                                   op->ch_rows.p);
+        CKL();
+      }
       if (op->fast2d) {  // fold sources per tile (k2_fold_src): same order as k2_fold_tiles' coverage loops
         std::vector<int> fst((size_t)B * (ntiles + 1));
         std::vector<int4> fs;
@@ -883,7 +891,7 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
 #define GS_F_INTERP(PP)                                                                                            \
   if (interp_mma())                                                                                                \
     k2f_interp_mma<PP><<<grid, 32 * F_IWARPS * F_IMSPLIT, FInterpM<PP>::bytes(), st>>>(                                       \
-        P, op->ch_tile.p, op->ch_s0.p, op->ch_s1.p, op->ch_count.p, op->cap, op->base_x.p, op->base_y.p,            \
+        P, op->ch_tile.p, op->ch_s0.p, op->ch_s1.p, op->ch_count.p, op->ch_rows.p, op->cap, op->base_x.p, op->base_y.p,            \
         op->wts_x.p, op->wts_y.p, op->rec_x.p, op->rec_y.p, op->G.p, op->lines.p, x, pp, y);                        \
   else                                                                                                             \
     k2f_interp<PP><<<grid, F_ITHREADS, FInterp<PP>::bytes(), st>>>(                                              \
@@ -953,7 +961,7 @@ void adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
 #define GS_F_SPREAD(PP)                                                                                          \
   if (spread_mma())                                                                                              \
     k2f_spread_mma<PP><<<grid, 32 * F_MWARPS, FSpreadM<PP>::bytes(), st>>>(                                     \
-        P, op->ch_tile.p, op->ch_s0.p, op->ch_s1.p, op->ch_count.p, op->cap, op->base_x.p, op->base_y.p,          \
+        P, op->ch_tile.p, op->ch_s0.p, op->ch_s1.p, op->ch_count.p, op->ch_rows.p, op->cap, op->base_x.p, op->base_y.p,          \
         op->wts_x.p, op->wts_y.p, op->rec_x.p, op->rec_y.p, y, pp, op->TB.p, op->TL.p, op->TC.p);                 \
   else                                                                                                           \
     k2f_spread<PP><<<grid, 32 * F_WARPS, FSpread<PP>::bytes(), st>>>(                                          \

@@ -134,6 +134,34 @@ __device__ __forceinline__ unsigned char* bulk_stage(unsigned char* dst, const v
   return dst + (a - al);
 }
 
+// Row starts of every chunk (built once per operator): byte r of ch_rows[chunk]
+// = first sample (relative to the chunk start) whose window row is >= tile
+// row r, r = 0..F_T (samples are sorted by cell, row-major, inside a tile).
+__global__ void k2f_chunk_rows(const int* __restrict__ ch_tile, const int* __restrict__ ch_s0,
+                               const int* __restrict__ ch_s1, int64_t nchunks, int cap, int64_t M, int nt,
+                               const int* __restrict__ base_y, uint4* __restrict__ ch_rows) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= nchunks) return;
+  const int prob = (int)(q / cap), a = ch_s0[q], n = ch_s1[q] - a;
+  const int ty0 = (ch_tile[q] / nt) * F_T;
+  const int* by = base_y + (int64_t)prob * M + a;
+  unsigned char r8[16] = {0};
+  for (int r = 0; r <= F_T; ++r) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (by[mid] < ty0 + r) lo = mid + 1;
+      else hi = mid;
+    }
+    r8[r] = (unsigned char)lo;
+  }
+  ch_rows[q] = *reinterpret_cast<const uint4*>(r8);
+}
+__device__ __forceinline__ int row_start(const uint4& rw, int r) {
+  const unsigned w = r < 4 ? rw.x : (r < 8 ? rw.y : (r < 12 ? rw.z : rw.w));
+  return (int)((w >> (8 * (r & 3))) & 0xffu);
+}
+
 // Debug-only CTA timeline (build with -DF_TIMELINE): per chunk, the SM id and
 // SM clock at entry, staging complete, compute complete (tools/timeline.py).
 #ifdef F_TIMELINE
@@ -765,7 +793,7 @@ struct FSpreadM {
 template <int P>
 __global__ void __launch_bounds__(32 * F_MWARPS, F_SBLOCKS)
 k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ ch_s0, const int* __restrict__ ch_s1,
-               const int* __restrict__ ch_count, int cap, const int* __restrict__ base_x,
+               const int* __restrict__ ch_count, const uint4* __restrict__ ch_rows, int cap, const int* __restrict__ base_x,
                const int* __restrict__ base_y, const double* __restrict__ wx_all, const double* __restrict__ wy_all,
                const cplx* __restrict__ recx_all, const cplx* __restrict__ recy_all, const cplx* __restrict__ yin,
                const int* __restrict__ in_perm, cplx* __restrict__ TB, cplx* __restrict__ TL, cplx* __restrict__ TC) {
@@ -779,6 +807,7 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   if (c >= ch_count[prob]) return;
   F_TLS(0);
   const int tile = ch_tile[prob * cap + c], s0 = ch_s0[prob * cap + c], s1 = ch_s1[prob * cap + c];
+  const uint4 rw = ch_rows[prob * cap + c];
   const int n = s1 - s0;
   const int ty = tile / Pp.nt, tx = tile - ty * Pp.nt;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
@@ -832,20 +861,9 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   bar_wait(&stage_bar, 0);
   F_TLS(1);
   const int ty0 = ty * T, tx0 = tx * T;
-  if (threadIdx.x <= T) {  // row starts (samples are sorted by cell, row-major, in a tile)
-    const int key = ty0 + threadIdx.x;
-    int lo = 0, hi = n;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (s_by[mid] < key) lo = mid + 1;
-      else hi = mid;
-    }
-    rs[threadIdx.x] = lo;
-  }
-  __syncthreads();
   const int band = warp % F_WARPS, half = warp / F_WARPS;  // band of rows, K-step parity
   const int band0 = band * BAND;
-  const int sa = rs[band0], sb = rs[band0 + BAND];
+  const int sa = row_start(rw, band0), sb = row_start(rw, band0 + BAND);  // precomputed band starts
   double rg[2][6][2], ly[2][2][2], lx[2][3][2], co[2][2][2];
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
@@ -1236,7 +1254,8 @@ __device__ __forceinline__ void f_interp_band(int band0, int half, int sa, int s
 template <int P>
 __global__ void __launch_bounds__(32 * F_IWARPS * F_IMSPLIT, F_IBLOCKS_M)
 k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ ch_s0, const int* __restrict__ ch_s1,
-               const int* __restrict__ ch_count, int cap, const int* __restrict__ base_x,
+               const int* __restrict__ ch_count, const uint4* __restrict__ ch_rows, int cap,
+               const int* __restrict__ base_x,
                const int* __restrict__ base_y, const double* __restrict__ wx_all, const double* __restrict__ wy_all,
                const cplx* __restrict__ recx_all, const cplx* __restrict__ recy_all, const cplx* __restrict__ G,
                const cplx* __restrict__ lines, const cplx* __restrict__ x, const int* __restrict__ out_perm,
@@ -1258,6 +1277,7 @@ k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   const int64_t chunk = (int64_t)prob * cap + c;
   F_TL(0);
   const int tile = ch_tile[chunk], s0 = ch_s0[chunk], s1 = ch_s1[chunk];
+  const uint4 rw = ch_rows[chunk];
   const int n = s1 - s0;
   const int ty = tile / Pp.nt, tx = tile - ty * Pp.nt;
   const int ty0 = ty * T, tx0 = tx * T;
@@ -1339,19 +1359,8 @@ k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   __syncthreads();  // barrier initialised, region / lines / corners landed
   bar_wait(&stage_bar, 0);
   F_TL(1);
-  if (threadIdx.x <= T) {  // row starts (samples are sorted by cell, row-major, in a tile)
-    const int key = ty0 + threadIdx.x;
-    int lo = 0, hi = n;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (s_by[mid] < key) lo = mid + 1;
-      else hi = mid;
-    }
-    rs[threadIdx.x] = lo;
-  }
-  __syncthreads();
   const int band0 = (warp % F_IWARPS) * BAND, half = warp / F_IWARPS;
-  const int sa = rs[band0], sb = rs[band0 + BAND];
+  const int sa = row_start(rw, band0), sb = row_start(rw, band0 + BAND);  // precomputed band starts
   f_interp_band<P, F_IMSPLIT>(band0, half, sa, sb, ty0, tx0, s_wx, s_wy, s_rx, s_ry, s_bx, s_by, gre, gim, lxre, lxim,
                               lys, cxs, (int64_t)prob * Pp.M, g0, s0, out_perm, y);
   F_TL_SYNC();
