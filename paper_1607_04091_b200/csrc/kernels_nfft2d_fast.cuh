@@ -762,6 +762,9 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 #define F_MUNROLL 2  // K steps per loop trip: the next step's fragments load under this step's DMMAs
 #endif
 
+#ifndef F_SA1V2
+#define F_SA1V2 0
+#endif
 #ifndef F_SREC_GLOBAL
 #define F_SREC_GLOBAL 0  // 1: factor records read from global (L2-prefetched), not staged in shared memory
 #endif
@@ -906,6 +909,19 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
     bool hit[3];
 #pragma unroll
     for (int nt = 0; nt < 3; ++nt) hit[nt] = __any_sync(0xffffffffu, b3[nt] != 0.0);
+#if F_SA1V2
+    // the sample's factor conj(Dx Dy) y scales the row operand (2 x 2 products) instead of each reached column tile
+    const double ar[2] = {a1[0] * v2.x, a1[1] * v2.x}, ai[2] = {a1[0] * v2.y, a1[1] * v2.y};
+#pragma unroll
+    for (int nt = 0; nt < 3; ++nt) {
+      if (!hit[nt]) continue;
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        dmma884(rg[mt][nt][0], rg[mt][nt][1], ar[mt], b3[nt]);
+        dmma884(rg[mt][nt + 3][0], rg[mt][nt + 3][1], ai[mt], b3[nt]);
+      }
+    }
+#else
 #pragma unroll
     for (int nt = 0; nt < 3; ++nt) {
       if (!hit[nt]) continue;
@@ -916,6 +932,7 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
         dmma884(rg[mt][nt + 3][0], rg[mt][nt + 3][1], a1[mt], bim);
       }
     }
+#endif
     if (E > 0) {
       const bool ge = g < E;
       const cplx Ax = rx[1 + (ge ? g : 0)], By = ry[1 + (ge ? g : 0)];
