@@ -326,3 +326,26 @@ print("ok", ef, ea)
     env = dict(os.environ, GS_B200_SPREAD="dfma", GS_B200_INTERP="dfma", PYTHONPATH=root)
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.startswith("ok"), r.stdout + r.stderr
+
+
+# ------------------------------------------------------------------ fast 2D tile path, every family it serves
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_fast2d_tile_path_families_dense_tiles(p):
+    """The DMMA tile kernels (n_ov >= 48: J = 5 -> n_ov 64) for haar .. db4,
+    on uniform points plus a dense cluster (tiles of > 144 samples: several
+    chunks per tile, band starts inside later chunks, the band-major sample
+    order), the public apply (caller order) and the CGLS session (sorted
+    order)."""
+    g = gs()
+    rng = np.random.default_rng(500 + p)
+    J = 5
+    n = 1 << J
+    spread_pts = rng.uniform(-0.49 * n, 0.49 * n, (700, 2))
+    cluster = rng.normal(0.0, 0.6, (500, 2)) + np.array([3.3, -5.1])
+    coords = np.concatenate([spread_pts, cluster]).reshape(-1)
+    ref, op = build_pair(2, p, J, coords)
+    assert op.route == "nfft_2d", op.route
+    check_factors(ref, op, 2)
+    check_apply(ref, op, rng)
+    b = rc(ref.rows, rng)
+    check_cgls(ref, op, b, 6)
