@@ -805,7 +805,6 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   constexpr int S = F_S, T = F_T, R = F_R, BAND = F_BAND, E = F::E, RR = F::RR, NCE = F::NCE, MU = F_MUNROLL;
   extern __shared__ __align__(16) unsigned char fsm_raw[];
   cplx* s_ys = reinterpret_cast<cplx*>(fsm_raw + FM::YS);
-  __shared__ int rs[T + 1];
   const int prob = blockIdx.y, c = blockIdx.x;
   if (c >= ch_count[prob]) return;
   F_TLS(0);
@@ -1287,7 +1286,6 @@ k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   double* lxim = reinterpret_cast<double*>(fim_raw + FI::LXIM);
   __shared__ __align__(16) cplx lys[EE][R];
   __shared__ __align__(16) cplx cxs[P >= 2 ? 4 * P * P : 1];
-  __shared__ int rs[T + 1];
   __shared__ __align__(8) uint64_t stage_bar;
   const int prob = blockIdx.y, c = blockIdx.x;
   if (c >= ch_count[prob]) return;
