@@ -750,6 +750,14 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
       : "+d"(c0), "+d"(c1)
       : "d"(a), "d"(b));
 }
+// m16n8k8: A 16 x 8 (a0 = (g, t), a1 = (g + 8, t), a2 = (g, t + 4), a3 = (g + 8, t + 4)),
+// B 8 x 8 (b0 = (t, g), b1 = (t + 4, g)), C rows g (c0, c1) and g + 8 (c2, c3), columns 2t, 2t + 1
+__device__ __forceinline__ void dmma1688(double& c0, double& c1, double& c2, double& c3, const double* a,
+                                         const double* b) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+d"(c0), "+d"(c1), "+d"(c2), "+d"(c3)
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+}
 
 // CTA of the DMMA spreading kernel: F_MSPLIT warps per band of F_BAND sample
 // rows (they take alternate K steps of the band's samples), so 2 CTAs/SM hold
@@ -1053,6 +1061,9 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
 #ifndef F_IMUNROLL
 #define F_IMUNROLL 8  // sample tiles per loop trip: a whole band in one trip (DMMAs of one tile overlap the epilogue of another)
 #endif
+#ifndef F_IMMA168
+#define F_IMMA168 0  // 1: m16n8k8 DMMAs in the interpolation
+#endif
 #ifndef F_ICONST_RELOAD
 #define F_ICONST_RELOAD 0
 #endif
@@ -1180,6 +1191,45 @@ __device__ __forceinline__ void f_interp_band(int band0, int half, int sa, int s
     for (int mt = 0; mt < 6; ++mt) h[mt][0] = h[mt][1] = 0.0;
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) uy[mt][0] = uy[mt][1] = cbo[mt][0] = cbo[mt][1] = 0.0;
+#if F_IMMA168
+    // m16n8k8 form: one instruction per 16 rows x 8 columns x 8 samples
+    // (A = [re rows 0..15] or [im rows 0..15] or [LX_re; LX_im], K = 8 columns)
+    bool hk8[3];
+#pragma unroll
+    for (int kb = 0; kb < 3; ++kb) hk8[kb] = __any_sync(0xffffffffu, wb[2 * kb] != 0.0 || wb[2 * kb + 1] != 0.0);
+#pragma unroll
+    for (int kb = 0; kb < 3; ++kb) {
+      if (!hk8[kb]) continue;
+      const int col = kb * 8 + t;
+      const int r0 = band0 + g, r1 = band0 + 8 + g;
+      const double bb[2] = {wb[2 * kb], wb[2 * kb + 1]};
+      {
+        const double a[4] = {r0 < R ? gre[r0 * F_GS + col] : 0.0, r1 < R ? gre[r1 * F_GS + col] : 0.0,
+                             r0 < R ? gre[r0 * F_GS + col + 4] : 0.0, r1 < R ? gre[r1 * F_GS + col + 4] : 0.0};
+        dmma1688(h[0][0], h[0][1], h[1][0], h[1][1], a, bb);
+      }
+      {
+        const double a[4] = {r0 < R ? gim[r0 * F_GS + col] : 0.0, r1 < R ? gim[r1 * F_GS + col] : 0.0,
+                             r0 < R ? gim[r0 * F_GS + col + 4] : 0.0, r1 < R ? gim[r1 * F_GS + col + 4] : 0.0};
+        dmma1688(h[2][0], h[2][1], h[3][0], h[3][1], a, bb);
+      }
+      if (E > 0) {
+        const double a[4] = {lxre[g * F_GS + col], lxim[g * F_GS + col], lxre[g * F_GS + col + 4],
+                             lxim[g * F_GS + col + 4]};
+        dmma1688(h[4][0], h[4][1], h[5][0], h[5][1], a, bb);
+      }
+    }
+    if (E > 0) {
+#pragma unroll
+      for (int kb = 0; kb < 2; ++kb) {
+        const double bu[2] = {yb[2 * kb], yb[2 * kb + 1]}, bc[2] = {cb[2 * kb], cb[2 * kb + 1]};
+        const double au[4] = {lyA[0][2 * kb], lyA[1][2 * kb], lyA[0][2 * kb + 1], lyA[1][2 * kb + 1]};
+        const double ac[4] = {crA[0][2 * kb], crA[1][2 * kb], crA[0][2 * kb + 1], crA[1][2 * kb + 1]};
+        dmma1688(uy[0][0], uy[0][1], uy[1][0], uy[1][1], au, bu);
+        dmma1688(cbo[0][0], cbo[0][1], cbo[1][0], cbo[1][1], ac, bc);
+      }
+    }
+#else
     // column blocks no sample of the tile reaches are all-zero: skip them (warp-uniform vote)
     bool hk[6];
 #pragma unroll
@@ -1217,6 +1267,7 @@ __device__ __forceinline__ void f_interp_band(int band0, int half, int sa, int s
           }
         }
     }
+#endif
     // epilogue: lane (g, t) holds row g of every product for samples n0 + 2t + j
     // part = Dx (Dy rp + b_g hx_g) + a_g (Dy uy_g + (C b)_g), then the sum over g
     cplx pj[2];
