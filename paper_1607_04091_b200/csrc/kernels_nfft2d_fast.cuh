@@ -915,7 +915,8 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
     // column tiles the step's 4 samples do not reach are all-zero: skip them (warp-uniform vote)
     bool hit[3];
 #pragma unroll
-    for (int nt = 0; nt < 3; ++nt) hit[nt] = __any_sync(0xffffffffu, b3[nt] != 0.0);
+    for (int nt = 0; nt < 3; ++nt)  // integer window test (KB taps inside the window are >= 1): no FP64 compare
+      hit[nt] = __any_sync(0xffffffffu, (unsigned)(nt * 8 + g - ox) < (unsigned)S);
 #if F_SA1V2
     // the sample's factor conj(Dx Dy) y scales the row operand (2 x 2 products) instead of each reached column tile
     const double ar[2] = {a1[0] * v2.x, a1[1] * v2.x}, ai[2] = {a1[0] * v2.y, a1[1] * v2.y};
@@ -1233,7 +1234,8 @@ __device__ __forceinline__ void f_interp_band(int band0, int half, int sa, int s
     // column blocks no sample of the tile reaches are all-zero: skip them (warp-uniform vote)
     bool hk[6];
 #pragma unroll
-    for (int ks = 0; ks < 6; ++ks) hk[ks] = __any_sync(0xffffffffu, wb[ks] != 0.0);
+    for (int ks = 0; ks < 6; ++ks)  // integer window test (KB taps inside the window are >= 1): no FP64 compare
+      hk[ks] = __any_sync(0xffffffffu, (unsigned)(ks * 4 + t - oxg) < (unsigned)S);
 #pragma unroll
     for (int ks = 0; ks < 6; ++ks) {
       if (!hk[ks]) continue;
