@@ -143,6 +143,27 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
+def algorithmic_flops(kernel, p, M, S=13):
+    """FP64 flops of one 2D gridding launch per problem: 4 real
+    flops per (complex value x real weight) tap over the S x S region and the
+    4p side lines of S taps, plus the p x p corner blocks (32 p^2 per sample)."""
+    base = kernel.split("[")[0]
+    if base not in ("k2f_interp", "k2f_spread", "k2_interp", "k2_spread"):
+        return None
+    return 4 * (S * S + (4 * p * S if p >= 2 else 0)) * M + (32 * p * p * M if p >= 2 else 0)
+
+
+def load_fp64_peak():
+    """FP64 tensor-pipe peak measured on this GPU model (tools/micro/fp64_mix_probe.cu,
+    DMMA alone; profiles/fp64_peak.json), else the B200 datasheet FP64 figure."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
+            d = json.load(f)
+        return float(d["dmma_tflops"]), "measured: " + d.get("source", "profiles/fp64_peak.json")
+    except Exception:
+        return 37.0, "fallback: B200 datasheet FP64"
+
+
 def load_traffic(kernel, workload):
     """dram bytes per launch per problem from the committed ncu capture, if any."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
@@ -324,6 +345,18 @@ def run_gpu(args):
                     "frac": round(ach / peak, 4), "traffic": (tr * B if tr is not None else None),
                     "algorithmic_bytes_per_launch": ab, "launch_ms": round(prof[dom], 4),
                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"}
+    # FP64 co-limit of the 2D gridding kernels (they issue DMMAs): algorithmic
+    # flops per launch / the same live launch time, against the FP64 pipe peak
+    fpeak, fpeak_src = load_fp64_peak()
+    roofline_fp64 = {}
+    for k in prof:
+        fl = algorithmic_flops(k, p, M) if dim == 2 else None
+        if fl is None or prof[k] <= 0:
+            continue
+        tf = fl * B / (prof[k] / 1e3) / 1e12
+        roofline_fp64[k] = {"bound": "fp64", "achieved": round(tf, 3), "peak": fpeak, "unit": "TFLOP/s",
+                            "frac": round(tf / fpeak, 4), "flops_per_launch": fl * B, "launch_ms": round(prof[k], 4),
+                            "peak_source": fpeak_src}
     pair_b, it_b = iteration_bytes(dim, p, M, Nc, uaxis)
     it_gbs = it_b * P / (ms_per_step / 1e3) / 1e9
     roof_iter = {"bytes_per_problem_iteration": it_b, "achieved_gbs": round(it_gbs, 2),
@@ -368,6 +401,7 @@ def run_gpu(args):
             "pairs_per_sec": round(pairs_per_sec, 3), "ms_per_pair": round(pair_ms, 4),
             "gpu_launches": int(launches),
             "roofline": roofline, "roofline_iteration": roof_iter,
+            "roofline_fp64": roofline_fp64 or None,
             "kernel_ms_per_pair": {k: round(v, 4) for k, v in prof.items()},
             "e2e": {"value": round(e2e_value, 3), "unit": "problem-iterations/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "h2d_bytes_per_call": h2d_call, "d2h_bytes_per_call": d2h_call,

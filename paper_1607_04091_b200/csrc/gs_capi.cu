@@ -22,6 +22,7 @@
 #include "kernels_nfft2d_fast.cuh"
 #include "kernels_uniform.cuh"
 #include "kernels_vec.cuh"
+#include "kernels_cgls_fused.cuh"
 
 namespace {
 
@@ -224,6 +225,7 @@ struct gs_op {
   DBuf<double> sqrtw;  // internal order ([B][M]) or empty
   // workspace
   DBuf<cplx> G, lines, TB, TL, TLF, TC, TCF, W;
+  DBuf<cplx> EP;  // 1D route: per-CTA edge-sum partials of k_n1_spread
   DBuf<cplx> stage_a, stage_b;
   gs_cgls_session* solve_cache = nullptr;  // workspace of the last gs_solve_least_squares
   std::mutex mu;
@@ -252,6 +254,7 @@ void set_smem_attrs() {
   if (done) return;
   allow_big_smem(k_uni_fwd);
   allow_big_smem(k_uni_adj);
+  allow_big_smem(k_uni_cgls_iter);
   allow_big_smem(k_n1_embed_fft);
   allow_big_smem(k_n1_ifft_crop);
   allow_big_smem(k2_rows_embed_fft);
@@ -397,7 +400,11 @@ void attach_phases(UniP& P, DBuf<cplx>& buf, cudaStream_t st) {
   P.ph_in = buf.p;
   P.ph_out = buf.p + P.n;
 }
+// single-CTA 1D FFT kernels: padded line + staged twiddles
+size_t n1_fft_smem(const NfP& P) { return (size_t)(fpad_len(P.n_ov) + P.n_ov / 2) * sizeof(cplx); }
 size_t uni_smem(const UniP& P) { return (size_t)(P.logN2 >= 0 ? fpad_len(P.N2) : 2 * P.N2) * sizeof(cplx); }
+// k_uni_* and the fused CGLS iteration: FFT buffer + the staged twiddle table
+size_t uni_smem_tw(const UniP& P) { return uni_smem(P) + (P.logN2 >= 0 ? (size_t)(P.N2 / 2) * sizeof(cplx) : 0); }
 
 bool interp_mma();  // kernel variant selectors (defined with the launch code)
 bool cols_fft8();
@@ -758,6 +765,7 @@ gs_op* create(const gs_op_desc* dsc) {
       }
     } else {
       op->G.alloc((size_t)B * n_ov);
+      if (op->edges) op->EP.alloc((size_t)B * ((n_ov + N1_SPREAD_CELLS - 1) / N1_SPREAD_CELLS) * 2 * op->p);
     }
     CKL();
     CK(cudaStreamSynchronize(st));
@@ -834,7 +842,7 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
   switch (op->route) {
     case GS_ROUTE_UNIFORM_1D: {
       const UniP& P = op->up;
-      k_uni_fwd<<<dim3(1, B), 256, uni_smem(P), st>>>(P, x, Strided{op->n, 0, 1}, op->rec_u.p, op->M * op->Rr, y,
+      k_uni_fwd<<<dim3(1, B), 256, uni_smem_tw(P), st>>>(P, x, Strided{op->n, 0, 1}, op->rec_u.p, op->M * op->Rr, y,
                                                      Strided{op->M, 0, 1}, nullptr, 0, op->tw.p, op->logLmax);
       pmark("k_uni_fwd", st);
       break;
@@ -842,12 +850,12 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
     case GS_ROUTE_TENSOR_2D: {
       const int64_t n = op->n, Ma = op->Ma, Mb = op->Mb;
       // W(a, j) = sum_i ax_a(i) X(i, j): one vector per column j
-      k_uni_fwd<<<dim3((unsigned)n, B), 256, uni_smem(op->upx), st>>>(
+      k_uni_fwd<<<dim3((unsigned)n, B), 256, uni_smem_tw(op->upx), st>>>(
           op->upx, x, Strided{n * n, n, 1}, op->rec_ax.p, Ma * op->Rr, op->W.p, Strided{Ma * n, 1, n}, nullptr, 0,
           op->tw.p, op->logLmax);
       pmark("k_uni_fwd[x-pass]", st);
       // Y(a, b) = sum_j ay_b(j) W(a, j): one vector per row a
-      k_uni_fwd<<<dim3((unsigned)Ma, B), 256, uni_smem(op->upy), st>>>(
+      k_uni_fwd<<<dim3((unsigned)Ma, B), 256, uni_smem_tw(op->upy), st>>>(
           op->upy, op->W.p, Strided{Ma * n, n, 1}, op->rec_ay.p, Mb * op->Rr, y, Strided{op->M, Mb, 1},
           op->weighted ? op->sqrtw.p : nullptr, op->M, op->tw.p, op->logLmax);
       pmark("k_uni_fwd[y-pass]", st);
@@ -855,7 +863,7 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
     }
     case GS_ROUTE_NFFT_1D: {
       const NfP& P = op->np;
-      k_n1_embed_fft<<<B, 256, fpad_len(P.n_ov) * sizeof(cplx), st>>>(P, x, op->deconv.p, op->G.p, op->tw.p, op->logLmax);
+      k_n1_embed_fft<<<B, 256, n1_fft_smem(P), st>>>(P, x, op->deconv.p, op->G.p, op->tw.p, op->logLmax);
       pmark("k_n1_embed_fft", st);
       k_n1_interp<<<dim3(nblk(op->M, 128), B), 128, 0, st>>>(P, op->base_x.p, op->wts_x.p, op->rec_x.p, op->G.p, x,
                                                               perm_io ? op->perm.p : nullptr, y);
@@ -918,12 +926,23 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
   CKL();
 }
 
-void adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t st) {
+// CGLS s-step (k_cg_sstep's arguments) a route may fuse into its last adjoint kernel
+struct SStep {
+  CgState* st;
+  cplx* p;
+  double tol;
+  double* hist;
+  int hist_stride;
+};
+
+// returns true when the route ran the s-step `ss` itself (NFFT_1D: in k_n1_ifft_crop)
+bool adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t st, const SStep* ss = nullptr) {
+  bool fused_sstep = false;
   const int B = op->B;
   switch (op->route) {
     case GS_ROUTE_UNIFORM_1D: {
       const UniP& P = op->up;
-      k_uni_adj<<<dim3(1, B), 256, uni_smem(P), st>>>(P, y, Strided{op->M, 0, 1}, nullptr, 0, op->rec_u.p,
+      k_uni_adj<<<dim3(1, B), 256, uni_smem_tw(P), st>>>(P, y, Strided{op->M, 0, 1}, nullptr, 0, op->rec_u.p,
                                                      op->M * op->Rr, z, Strided{op->n, 0, 1}, op->tw.p, op->logLmax);
       pmark("k_uni_adj", st);
       break;
@@ -931,12 +950,12 @@ void adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
     case GS_ROUTE_TENSOR_2D: {
       const int64_t n = op->n, Ma = op->Ma, Mb = op->Mb;
       // V(a, j) = sum_b conj(ay_b(j)) (sqrt(mu) y)(a, b): one vector per row a
-      k_uni_adj<<<dim3((unsigned)Ma, B), 256, uni_smem(op->upy), st>>>(
+      k_uni_adj<<<dim3((unsigned)Ma, B), 256, uni_smem_tw(op->upy), st>>>(
           op->upy, y, Strided{op->M, Mb, 1}, op->weighted ? op->sqrtw.p : nullptr, op->M, op->rec_ay.p, Mb * op->Rr,
           op->W.p, Strided{Ma * n, n, 1}, op->tw.p, op->logLmax);
       pmark("k_uni_adj[y-pass]", st);
       // X(i, j) = sum_a conj(ax_a(i)) V(a, j): one vector per column j
-      k_uni_adj<<<dim3((unsigned)n, B), 256, uni_smem(op->upx), st>>>(
+      k_uni_adj<<<dim3((unsigned)n, B), 256, uni_smem_tw(op->upx), st>>>(
           op->upx, op->W.p, Strided{Ma * n, 1, n}, nullptr, 0, op->rec_ax.p, Ma * op->Rr, z, Strided{n * n, n, 1},
           op->tw.p, op->logLmax);
       pmark("k_uni_adj[x-pass]", st);
@@ -944,11 +963,15 @@ void adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
     }
     case GS_ROUTE_NFFT_1D: {
       const NfP& P = op->np;
-      k_n1_spread<<<dim3(nblk(P.n_ov, 128), B), 128, 0, st>>>(P, op->bins.p, op->wts_x.p, op->rec_x.p, y,
-                                                               perm_io ? op->perm.p : nullptr, op->G.p);
+      const int nparts = (P.n_ov + N1_SPREAD_CELLS - 1) / N1_SPREAD_CELLS;
+      k_n1_spread<<<dim3(nparts, B), N1_SPREAD_THREADS, 0, st>>>(P, op->bins.p, op->wts_x.p, op->rec_x.p, y,
+                                                                perm_io ? op->perm.p : nullptr, op->G.p, op->EP.p);
       pmark("k_n1_spread", st);
-      k_n1_ifft_crop<<<B, 256, fpad_len(P.n_ov) * sizeof(cplx), st>>>(P, op->G.p, op->deconv.p, op->rec_x.p, y,
-                                                            perm_io ? op->perm.p : nullptr, z, op->tw.p, op->logLmax);
+      k_n1_ifft_crop<<<B, 256, n1_fft_smem(P), st>>>(P, op->G.p, op->deconv.p, op->EP.p, nparts, z, op->tw.p,
+                                                      op->logLmax, ss ? ss->st : nullptr, ss ? ss->p : nullptr,
+                                                      ss ? ss->tol : 0.0, ss ? ss->hist : nullptr,
+                                                      ss ? ss->hist_stride : 0);
+      fused_sstep = ss != nullptr;
       pmark("k_n1_ifft_crop", st);
       break;
     }
@@ -1021,6 +1044,7 @@ void adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
     }
   }
   CKL();
+  return fused_sstep;
 }
 
 bool is_device_ptr(const void* p) {
@@ -1144,9 +1168,39 @@ void session_begin(Session& S, gs_op* op, const cplx* b_raw, bool b_perm, const 
 }
 
 // one CGLS iteration for every still-active problem (solver.cpp:70-88)
+bool cg_fused_enabled() {  // GS_B200_CG_FUSED=0: the generic multi-kernel iteration (A/B)
+  static const bool on = [] {
+    const char* e = std::getenv("GS_B200_CG_FUSED");
+    return !(e && *e == '0');
+  }();
+  return on;
+}
+
 void session_iterate_body(Session& S, cudaStream_t st) {
   gs_op* op = S.op;
   const int64_t TM = S.M * S.B, TN = S.Nc * S.B;
+  if (op->route == GS_ROUTE_UNIFORM_1D && cg_fused_enabled()) {  // whole iteration in one launch
+    const UniP& P = op->up;
+    k_uni_cgls_iter<<<S.B, UNI_CG_THREADS, uni_smem_tw(P), st>>>(P, op->rec_u.p, op->M * op->Rr, S.x.p, S.p.p,
+                                                                 S.s.p, S.r.p, S.q.p, S.st.p, S.tol, S.hist.p,
+                                                                 S.hist_cap, op->tw.p, op->logLmax, 1);
+    pmark("k_uni_cgls_iter", st);
+    CKL();
+    return;
+  }
+  if (S.chunks_M == 1 && S.chunks_N == 1 && cg_fused_enabled()) {
+    // one CTA reduces each problem's vectors: the scalar / vector phases in 2 launches
+    forward_dev(op, S.p.p, S.q.p, false, st);                                                  // q = T p
+    k_cg_qstep<<<S.B, CG_STEP_THREADS, 0, st>>>(S.st.p, S.q.p, S.r.p, S.x.p, S.p.p, S.M, S.Nc);  // qq, alpha, x, r
+    pmark("k_cg_qstep", st);
+    const SStep ss{S.st.p, S.p.p, S.tol, S.hist.p, S.hist_cap};
+    if (!adjoint_dev(op, S.r.p, S.s.p, false, st, &ss)) {                                      // s = T* r
+      k_cg_sstep<<<S.B, CG_STEP_THREADS, 0, st>>>(S.st.p, S.s.p, S.p.p, S.Nc, S.tol, S.hist.p, S.hist_cap);
+      pmark("k_cg_sstep", st);                                                                 // gamma', beta, p
+    }
+    CKL();
+    return;
+  }
   forward_dev(op, S.p.p, S.q.p, false, st);                          // q = T p
   norm2(S, S.q.p, S.M, S.chunks_M, st);                              // qq
   k_cg_alpha<<<nblk(S.B, 128), 128, 0, st>>>(S.st.p, S.n2.p, S.B);  // alpha (or stop)
@@ -1176,6 +1230,16 @@ bool graphs_enabled() {
 void session_iterate(Session& S, cudaStream_t st, int k) {
   if (k <= 0) return;
   S.it += k;
+  if (S.op->route == GS_ROUTE_UNIFORM_1D && cg_fused_enabled() && !g_prof.on) {
+    // all k iterations in one launch (k_uni_cgls_iter loops on the device)
+    const UniP& P = S.op->up;
+    k_uni_cgls_iter<<<S.B, UNI_CG_THREADS, uni_smem_tw(P), st>>>(P, S.op->rec_u.p, S.op->M * S.op->Rr, S.x.p, S.p.p,
+                                                                 S.s.p, S.r.p, S.q.p, S.st.p, S.tol, S.hist.p,
+                                                                 S.hist_cap, S.op->tw.p, S.op->logLmax, k);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    CKL();
+    return;
+  }
   if (!graphs_enabled() || g_prof.on) {
     for (int i = 0; i < k; ++i) session_iterate_body(S, st);
     return;

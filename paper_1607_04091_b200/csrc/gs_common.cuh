@@ -74,7 +74,9 @@ __device__ __forceinline__ void block_fft_bitrev(cplx* buf, int logL, int count,
 __host__ __device__ __forceinline__ int fpad(int i) { return i + (i >> 3); }
 __host__ __device__ __forceinline__ int fpad_len(int L) { return L + (L >> 3); }
 
-template <int NST>
+// TWS: tw points to shared memory (staged table; a generic load, since
+// ld.global.nc on a shared address faults) instead of the global table
+template <int NST, bool TWS = false>
 __device__ __forceinline__ void fft_fused_pass(cplx* buf, int logL, int s, int count, int lstride,
                                                const cplx* __restrict__ tw, int logLmax, int sign) {
   constexpr int G = 1 << NST;
@@ -96,7 +98,7 @@ __device__ __forceinline__ void fft_fused_pass(cplx* buf, int logL, int s, int c
       for (int m = 0; m < G; ++m) {
         if ((m >> q) & 1) continue;
         const int k = jh + (m & ((1 << q) - 1)) * h;
-        cplx w = ldg2(tw + (k << twshift));
+        cplx w = TWS ? tw[k << twshift] : ldg2(tw + (k << twshift));
         if (sign > 0) w.y = -w.y;
         const cplx u = v[m], x = cmul(v[m + (1 << q)], w);
         v[m] = cadd(u, x);
@@ -108,17 +110,25 @@ __device__ __forceinline__ void fft_fused_pass(cplx* buf, int logL, int s, int c
   }
 }
 
+template <bool TWS = false>
 __device__ __forceinline__ void block_fft_padded(cplx* buf, int logL, int count, int lstride,
                                                  const cplx* __restrict__ tw, int logLmax, int sign) {
   int s = 1;
   while (s <= logL) {
     const int nst = logL - s + 1 >= 3 ? 3 : logL - s + 1;
-    if (nst == 3) fft_fused_pass<3>(buf, logL, s, count, lstride, tw, logLmax, sign);
-    else if (nst == 2) fft_fused_pass<2>(buf, logL, s, count, lstride, tw, logLmax, sign);
-    else fft_fused_pass<1>(buf, logL, s, count, lstride, tw, logLmax, sign);
+    if (nst == 3) fft_fused_pass<3, TWS>(buf, logL, s, count, lstride, tw, logLmax, sign);
+    else if (nst == 2) fft_fused_pass<2, TWS>(buf, logL, s, count, lstride, tw, logLmax, sign);
+    else fft_fused_pass<1, TWS>(buf, logL, s, count, lstride, tw, logLmax, sign);
     __syncthreads();
     s += nst;
   }
+}
+
+// compact twiddle table of one FFT length 2^logL (entries k < 2^logL / 2) out of
+// the 2^logLmax device table, for block_fft_padded(..., tws, logL, ...) from
+// shared memory (caller synchronises before use)
+__device__ __forceinline__ void stage_twiddles(cplx* tws, const cplx* __restrict__ tw, int logL, int logLmax) {
+  for (int k = threadIdx.x; k < (1 << logL) / 2; k += blockDim.x) tws[k] = ldg2(tw + ((int64_t)k << (logLmax - logL)));
 }
 
 __device__ __forceinline__ int bitrev(int i, int logL) { return (int)(__brev((unsigned)i) >> (32 - logL)); }

@@ -13,6 +13,7 @@
 //          tile regions that cover each cell while loading.
 #pragma once
 #include "gs_common.cuh"
+#include "kernels_vec.cuh"
 
 struct NfP {
   int n;        // modes per axis (2^J)
@@ -35,7 +36,9 @@ __global__ void k_n1_embed_fft(NfP P, const cplx* __restrict__ x, const double* 
   const int prob = blockIdx.x;
   x += (int64_t)prob * P.n;
   G += (int64_t)prob * P.n_ov;
+  cplx* tws = sm + fpad_len(P.n_ov);  // twiddles staged in shared memory (dynamic smem: + n_ov / 2)
   for (int i = threadIdx.x; i < fpad_len(P.n_ov); i += blockDim.x) sm[i] = mk(0, 0);
+  stage_twiddles(tws, tw, P.log_nov, logLmax);
   __syncthreads();
   for (int idx = threadIdx.x; idx < P.n; idx += blockDim.x) {
     int k = idx - P.n / 2;
@@ -45,7 +48,7 @@ __global__ void k_n1_embed_fft(NfP P, const cplx* __restrict__ x, const double* 
     sm[fpad(bitrev(pos, P.log_nov))] = cscale(v, deconv[idx]);
   }
   __syncthreads();
-  block_fft_padded(sm, P.log_nov, 1, 0, tw, logLmax, -1);
+  block_fft_padded<true>(sm, P.log_nov, 1, 0, tws, P.log_nov, -1);
   for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) G[i] = sm[fpad(i)];
 }
 
@@ -77,71 +80,112 @@ __global__ void k_n1_interp(NfP P, const int* __restrict__ base, const double* _
 }
 
 // spreading, owner-computes: cell j sums w_s[t] conj(D_s) y_s over the points
-// whose window base is (j - t) mod n_ov  (transpose of nufft.cpp:313-322)
-__global__ void k_n1_spread(NfP P, const int* __restrict__ cell_start, const double* __restrict__ wts,
-                            const cplx* __restrict__ rec, const cplx* __restrict__ yin, const int* __restrict__ in_perm,
-                            cplx* __restrict__ line) {
+// whose window base is (j - t) mod n_ov  (transpose of nufft.cpp:313-322).
+// 16 lanes per cell, lane t < S takes tap t (S <= 15), so a thread walks the
+// ~M/n_ov samples of one cell instead of S cells; the lanes' sums are folded
+// by shuffles in a fixed order.  Lane 0 (tap 0) visits every sample of its
+// own cell, i.e. every sample exactly once over the grid: it also
+// accumulates the edge sums L^H y, R^H y (freq2wave.cpp:323-324), reduced per
+// CTA into edge_part[prob][blockIdx.x][2p] (summed by k_n1_ifft_crop).
+constexpr int N1_SPREAD_THREADS = 128;
+constexpr int N1_SPREAD_CELLS = N1_SPREAD_THREADS / 16;
+__global__ void __launch_bounds__(N1_SPREAD_THREADS)
+k_n1_spread(NfP P, const int* __restrict__ cell_start, const double* __restrict__ wts,
+            const cplx* __restrict__ rec, const cplx* __restrict__ yin, const int* __restrict__ in_perm,
+            cplx* __restrict__ line, cplx* __restrict__ edge_part) {
+  __shared__ cplx esm[N1_SPREAD_THREADS / 32][16];
   const int prob = blockIdx.y;
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= P.n_ov) return;
+  const int lane16 = threadIdx.x & 15;
+  const int j = blockIdx.x * N1_SPREAD_CELLS + (threadIdx.x >> 4);  // n_ov is a multiple of the cells per CTA
   const int Rr = 1 + (P.edges ? 2 * P.p : 0);
   const int* cs = cell_start + (int64_t)prob * (P.n_ov + 1);
   const cplx* yp = yin + (int64_t)prob * P.M;
   cplx acc = mk(0, 0);
-  for (int t = 0; t < P.S; ++t) {
+  cplx e[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) e[c] = mk(0, 0);
+  if (lane16 < P.S) {
+    const int t = lane16;
     const int cell = (j - t + P.n_ov) & (P.n_ov - 1);
-    for (int s = cs[cell]; s < cs[cell + 1]; ++s) {
+    const int s1 = cs[cell + 1];
+    for (int s = cs[cell]; s < s1; ++s) {
       const int64_t gs = prob * P.M + s;
       const cplx yv = ldg2(yp + (in_perm ? (int64_t)in_perm[gs] : s));
-      const cplx v = cmul(conj_(ldg2(rec + gs * Rr)), yv);
+      const cplx* r = rec + gs * Rr;
+      const cplx v = cmul(conj_(ldg2(r)), yv);
       acc = caxpy(acc, __ldg(wts + gs * P.S + t), v);
+      if (P.edges && t == 0) {
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          if (c < 2 * P.p) e[c] = cadd(e[c], cmul(conj_(ldg2(r + 1 + c)), yv));
+      }
     }
   }
-  line[(int64_t)prob * P.n_ov + j] = acc;
+  // fold the 16 taps of the cell: lane t += lane t + 8, + 4, + 2, + 1
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) {
+    acc.x += __shfl_down_sync(0xffffffffu, acc.x, o, 16);
+    acc.y += __shfl_down_sync(0xffffffffu, acc.y, o, 16);
+  }
+  if (lane16 == 0) line[(int64_t)prob * P.n_ov + j] = acc;
+  if (!P.edges) return;
+  // edge sums: lanes 0 and 16 of each warp hold them; fold the pair, then the warps
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    if (c >= 2 * P.p) break;
+    e[c].x += __shfl_down_sync(0xffffffffu, e[c].x, 16);
+    e[c].y += __shfl_down_sync(0xffffffffu, e[c].y, 16);
+    if (lane == 0) esm[warp][c] = e[c];
+  }
+  __syncthreads();
+  if (threadIdx.x < 2 * P.p) {
+    cplx sum = esm[0][threadIdx.x];
+    for (int w = 1; w < N1_SPREAD_THREADS / 32; ++w) sum = cadd(sum, esm[w][threadIdx.x]);
+    edge_part[((int64_t)prob * gridDim.x + blockIdx.x) * (2 * P.p) + threadIdx.x] = sum;
+  }
 }
 
 // FFT_{+}, crop, deconvolve (nufft.cpp:340-350); edge slots <- L^H y, R^H y
-// (freq2wave.cpp:317-325)
+// (freq2wave.cpp:317-325) from the nparts per-CTA partials of k_n1_spread,
+// one warp per edge column summing them in a fixed order.  Inside CGLS
+// (cst != nullptr) the CTA that owns the problem's s also runs the s-step
+// (gamma', history, beta, p = s + beta p: k_cg_beta + k_pupdate).
 __global__ void k_n1_ifft_crop(NfP P, const cplx* __restrict__ line, const double* __restrict__ deconv,
-                               const cplx* __restrict__ rec, const cplx* __restrict__ yin,
-                               const int* __restrict__ in_perm, cplx* __restrict__ z, const cplx* __restrict__ tw,
-                               int logLmax) {
+                               const cplx* __restrict__ edge_part, int nparts, cplx* __restrict__ z,
+                               const cplx* __restrict__ tw, int logLmax, CgState* cst, cplx* __restrict__ pvec,
+                               double tol, double* hist, int hist_stride) {
   extern __shared__ cplx sm[];
   __shared__ double red[32];
   const int prob = blockIdx.x;
   line += (int64_t)prob * P.n_ov;
   z += (int64_t)prob * P.n;
+  cplx* tws = sm + fpad_len(P.n_ov);  // dynamic smem: + n_ov / 2 twiddles
   for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) sm[fpad(bitrev(i, P.log_nov))] = line[i];
+  stage_twiddles(tws, tw, P.log_nov, logLmax);
   __syncthreads();
-  block_fft_padded(sm, P.log_nov, 1, 0, tw, logLmax, +1);
+  block_fft_padded<true>(sm, P.log_nov, 1, 0, tws, P.log_nov, +1);
   for (int idx = threadIdx.x; idx < P.n; idx += blockDim.x) {
     int k = idx - P.n / 2;
-    cplx v = cscale(sm[fpad((k + P.n_ov) & (P.n_ov - 1))], deconv[idx]);
-    if (P.edges && (idx < P.p || idx >= P.n - P.p)) v = mk(0, 0);
-    z[idx] = v;
+    if (P.edges && (idx < P.p || idx >= P.n - P.p)) continue;  // edge slots: written below
+    z[idx] = cscale(sm[fpad((k + P.n_ov) & (P.n_ov - 1))], deconv[idx]);
   }
-  if (!P.edges) return;
-  const int Rr = 1 + 2 * P.p;
-  cplx eh[8], et[8];
-  for (int c = 0; c < 8; ++c) eh[c] = et[c] = mk(0, 0);
-  for (int64_t s = threadIdx.x; s < P.M; s += blockDim.x) {
-    const int64_t gs = prob * P.M + s;
-    const cplx u = yin[prob * P.M + (in_perm ? (int64_t)in_perm[gs] : s)];
-    const cplx* r = rec + gs * Rr;
-    for (int c = 0; c < P.p; ++c) {
-      eh[c] = cadd(eh[c], cmul(conj_(r[1 + c]), u));
-      et[c] = cadd(et[c], cmul(conj_(r[1 + P.p + c]), u));
+  if (P.edges) {
+    const int lane = threadIdx.x & 31, E = 2 * P.p;
+    const cplx* ep = edge_part + (int64_t)prob * nparts * E;
+    for (int c = threadIdx.x >> 5; c < E; c += blockDim.x >> 5) {
+      cplx a = mk(0, 0);
+      for (int k = lane; k < nparts; k += 32) a = cadd(a, ep[(int64_t)k * E + c]);
+      const double re = warp_sum(a.x), im = warp_sum(a.y);
+      if (lane == 0) z[c < P.p ? c : P.n - 2 * P.p + c] = mk(re, im);
     }
   }
-  __syncthreads();
-  for (int c = 0; c < P.p; ++c) {
-    double hr = block_sum(eh[c].x, red), hi = block_sum(eh[c].y, red);
-    double tr = block_sum(et[c].x, red), ti = block_sum(et[c].y, red);
-    if (threadIdx.x == 0) {
-      z[c] = mk(hr, hi);
-      z[P.n - P.p + c] = mk(tr, ti);
-    }
-  }
+  if (!cst) return;
+  CgState cs = cst[prob];
+  if (!cs.active) return;
+  __syncthreads();  // s complete block-wide
+  cg_sstep_dev(cs, cst + prob, z, pvec + (int64_t)prob * P.n, P.n, tol,
+               hist ? hist + (int64_t)prob * hist_stride : nullptr, hist_stride, red);
 }
 
 // ============================================================== 2D route

@@ -21,16 +21,18 @@ struct UniP {
   const cplx* ph_out;
 };
 
+constexpr int UNI_MAX_WARPS = 16;  // k_uni_* run 256 threads, the fused CGLS iteration 512
+
 struct Strided {
   int64_t prob, vec, elem;  // strides in complex elements
 };
 
 // y = D o (e^{i pi N xi} FFT_{-}(z)) + L x_head + R x_tail
-__global__ void k_uni_fwd(UniP P, const cplx* __restrict__ x, Strided xs, const cplx* __restrict__ rec,
-                          int64_t rec_prob, cplx* __restrict__ y, Strided ys, const double* __restrict__ post,
-                          int64_t post_prob, const cplx* __restrict__ tw, int logLmax) {
-  extern __shared__ cplx sm[];
-  const int vec = blockIdx.x, prob = blockIdx.y;
+// (device body: one CTA per (vec, prob); the caller owns the shared buffer sm)
+__device__ __forceinline__ void uni_fwd_body(const UniP& P, const cplx* __restrict__ x, Strided xs,
+                                             const cplx* __restrict__ rec, int64_t rec_prob, cplx* __restrict__ y,
+                                             Strided ys, const double* __restrict__ post, int64_t post_prob,
+                                             const cplx* __restrict__ tw, int logLmax, int vec, int prob, cplx* sm) {
   x += prob * xs.prob + vec * xs.vec;
   y += prob * ys.prob + vec * ys.vec;
   rec += prob * rec_prob;
@@ -50,25 +52,30 @@ __global__ void k_uni_fwd(UniP P, const cplx* __restrict__ x, Strided xs, const 
   __syncthreads();
   cplx* Z = sm;
   if (pow2) {
-    block_fft_padded(sm, P.logN2, 1, 0, tw, logLmax, -1);
+    block_fft_padded<true>(sm, P.logN2, 1, 0, tw, logLmax, -1);  // tw: the staged table
   } else {
     block_dft(sm, sm + P.N2, P.N2, -1);
     Z = sm + P.N2;
   }
-  cplx xh[8], xt[8];
-  if (P.edges)
-    for (int c = 0; c < P.p; ++c) {
-      xh[c] = x[c * xs.elem];
-      xt[c] = x[(P.n - P.p + c) * xs.elem];
-    }
+  cplx xh[8], xt[8];  // fixed-trip unrolled loops with a p predicate keep these in registers
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const bool on = P.edges && c < P.p;
+    xh[c] = on ? x[c * xs.elem] : mk(0, 0);
+    xt[c] = on ? x[(P.n - P.p + c) * xs.elem] : mk(0, 0);
+  }
   for (int m = threadIdx.x; m < P.M; m += blockDim.x) {
     cplx o = cmul(ldg2(P.ph_out + m), Z[pow2 ? fpad(m) : m]);
     const cplx* r = rec + (int64_t)m * R;
     cplx ym = cmul(r[0], o);
     if (P.edges) {
       cplx a = mk(0, 0), b = mk(0, 0);
-      for (int c = 0; c < P.p; ++c) a = cadd(a, cmul(r[1 + c], xh[c]));
-      for (int c = 0; c < P.p; ++c) b = cadd(b, cmul(r[1 + P.p + c], xt[c]));
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < P.p) a = cadd(a, cmul(r[1 + c], xh[c]));
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < P.p) b = cadd(b, cmul(r[1 + P.p + c], xt[c]));
       ym = cadd(ym, cadd(a, b));
     }
     if (post) ym = cscale(ym, post[m * ys.elem]);
@@ -76,14 +83,26 @@ __global__ void k_uni_fwd(UniP P, const cplx* __restrict__ x, Strided xs, const 
   }
 }
 
+__global__ void k_uni_fwd(UniP P, const cplx* __restrict__ x, Strided xs, const cplx* __restrict__ rec,
+                          int64_t rec_prob, cplx* __restrict__ y, Strided ys, const double* __restrict__ post,
+                          int64_t post_prob, const cplx* __restrict__ tw, int logLmax) {
+  extern __shared__ cplx sm[];  // FFT buffer + (power-of-two N2) N2/2 staged twiddles
+  const cplx* twf = tw;
+  if (P.logN2 >= 0) {  // visible after the body's first barrier
+    stage_twiddles(sm + fpad_len(P.N2), tw, P.logN2, logLmax);
+    twf = sm + fpad_len(P.N2);
+    logLmax = P.logN2;
+  }
+  uni_fwd_body(P, x, xs, rec, rec_prob, y, ys, post, post_prob, twf, logLmax, blockIdx.x, blockIdx.y, sm);
+}
+
 // z = gather_q(FFT_{+}(e^{-i pi N xi} conj(D) o u)) e^{-i phase l}, edge slots
 // replaced by L^H u / R^H u.   u = pre o y  (pre = sqrt(mu) on the tensor route)
-__global__ void k_uni_adj(UniP P, const cplx* __restrict__ y, Strided ys, const double* __restrict__ pre,
-                          int64_t pre_prob, const cplx* __restrict__ rec, int64_t rec_prob,
-                          cplx* __restrict__ z, Strided zs, const cplx* __restrict__ tw, int logLmax) {
-  extern __shared__ cplx sm[];
-  __shared__ double red[32];
-  const int vec = blockIdx.x, prob = blockIdx.y;
+__device__ __forceinline__ void uni_adj_body(const UniP& P, const cplx* __restrict__ y, Strided ys,
+                                             const double* __restrict__ pre, int64_t pre_prob,
+                                             const cplx* __restrict__ rec, int64_t rec_prob, cplx* __restrict__ z,
+                                             Strided zs, const cplx* __restrict__ tw, int logLmax, int vec, int prob,
+                                             cplx* sm, double* ered) {
   y += prob * ys.prob + vec * ys.vec;
   z += prob * zs.prob + vec * zs.vec;
   rec += prob * rec_prob;
@@ -103,15 +122,17 @@ __global__ void k_uni_adj(UniP P, const cplx* __restrict__ y, Strided ys, const 
     cplx val = cmul(v, conj_(ldg2(P.ph_out + m)));  // e^{-i pi N xi_m}, nufft.cpp:443-445
     sm[pow2 ? fpad(bitrev(m, P.logN2)) : m] = val;
     if (P.edges)
-      for (int c = 0; c < P.p; ++c) {
-        eh[c] = cadd(eh[c], cmul(conj_(r[1 + c]), u));
-        et[c] = cadd(et[c], cmul(conj_(r[1 + P.p + c]), u));
-      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < P.p) {
+          eh[c] = cadd(eh[c], cmul(conj_(r[1 + c]), u));
+          et[c] = cadd(et[c], cmul(conj_(r[1 + P.p + c]), u));
+        }
   }
   __syncthreads();
   cplx* Z = sm;
   if (pow2) {
-    block_fft_padded(sm, P.logN2, 1, 0, tw, logLmax, +1);
+    block_fft_padded<true>(sm, P.logN2, 1, 0, tw, logLmax, +1);  // tw: the staged table
   } else {
     block_dft(sm, sm + P.N2, P.N2, +1);
     Z = sm + P.N2;
@@ -122,16 +143,43 @@ __global__ void k_uni_adj(UniP P, const cplx* __restrict__ y, Strided ys, const 
     z[l * zs.elem] = v;
   }
   if (P.edges) {
-    // block reductions of L^H u, R^H u (freq2wave.cpp:323-324); all threads
-    // participate in every block_sum, thread 0 writes after the last one.
-    __syncthreads();
-    for (int c = 0; c < P.p; ++c) {
-      double hr = block_sum(eh[c].x, red), hi = block_sum(eh[c].y, red);
-      double tr = block_sum(et[c].x, red), ti = block_sum(et[c].y, red);
-      if (threadIdx.x == 0) {
-        z[c * zs.elem] = mk(hr, hi);
-        z[(P.n - P.p + c) * zs.elem] = mk(tr, ti);
+    // block reductions of L^H u, R^H u (freq2wave.cpp:323-324): warp sums of
+    // all 4p components, one barrier, then thread k < 4p folds component k
+    // over the warps in a fixed order (ered: >= 32 doubles per warp)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (c < P.p) {
+        const double v0 = warp_sum(eh[c].x), v1 = warp_sum(eh[c].y);
+        const double v2 = warp_sum(et[c].x), v3 = warp_sum(et[c].y);
+        if (lane == 0) {
+          ered[wid * 32 + 4 * c + 0] = v0;
+          ered[wid * 32 + 4 * c + 1] = v1;
+          ered[wid * 32 + 4 * c + 2] = v2;
+          ered[wid * 32 + 4 * c + 3] = v3;
+        }
       }
+    __syncthreads();  // also orders the zero writes of the edge slots above before the sums below
+    if (threadIdx.x < 4 * P.p) {
+      double a = 0.0;
+      for (int w = 0; w < nw; ++w) a += ered[w * 32 + threadIdx.x];
+      const int c = threadIdx.x >> 2, comp = threadIdx.x & 3;
+      const int idx = comp < 2 ? c : P.n - P.p + c;
+      reinterpret_cast<double*>(z + idx * zs.elem)[comp & 1] = a;
     }
   }
+}
+
+__global__ void k_uni_adj(UniP P, const cplx* __restrict__ y, Strided ys, const double* __restrict__ pre,
+                          int64_t pre_prob, const cplx* __restrict__ rec, int64_t rec_prob,
+                          cplx* __restrict__ z, Strided zs, const cplx* __restrict__ tw, int logLmax) {
+  extern __shared__ cplx sm[];  // FFT buffer + (power-of-two N2) N2/2 staged twiddles
+  __shared__ double ered[UNI_MAX_WARPS * 32];
+  const cplx* twf = tw;
+  if (P.logN2 >= 0) {  // visible after the body's first barrier
+    stage_twiddles(sm + fpad_len(P.N2), tw, P.logN2, logLmax);
+    twf = sm + fpad_len(P.N2);
+    logLmax = P.logN2;
+  }
+  uni_adj_body(P, y, ys, pre, pre_prob, rec, rec_prob, z, zs, twf, logLmax, blockIdx.x, blockIdx.y, sm, ered);
 }

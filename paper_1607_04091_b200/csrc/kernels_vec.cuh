@@ -191,3 +191,99 @@ __global__ void k_zero_if_ref0(cplx* __restrict__ x, int64_t len, int B, const C
   if (i >= len * B) return;
   if (st[i / len].ref == 0.0) x[i] = mk(0, 0);
 }
+
+// ---------------------------------------------------------------------------
+// One-CTA-per-problem forms of the scalar / vector phases (fused CGLS paths)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double norm2_local(const cplx* __restrict__ v, int len) {
+  double acc = 0.0;  // same per-entry fma order as k_norm2
+  for (int i = threadIdx.x; i < len; i += blockDim.x) {
+    const cplx a = v[i];
+    acc = fma(a.x, a.x, fma(a.y, a.y, acc));
+  }
+  return acc;
+}
+
+// qq = ||q||^2; alpha or stop; x += alpha p; r -= alpha q   (k_cg_alpha +
+// k_axpy_alpha x2).  One CTA owns the problem; returns false when it stopped.
+__device__ __forceinline__ bool cg_qstep_dev(CgState& cs, CgState* stp, const cplx* __restrict__ qp,
+                                             cplx* __restrict__ rp, cplx* __restrict__ xp,
+                                             const cplx* __restrict__ pp, int M, int n, double* red) {
+  const double qq = block_sum(norm2_local(qp, M), red);
+  cs.qq = qq;
+  if (qq == 0.0) {  // search direction in the numerical null space
+    cs.active = 0;
+    cs.alpha = 0.0;
+    if (threadIdx.x == 0) *stp = cs;
+    return false;
+  }
+  const double alpha = cs.gamma / qq;
+  cs.alpha = alpha;
+  for (int l = threadIdx.x; l < n; l += blockDim.x) {
+    const cplx a0 = xp[l], b0 = pp[l];
+    xp[l] = mk(fma(alpha, b0.x, a0.x), fma(alpha, b0.y, a0.y));
+  }
+  for (int m = threadIdx.x; m < M; m += blockDim.x) {
+    const cplx a0 = rp[m], b0 = qp[m];
+    rp[m] = mk(fma(-alpha, b0.x, a0.x), fma(-alpha, b0.y, a0.y));
+  }
+  return true;
+}
+
+// gamma' = ||s||^2; history; tolerance; beta; p = s + beta p   (k_cg_beta +
+// k_pupdate).  s must be complete block-wide (barrier before the call).
+__device__ __forceinline__ void cg_sstep_dev(CgState& cs, CgState* stp, const cplx* __restrict__ sp,
+                                             cplx* __restrict__ pp, int n, double tol, double* hist,
+                                             int hist_stride, double* red) {
+  const double gn = block_sum(norm2_local(sp, n), red);
+  const int it = cs.iterations + 1;
+  const double h = sqrt(gn) / cs.ref;
+  cs.iterations = it;
+  cs.hist_len = (it < hist_stride ? it : hist_stride - 1) + 1;
+  const bool stop = h <= tol;
+  if (stop) {
+    cs.converged = 1;
+    cs.active = 0;
+    cs.beta = 0.0;
+  } else {
+    cs.beta = gn / cs.gamma;
+    cs.gamma = gn;
+  }
+  if (threadIdx.x == 0) {
+    if (hist) hist[it < hist_stride ? it : hist_stride - 1] = h;
+    *stp = cs;
+  }
+  if (stop) return;
+  const double beta = cs.beta;
+  for (int l = threadIdx.x; l < n; l += blockDim.x) {
+    const cplx pv = pp[l], sv = sp[l];
+    pp[l] = mk(fma(beta, pv.x, sv.x), fma(beta, pv.y, sv.y));
+  }
+}
+
+constexpr int CG_STEP_THREADS = 1024;
+
+// the two scalar/vector phases of the generic iteration for problems whose
+// vectors one CTA reduces (Session chunks == 1): 2 launches instead of 7
+__global__ void __launch_bounds__(CG_STEP_THREADS)
+k_cg_qstep(CgState* st, const cplx* __restrict__ q, cplx* __restrict__ r, cplx* __restrict__ x,
+           const cplx* __restrict__ p, int64_t M, int64_t n) {
+  __shared__ double red[32];
+  const int prob = blockIdx.x;
+  CgState cs = st[prob];
+  if (!cs.active) return;
+  cg_qstep_dev(cs, st + prob, q + prob * M, r + prob * M, x + prob * n, p + prob * n, (int)M, (int)n, red);
+  if (threadIdx.x == 0 && cs.active) st[prob] = cs;  // alpha, qq
+}
+
+__global__ void __launch_bounds__(CG_STEP_THREADS)
+k_cg_sstep(CgState* st, const cplx* __restrict__ s, cplx* __restrict__ p, int64_t n, double tol, double* hist,
+           int hist_stride) {
+  __shared__ double red[32];
+  const int prob = blockIdx.x;
+  CgState cs = st[prob];
+  if (!cs.active) return;
+  cg_sstep_dev(cs, st + prob, s + prob * n, p + prob * n, (int)n, tol, hist ? hist + (int64_t)prob * hist_stride : nullptr,
+               hist_stride, red);
+}
+

@@ -349,3 +349,73 @@ def test_fast2d_tile_path_families_dense_tiles(p):
     check_apply(ref, op, rng)
     b = rc(ref.rows, rng)
     check_cgls(ref, op, b, 6)
+
+
+# ------------------------------------------------------------------ one-launch / two-launch CGLS iterations
+def test_fused_cgls_iterations_match_generic_and_oracle():
+    """The 1D-uniform whole-iteration kernel (k_uni_cgls_iter) and the
+    one-CTA-per-problem q/s steps (k_cg_qstep / k_cg_sstep) against the
+    generic 11-launch iteration (GS_B200_CG_FUSED=0, subprocess) and the
+    oracle: same iterates, iteration counts, converged flags and residual
+    histories, including a batch where one problem converges early under the
+    default tolerance and one has zero data (solver.cpp:42-48)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import json, numpy as np, oracle, paper_1607_04091_b200 as gs
+rng = np.random.default_rng(11)
+out = {}
+def rc(n):
+    return (rng.standard_normal(n) + 1j * rng.standard_normal(n)) / np.sqrt(2)
+cases = [("uni_haar", 1, 1, 9, oracle.gen_grid(1024, 1.0), None, 512.0),
+         ("uni_db2", 1, 2, 7, oracle.gen_grid(300, 0.5), None, None),
+         ("nfft_db4", 1, 4, 8, oracle.gen_jitter(700, 0.5, 0.2, 5, 1), "voronoi", None)]
+for name, dim, p, J, c, w, bw in cases:
+    K = bw if bw is not None else float(np.max(np.abs(c))) + 1e-9
+    mu = oracle.voronoi(1, c, K) if w else None
+    ref = oracle.Op(dim, p, J, c, weights=mu, bandwidth=K)
+    op = gs.freq2wave(gs.SamplingSet(dim, c), p, J, bandwidth=K, weights=mu)
+    b = ref.forward(rc(ref.cols)) + 1e-3 * rc(ref.rows)
+    x, st = gs.solve_least_squares(op, b, max_iterations=30, tolerance=1e-300)
+    xr, sr = ref.solve(b, max_iterations=30, tolerance=1e-300)
+    assert st.iterations == 30 and oracle.rel_error(x, xr) <= 1e-8, (name, oracle.rel_error(x, xr))
+    x2, st2 = gs.solve_least_squares(op, b)  # default tolerance: stops early
+    xr2, sr2 = ref.solve(b)
+    assert st2.iterations == sr2["iterations"] and st2.converged == sr2["converged"], (name, st2.iterations, sr2)
+    out[name] = [x.tolist(), list(st.history), x2.tolist(), st2.iterations]
+# batch: problem 1 has zero data, problem 2 converges early (exact data)
+sets = [gs.SamplingSet(1, oracle.gen_jitter(600, 0.5, 0.2, 30 + i, 1)) for i in range(3)]
+K = max(float(np.max(np.abs(s.coords))) for s in sets) + 1e-9
+op = gs.freq2wave(sets, 4, 8, bandwidth=K)
+refs = [oracle.Op(1, 4, 8, s.coords, bandwidth=K) for s in sets]
+bs = [refs[0].forward(rc(256)) + 1e-3 * rc(600), np.zeros(600, complex), refs[2].forward(rc(256))]
+xb, sts = gs.solve_least_squares(op, np.concatenate(bs), max_iterations=40, tolerance=1e-9)
+for i in range(3):
+    xr, sr = refs[i].solve(bs[i], max_iterations=40, tolerance=1e-9)
+    assert sts[i].iterations == sr["iterations"] and sts[i].converged == sr["converged"], (i, sts[i].iterations, sr)
+    e = oracle.rel_error(xb[i * 256:(i + 1) * 256], xr) if i != 1 else float(np.max(np.abs(xb[256:512])))
+    assert e <= 1e-8, (i, e)
+out["batch"] = [xb.tolist(), [s.iterations for s in sts]]
+print("ok" + json.dumps(out, default=lambda z: [z.real, z.imag]))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for fused in ("1", "0"):
+        env = dict(os.environ, GS_B200_CG_FUSED=fused, PYTHONPATH=root)
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0 and r.stdout.startswith("ok"), r.stdout[-2000:] + r.stderr[-4000:]
+        res[fused] = __import__("json").loads(r.stdout[2:])
+    for k in res["1"]:
+        a, b = res["1"][k], res["0"][k]
+        xa = np.array(a[0], float)
+        xb = np.array(b[0], float)
+        assert np.max(np.abs(xa - xb)) <= 1e-9 * max(1.0, np.max(np.abs(xb))), k
+        if k != "batch":
+            ha, hb = np.asarray(a[1]), np.asarray(b[1])
+            live = hb > 1e-9  # above the roundoff floor, where CGNR stagnates differently
+            assert np.allclose(ha[live], hb[live], rtol=1e-9, atol=0), k  # residual histories
+            assert a[3] == b[3], k
+        else:
+            assert a[1] == b[1]
