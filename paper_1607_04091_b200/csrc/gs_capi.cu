@@ -889,7 +889,7 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
             P, op->G.p, op->tw.p, op->logLmax);
       pmark("k2_cols_fft", st);
       if (P.edges) {
-        k2_lines_fft<<<dim3(4 * P.p, B), 256, fpad_len(P.n_ov) * sizeof(cplx), st>>>(P, x, op->deconv.p, op->lines.p, op->tw.p,
+        k2_lines_fft<<<dim3(4 * P.p, B), 256, n1_fft_smem(P), st>>>(P, x, op->deconv.p, op->lines.p, op->tw.p,
                                                                            op->logLmax);
         pmark("k2_lines_fft", st);
       }
@@ -1030,13 +1030,13 @@ bool adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
       pmark("k2_rows_ifft_crop", st);
       if (P.edges) {
         const int per = P.nt * 2 * P.p * P.R;
-        k2_fold_lines<<<dim3(nblk(per, 128), 2, B), 128, 0, st>>>(P, op->TL.p, op->tcs.p, op->cap, op->TLF.p);
+        k2_fold_lines<<<dim3(nblk(per, 32), 2, B), 32 * K2_FL_SPLIT, 0, st>>>(P, op->TL.p, op->tcs.p, op->cap, op->TLF.p);
         pmark("k2_fold_lines", st);
         const int ngroups = (op->cap + K2_CGROUP - 1) / K2_CGROUP;
         k2_fold_corners<<<dim3(nblk(ngroups * 4 * P.p * P.p, 128), B), 128, 0, st>>>(
             P, op->TC.p, op->ch_count.p, op->cap, ngroups, op->TCF.p);
         pmark("k2_fold_corners", st);
-        k2_edges<<<dim3(4 * P.p + 1, B), 256, fpad_len(P.n_ov) * sizeof(cplx), st>>>(
+        k2_edges<<<dim3(4 * P.p + 1, B), 256, std::max(n1_fft_smem(P), (size_t)256 * sizeof(cplx)), st>>>(
             P, op->TLF.p, op->TCF.p, op->tcs.p, op->ch_count.p, op->cap, op->deconv.p, z, op->tw.p, op->logLmax);
         pmark("k2_edges", st);
       }

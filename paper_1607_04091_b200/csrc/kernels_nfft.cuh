@@ -252,7 +252,9 @@ __global__ void k2_lines_fft(NfP P, const cplx* __restrict__ x, const double* __
   const int e = yline ? L : L - twop;
   const int fixed = edge_index(e, P.n, P.p);
   const cplx* X = x + (int64_t)prob * P.n * P.n;
+  cplx* tws = sm + fpad_len(P.n_ov);  // dynamic smem: + n_ov / 2 staged twiddles
   for (int i = threadIdx.x; i < fpad_len(P.n_ov); i += blockDim.x) sm[i] = mk(0, 0);
+  stage_twiddles(tws, tw, P.log_nov, logLmax);
   __syncthreads();
   for (int v = P.p + threadIdx.x; v < P.n - P.p; v += blockDim.x) {
     cplx val = yline ? X[(int64_t)v * P.n + fixed] : X[(int64_t)fixed * P.n + v];
@@ -260,7 +262,7 @@ __global__ void k2_lines_fft(NfP P, const cplx* __restrict__ x, const double* __
     sm[fpad(bitrev(pos, P.log_nov))] = cscale(val, deconv[v]);
   }
   __syncthreads();
-  block_fft_padded(sm, P.log_nov, 1, 0, tw, logLmax, -1);
+  block_fft_padded<true>(sm, P.log_nov, 1, 0, tws, P.log_nov, -1);
   cplx* out = lines + ((int64_t)prob * 2 * twop + L) * P.n_ov;
   for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) out[i] = sm[fpad(i)];
 }
@@ -591,28 +593,44 @@ __global__ void k2_rows_ifft_crop(NfP P, const cplx* __restrict__ G, const doubl
 // Fold the side-line partials of every chunk along the tile row (y-lines) or
 // tile column (x-lines) they belong to: TLF[prob][axis][t][e][l], one thread
 // per (t, e, l) -- a fully parallel first level of the line gather.
-__global__ void k2_fold_lines(NfP P, const cplx* __restrict__ TL, const int* __restrict__ tcs_all, int cap,
-                              cplx* __restrict__ TLF) {
+// per (axis, tile line t, edge column e, region offset l): the sum of the
+// side-line partials of every chunk on that tile line.  A CTA takes 32
+// consecutive outputs (one per lane: coalesced partial rows) and splits the
+// nt tiles of the line over K2_FL_SPLIT warps, folded through shared memory
+// in a fixed order -- a single problem (C4) gets nt / K2_FL_SPLIT dependent
+// loads per thread instead of nt.
+#define K2_FL_SPLIT 8
+__global__ void __launch_bounds__(32 * K2_FL_SPLIT)
+k2_fold_lines(NfP P, const cplx* __restrict__ TL, const int* __restrict__ tcs_all, int cap, cplx* __restrict__ TLF) {
+  __shared__ cplx part[K2_FL_SPLIT][32];
   const int prob = blockIdx.z, axis = blockIdx.y;
   const int twop = 2 * P.p, R = P.R, nt = P.nt;
   const int per = nt * twop * R;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= per) return;
-  const int t = i / (twop * R), rem = i - t * twop * R;  // rem = e * R + l
-  const int nlin = 2 * twop * R;
-  const int* tcs = tcs_all + (int64_t)prob * (nt * nt + 1);
-  const cplx* TLp = TL + (int64_t)prob * cap * nlin + (axis ? twop * R : 0) + rem;
+  const int lane = threadIdx.x & 31, sp = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + lane;
   cplx a = mk(0, 0);
-  for (int o = 0; o < nt; ++o) {
-    const int tile = axis == 0 ? t * nt + o : o * nt + t;
-    for (int ch = tcs[tile]; ch < tcs[tile + 1]; ++ch) a = cadd(a, ldg2(TLp + (int64_t)ch * nlin));
+  if (i < per) {
+    const int t = i / (twop * R), rem = i - t * twop * R;  // rem = e * R + l
+    const int nlin = 2 * twop * R;
+    const int* tcs = tcs_all + (int64_t)prob * (nt * nt + 1);
+    const cplx* TLp = TL + (int64_t)prob * cap * nlin + (axis ? twop * R : 0) + rem;
+    for (int o = sp; o < nt; o += K2_FL_SPLIT) {
+      const int tile = axis == 0 ? t * nt + o : o * nt + t;
+      for (int ch = tcs[tile]; ch < tcs[tile + 1]; ++ch) a = cadd(a, ldg2(TLp + (int64_t)ch * nlin));
+    }
   }
-  TLF[(((int64_t)prob * 2 + axis) * nt + t) * twop * R + rem] = a;
+  part[sp][lane] = a;
+  __syncthreads();
+  if (sp == 0 && i < per) {
+    for (int k = 1; k < K2_FL_SPLIT; ++k) a = cadd(a, part[k][lane]);
+    const int t = i / (twop * R), rem = i - t * twop * R;
+    TLF[(((int64_t)prob * 2 + axis) * nt + t) * twop * R + rem] = a;
+  }
 }
 
 // First level of the corner reduction: TCF[prob][g][q] = sum of the corner
 // partials of chunks g*64 .. g*64+63 (fixed order).
-#define K2_CGROUP 64
+#define K2_CGROUP 16
 __global__ void k2_fold_corners(NfP P, const cplx* __restrict__ TC, const int* __restrict__ ch_count, int cap,
                                 int ngroups, cplx* __restrict__ TCF) {
   const int prob = blockIdx.y;
@@ -637,14 +655,21 @@ __global__ void k2_edges(NfP P, const cplx* __restrict__ TLF, const cplx* __rest
   const int nlin = 2 * twop * R;
   const int* tcs = tcs_all + (int64_t)prob * (nt * nt + 1);
   cplx* Z = z + (int64_t)prob * n * n;
-  if (L == 2 * twop) {  // corners: fixed-order sum of the chunk-group partials (TC = TCF here)
+  if (L == 2 * twop) {  // corners: fixed-order sum of the chunk-group partials (TC = TCF here),
+    // the groups split over blockDim / ncorner thread slices folded in shared memory
     const int ncorner = 4 * p * p;
     const int ngroups = (cap + K2_CGROUP - 1) / K2_CGROUP;
     const cplx* tc = TC + (int64_t)prob * ngroups * ncorner;
     const int nch = (ch_count[prob] + K2_CGROUP - 1) / K2_CGROUP;
-    for (int q = threadIdx.x; q < ncorner; q += blockDim.x) {
-      cplx a = mk(0, 0);
-      for (int t = 0; t < nch; ++t) a = cadd(a, tc[(int64_t)t * ncorner + q]);
+    const int nsl = max(1, (int)blockDim.x / ncorner);  // slices (ncorner <= 256 for p <= 8)
+    const int q = threadIdx.x % ncorner, sl = threadIdx.x / ncorner;
+    cplx a = mk(0, 0);
+    if (sl < nsl)
+      for (int t = sl; t < nch; t += nsl) a = cadd(a, tc[(int64_t)t * ncorner + q]);
+    if (sl < nsl) sm[sl * ncorner + q] = a;
+    __syncthreads();
+    if (sl == 0) {
+      for (int k = 1; k < nsl; ++k) a = cadd(a, sm[k * ncorner + q]);
       const int k = q / (p * p), rem = q - k * p * p, i = rem / p, j = rem - i * p;
       const int row0 = (k < 2) ? 0 : n - p, col0 = (k % 2 == 0) ? 0 : n - p;
       Z[(int64_t)(col0 + j) * n + row0 + i] = a;
@@ -656,6 +681,8 @@ __global__ void k2_edges(NfP P, const cplx* __restrict__ TLF, const cplx* __rest
   const cplx* TLFp = TLF + ((int64_t)prob * 2 + (yline ? 0 : 1)) * nt * twop * R;
   (void)nlin;
   (void)tcs;
+  cplx* tws = sm + fpad_len(P.n_ov);  // dynamic smem: + n_ov / 2 staged twiddles
+  stage_twiddles(tws, tw, P.log_nov, logLmax);
   for (int pos = threadIdx.x; pos < P.n_ov; pos += blockDim.x) {
     cplx a = mk(0, 0);
     int tk[MAX_COVER], lk[MAX_COVER];
@@ -664,7 +691,7 @@ __global__ void k2_edges(NfP P, const cplx* __restrict__ TLF, const cplx* __rest
     sm[fpad(bitrev(pos, P.log_nov))] = a;
   }
   __syncthreads();
-  block_fft_padded(sm, P.log_nov, 1, 0, tw, logLmax, +1);
+  block_fft_padded<true>(sm, P.log_nov, 1, 0, tws, P.log_nov, +1);
   const int fixed = edge_index(e, n, p);
   for (int v = p + threadIdx.x; v < n - p; v += blockDim.x) {
     cplx val = cscale(sm[fpad((v - n / 2 + P.n_ov) & (P.n_ov - 1))], deconv[v]);
