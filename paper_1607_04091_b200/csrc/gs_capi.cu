@@ -1116,6 +1116,24 @@ void norm2(Session& S, const cplx* v, int64_t len, int chunks, cudaStream_t st) 
   CKL();
 }
 
+// ||v||^2 per problem followed by the alpha (q) or beta (s) step of the iteration
+void norm2_step(Session& S, const cplx* v, int64_t len, int chunks, cudaStream_t st, bool alpha) {
+  if (chunks <= 1) {
+    norm2(S, v, len, chunks, st);
+    if (alpha) k_cg_alpha<<<nblk(S.B, 128), 128, 0, st>>>(S.st.p, S.n2.p, S.B);
+    else k_cg_beta<<<nblk(S.B, 128), 128, 0, st>>>(S.st.p, S.n2.p, S.tol, S.hist.p, S.hist_cap, S.B);
+    pmark(alpha ? "k_cg_alpha" : "k_cg_beta", st);
+  } else {
+    k_norm2_part<<<dim3(chunks, S.B), 512, 0, st>>>(v, len, chunks, S.part.p);
+    pmark("k_norm2_part", st);
+    if (alpha) k_norm2_fold_alpha<<<nblk(S.B, 128), 128, 0, st>>>(S.part.p, chunks, S.B, S.st.p);
+    else
+      k_norm2_fold_beta<<<nblk(S.B, 128), 128, 0, st>>>(S.part.p, chunks, S.B, S.st.p, S.tol, S.hist.p, S.hist_cap);
+    pmark(alpha ? "k_norm2_fold_alpha" : "k_norm2_fold_beta", st);
+  }
+  CKL();
+}
+
 int pick_chunks(int B, int64_t len) {
   int c = (int)std::max<int64_t>(1, std::min<int64_t>(64, (296 + B - 1) / B));
   c = (int)std::min<int64_t>(c, std::max<int64_t>(1, len / 4096));
@@ -1198,6 +1216,18 @@ void session_iterate_body(Session& S, cudaStream_t st) {
       k_cg_sstep<<<S.B, CG_STEP_THREADS, 0, st>>>(S.st.p, S.s.p, S.p.p, S.Nc, S.tol, S.hist.p, S.hist_cap);
       pmark("k_cg_sstep", st);                                                                 // gamma', beta, p
     }
+    CKL();
+    return;
+  }
+  if (cg_fused_enabled()) {  // 6 launches around T / T*: folds fused with alpha / beta, one axpy launch
+    forward_dev(op, S.p.p, S.q.p, false, st);  // q = T p
+    norm2_step(S, S.q.p, S.M, S.chunks_M, st, true);  // qq, alpha (or stop)
+    k_axpy_xr<<<nblk(TN + TM, 256), 256, 0, st>>>(S.x.p, S.p.p, S.Nc, S.r.p, S.q.p, S.M, S.B, S.st.p);
+    pmark("k_axpy_xr", st);  // x += alpha p, r -= alpha q
+    adjoint_dev(op, S.r.p, S.s.p, false, st);  // s = T* r
+    norm2_step(S, S.s.p, S.Nc, S.chunks_N, st, false);  // gamma', beta
+    k_pupdate<<<nblk(TN, 256), 256, 0, st>>>(S.p.p, S.s.p, S.Nc, S.B, S.st.p);  // p = s + beta p
+    pmark("k_pupdate", st);
     CKL();
     return;
   }

@@ -599,7 +599,7 @@ __global__ void k2_rows_ifft_crop(NfP P, const cplx* __restrict__ G, const doubl
 // nt tiles of the line over K2_FL_SPLIT warps, folded through shared memory
 // in a fixed order -- a single problem (C4) gets nt / K2_FL_SPLIT dependent
 // loads per thread instead of nt.
-#define K2_FL_SPLIT 16
+#define K2_FL_SPLIT 8
 __global__ void __launch_bounds__(32 * K2_FL_SPLIT)
 k2_fold_lines(NfP P, const cplx* __restrict__ TL, const int* __restrict__ tcs_all, int cap, cplx* __restrict__ TLF) {
   __shared__ cplx part[K2_FL_SPLIT][32];

@@ -113,31 +113,28 @@ __global__ void k_cg_gamma0(CgState* st, const double* __restrict__ n2, double t
 }
 
 // qq = ||q||^2; break on qq == 0; alpha = gamma / qq  (solver.cpp:71-74)
-__global__ void k_cg_alpha(CgState* st, const double* __restrict__ n2, int B) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  CgState s = st[b];
-  if (!s.active) return;
-  s.qq = n2[b];
+__device__ __forceinline__ void cg_alpha_dev(CgState& s, double qq) {
+  s.qq = qq;
   if (s.qq == 0.0) {
     s.active = 0;  // search direction in the numerical null space
     s.alpha = 0.0;
   } else {
     s.alpha = s.gamma / s.qq;
   }
+}
+__global__ void k_cg_alpha(CgState* st, const double* __restrict__ n2, int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  CgState s = st[b];
+  if (!s.active) return;
+  cg_alpha_dev(s, n2[b]);
   st[b] = s;
 }
 
 // gamma' = ||s||^2; history; tolerance; beta  (solver.cpp:77-87)
 // (the iteration number lives on the device, so one captured CUDA graph replays
 // every iteration)
-__global__ void k_cg_beta(CgState* st, const double* __restrict__ n2, double tol, double* hist, int hist_stride,
-                          int B) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  CgState s = st[b];
-  if (!s.active) return;
-  double gn = n2[b];
+__device__ __forceinline__ void cg_beta_dev(CgState& s, double gn, double tol, double* hist, int hist_stride, int b) {
   const int it = s.iterations + 1;
   s.iterations = it;
   double h = sqrt(gn) / s.ref;
@@ -151,7 +148,61 @@ __global__ void k_cg_beta(CgState* st, const double* __restrict__ n2, double tol
     s.beta = gn / s.gamma;
     s.gamma = gn;
   }
+}
+__global__ void k_cg_beta(CgState* st, const double* __restrict__ n2, double tol, double* hist, int hist_stride,
+                          int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  CgState s = st[b];
+  if (!s.active) return;
+  cg_beta_dev(s, n2[b], tol, hist, hist_stride, b);
   st[b] = s;
+}
+
+// the two-level norm's fold fused with the alpha / beta step (one launch less each)
+__global__ void k_norm2_fold_alpha(const double* __restrict__ part, int chunks, int B, CgState* st) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  CgState s = st[b];
+  if (!s.active) return;
+  double a = 0.0;  // same sequential order as k_norm2_fold
+  for (int c = 0; c < chunks; ++c) a += part[(int64_t)b * chunks + c];
+  cg_alpha_dev(s, a);
+  st[b] = s;
+}
+__global__ void k_norm2_fold_beta(const double* __restrict__ part, int chunks, int B, CgState* st, double tol,
+                                  double* hist, int hist_stride) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  CgState s = st[b];
+  if (!s.active) return;
+  double a = 0.0;
+  for (int c = 0; c < chunks; ++c) a += part[(int64_t)b * chunks + c];
+  cg_beta_dev(s, a, tol, hist, hist_stride, b);
+  st[b] = s;
+}
+
+// x += alpha p (first lenx * B entries of the grid) and r -= alpha q (the next
+// lenr * B) in one launch -- k_axpy_alpha twice
+__global__ void k_axpy_xr(cplx* __restrict__ x, const cplx* __restrict__ p, int64_t lenx, cplx* __restrict__ r,
+                          const cplx* __restrict__ q, int64_t lenr, int B, const CgState* st) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  cplx* v;
+  const cplx* w;
+  int64_t len;
+  double sign;
+  if (i < lenx * B) {
+    v = x; w = p; len = lenx; sign = 1.0;
+  } else {
+    i -= lenx * B;
+    if (i >= lenr * B) return;
+    v = r; w = q; len = lenr; sign = -1.0;
+  }
+  const CgState& s = st[i / len];
+  if (!s.active) return;
+  const double a = sign * s.alpha;
+  cplx a0 = v[i], b0 = w[i];
+  v[i] = mk(fma(a, b0.x, a0.x), fma(a, b0.y, a0.y));
 }
 
 // v += alpha w   (x += alpha p,  solver.cpp:75)  -- only while the problem is active
