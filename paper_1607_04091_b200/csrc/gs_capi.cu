@@ -400,6 +400,8 @@ void attach_phases(UniP& P, DBuf<cplx>& buf, cudaStream_t st) {
   P.ph_in = buf.p;
   P.ph_out = buf.p + P.n;
 }
+// tensor-route passes: many CTAs of one short vector each -> small CTAs, one wave
+constexpr int UNI_TENSOR_THREADS = 128;
 // single-CTA 1D FFT kernels: padded line + staged twiddles
 size_t n1_fft_smem(const NfP& P) { return (size_t)(fpad_len(P.n_ov) + P.n_ov / 2) * sizeof(cplx); }
 size_t uni_smem(const UniP& P) { return (size_t)(P.logN2 >= 0 ? fpad_len(P.N2) : 2 * P.N2) * sizeof(cplx); }
@@ -850,12 +852,12 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
     case GS_ROUTE_TENSOR_2D: {
       const int64_t n = op->n, Ma = op->Ma, Mb = op->Mb;
       // W(a, j) = sum_i ax_a(i) X(i, j): one vector per column j
-      k_uni_fwd<<<dim3((unsigned)n, B), 256, uni_smem_tw(op->upx), st>>>(
+      k_uni_fwd<<<dim3((unsigned)n, B), UNI_TENSOR_THREADS, uni_smem_tw(op->upx), st>>>(
           op->upx, x, Strided{n * n, n, 1}, op->rec_ax.p, Ma * op->Rr, op->W.p, Strided{Ma * n, 1, n}, nullptr, 0,
           op->tw.p, op->logLmax);
       pmark("k_uni_fwd[x-pass]", st);
       // Y(a, b) = sum_j ay_b(j) W(a, j): one vector per row a
-      k_uni_fwd<<<dim3((unsigned)Ma, B), 256, uni_smem_tw(op->upy), st>>>(
+      k_uni_fwd<<<dim3((unsigned)Ma, B), UNI_TENSOR_THREADS, uni_smem_tw(op->upy), st>>>(
           op->upy, op->W.p, Strided{Ma * n, n, 1}, op->rec_ay.p, Mb * op->Rr, y, Strided{op->M, Mb, 1},
           op->weighted ? op->sqrtw.p : nullptr, op->M, op->tw.p, op->logLmax);
       pmark("k_uni_fwd[y-pass]", st);
@@ -950,12 +952,12 @@ bool adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
     case GS_ROUTE_TENSOR_2D: {
       const int64_t n = op->n, Ma = op->Ma, Mb = op->Mb;
       // V(a, j) = sum_b conj(ay_b(j)) (sqrt(mu) y)(a, b): one vector per row a
-      k_uni_adj<<<dim3((unsigned)Ma, B), 256, uni_smem_tw(op->upy), st>>>(
+      k_uni_adj<<<dim3((unsigned)Ma, B), UNI_TENSOR_THREADS, uni_smem_tw(op->upy), st>>>(
           op->upy, y, Strided{op->M, Mb, 1}, op->weighted ? op->sqrtw.p : nullptr, op->M, op->rec_ay.p, Mb * op->Rr,
           op->W.p, Strided{Ma * n, n, 1}, op->tw.p, op->logLmax);
       pmark("k_uni_adj[y-pass]", st);
       // X(i, j) = sum_a conj(ax_a(i)) V(a, j): one vector per column j
-      k_uni_adj<<<dim3((unsigned)n, B), 256, uni_smem_tw(op->upx), st>>>(
+      k_uni_adj<<<dim3((unsigned)n, B), UNI_TENSOR_THREADS, uni_smem_tw(op->upx), st>>>(
           op->upx, op->W.p, Strided{Ma * n, 1, n}, nullptr, 0, op->rec_ax.p, Ma * op->Rr, z, Strided{n * n, n, 1},
           op->tw.p, op->logLmax);
       pmark("k_uni_adj[x-pass]", st);

@@ -83,7 +83,9 @@ __device__ __forceinline__ void uni_fwd_body(const UniP& P, const cplx* __restri
   }
 }
 
-__global__ void k_uni_fwd(UniP P, const cplx* __restrict__ x, Strided xs, const cplx* __restrict__ rec,
+// <= 128 registers: 2 CTAs of 256 or 4 of 128 threads per SM (the tensor route
+// launches 256-512 CTAs of 128 threads: one wave on 148 SMs)
+__global__ void __launch_bounds__(256, 2) k_uni_fwd(UniP P, const cplx* __restrict__ x, Strided xs, const cplx* __restrict__ rec,
                           int64_t rec_prob, cplx* __restrict__ y, Strided ys, const double* __restrict__ post,
                           int64_t post_prob, const cplx* __restrict__ tw, int logLmax) {
   extern __shared__ cplx sm[];  // FFT buffer + (power-of-two N2) N2/2 staged twiddles
@@ -170,7 +172,7 @@ __device__ __forceinline__ void uni_adj_body(const UniP& P, const cplx* __restri
   }
 }
 
-__global__ void k_uni_adj(UniP P, const cplx* __restrict__ y, Strided ys, const double* __restrict__ pre,
+__global__ void __launch_bounds__(256, 2) k_uni_adj(UniP P, const cplx* __restrict__ y, Strided ys, const double* __restrict__ pre,
                           int64_t pre_prob, const cplx* __restrict__ rec, int64_t rec_prob,
                           cplx* __restrict__ z, Strided zs, const cplx* __restrict__ tw, int logLmax) {
   extern __shared__ cplx sm[];  // FFT buffer + (power-of-two N2) N2/2 staged twiddles
