@@ -839,13 +839,14 @@ void pmark(const char* name, cudaStream_t st) {
 // ------------------------------------------------------------------ applies
 // x, y are device pointers; perm_io: samples in the caller's order (true) or
 // the internal bin-sorted order (false, used inside CGLS).
-void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t st) {
+// npart (tensor route only): per-vector partials of ||y||^2 from the last pass, [B][Ma]
+void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t st, double* npart = nullptr) {
   const int B = op->B;
   switch (op->route) {
     case GS_ROUTE_UNIFORM_1D: {
       const UniP& P = op->up;
       k_uni_fwd<<<dim3(1, B), 256, uni_smem_tw(P), st>>>(P, x, Strided{op->n, 0, 1}, op->rec_u.p, op->M * op->Rr, y,
-                                                     Strided{op->M, 0, 1}, nullptr, 0, op->tw.p, op->logLmax);
+                                                     Strided{op->M, 0, 1}, nullptr, 0, op->tw.p, op->logLmax, nullptr);
       pmark("k_uni_fwd", st);
       break;
     }
@@ -854,12 +855,12 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
       // W(a, j) = sum_i ax_a(i) X(i, j): one vector per column j
       k_uni_fwd<<<dim3((unsigned)n, B), UNI_TENSOR_THREADS, uni_smem_tw(op->upx), st>>>(
           op->upx, x, Strided{n * n, n, 1}, op->rec_ax.p, Ma * op->Rr, op->W.p, Strided{Ma * n, 1, n}, nullptr, 0,
-          op->tw.p, op->logLmax);
+          op->tw.p, op->logLmax, nullptr);
       pmark("k_uni_fwd[x-pass]", st);
       // Y(a, b) = sum_j ay_b(j) W(a, j): one vector per row a
       k_uni_fwd<<<dim3((unsigned)Ma, B), UNI_TENSOR_THREADS, uni_smem_tw(op->upy), st>>>(
           op->upy, op->W.p, Strided{Ma * n, n, 1}, op->rec_ay.p, Mb * op->Rr, y, Strided{op->M, Mb, 1},
-          op->weighted ? op->sqrtw.p : nullptr, op->M, op->tw.p, op->logLmax);
+          op->weighted ? op->sqrtw.p : nullptr, op->M, op->tw.p, op->logLmax, npart);
       pmark("k_uni_fwd[y-pass]", st);
       break;
     }
@@ -938,14 +939,16 @@ struct SStep {
 };
 
 // returns true when the route ran the s-step `ss` itself (NFFT_1D: in k_n1_ifft_crop)
-bool adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t st, const SStep* ss = nullptr) {
+// npart (tensor route only): per-vector partials of ||z||^2 from the last pass, [B][n]
+bool adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t st, const SStep* ss = nullptr,
+                 double* npart = nullptr) {
   bool fused_sstep = false;
   const int B = op->B;
   switch (op->route) {
     case GS_ROUTE_UNIFORM_1D: {
       const UniP& P = op->up;
       k_uni_adj<<<dim3(1, B), 256, uni_smem_tw(P), st>>>(P, y, Strided{op->M, 0, 1}, nullptr, 0, op->rec_u.p,
-                                                     op->M * op->Rr, z, Strided{op->n, 0, 1}, op->tw.p, op->logLmax);
+                                                     op->M * op->Rr, z, Strided{op->n, 0, 1}, op->tw.p, op->logLmax, nullptr);
       pmark("k_uni_adj", st);
       break;
     }
@@ -954,12 +957,12 @@ bool adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
       // V(a, j) = sum_b conj(ay_b(j)) (sqrt(mu) y)(a, b): one vector per row a
       k_uni_adj<<<dim3((unsigned)Ma, B), UNI_TENSOR_THREADS, uni_smem_tw(op->upy), st>>>(
           op->upy, y, Strided{op->M, Mb, 1}, op->weighted ? op->sqrtw.p : nullptr, op->M, op->rec_ay.p, Mb * op->Rr,
-          op->W.p, Strided{Ma * n, n, 1}, op->tw.p, op->logLmax);
+          op->W.p, Strided{Ma * n, n, 1}, op->tw.p, op->logLmax, nullptr);
       pmark("k_uni_adj[y-pass]", st);
       // X(i, j) = sum_a conj(ax_a(i)) V(a, j): one vector per column j
       k_uni_adj<<<dim3((unsigned)n, B), UNI_TENSOR_THREADS, uni_smem_tw(op->upx), st>>>(
           op->upx, op->W.p, Strided{Ma * n, 1, n}, nullptr, 0, op->rec_ax.p, Ma * op->Rr, z, Strided{n * n, n, 1},
-          op->tw.p, op->logLmax);
+          op->tw.p, op->logLmax, npart);
       pmark("k_uni_adj[x-pass]", st);
       break;
     }
@@ -1088,6 +1091,7 @@ struct Session {
   DBuf<cplx> b, r, q, x, p, s;
   DBuf<CgState> st;
   DBuf<double> n2, part, hist;
+  DBuf<double> vpart;  // tensor route: per-vector norm partials of T / T* outputs
   DBuf<int> flag;
   int chunks_M = 1, chunks_N = 1;
   // one CGLS iteration captured as a CUDA graph (replayed on a private stream
@@ -1163,6 +1167,7 @@ void session_begin(Session& S, gs_op* op, const cplx* b_raw, bool b_perm, const 
   S.chunks_M = pick_chunks(S.B, S.M);
   S.chunks_N = pick_chunks(S.B, S.Nc);
   S.part.alloc((size_t)S.B * std::max(S.chunks_M, S.chunks_N));
+  if (op->route == GS_ROUTE_TENSOR_2D) S.vpart.alloc((size_t)S.B * std::max<int64_t>(op->Ma, op->n));
   S.hist.alloc((size_t)S.B * hist_cap);
   S.flag.alloc(1);
   const bool sorted = op->route == GS_ROUTE_NFFT_1D || op->route == GS_ROUTE_NFFT_2D;
@@ -1218,6 +1223,22 @@ void session_iterate_body(Session& S, cudaStream_t st) {
       k_cg_sstep<<<S.B, CG_STEP_THREADS, 0, st>>>(S.st.p, S.s.p, S.p.p, S.Nc, S.tol, S.hist.p, S.hist_cap);
       pmark("k_cg_sstep", st);                                                                 // gamma', beta, p
     }
+    CKL();
+    return;
+  }
+  if (op->route == GS_ROUTE_TENSOR_2D && cg_fused_enabled()) {
+    // the last pass of T / T* writes per-vector norm partials: 4 launches around the 4 passes
+    const int Ma = (int)op->Ma, n = (int)op->n;
+    forward_dev(op, S.p.p, S.q.p, false, st, S.vpart.p);  // q = T p (+ ||q||^2 partials)
+    k_fold_alpha_w<<<S.B, 32, 0, st>>>(S.vpart.p, Ma, S.st.p);
+    pmark("k_fold_alpha_w", st);
+    k_axpy_xr<<<nblk(TN + TM, 256), 256, 0, st>>>(S.x.p, S.p.p, S.Nc, S.r.p, S.q.p, S.M, S.B, S.st.p);
+    pmark("k_axpy_xr", st);
+    adjoint_dev(op, S.r.p, S.s.p, false, st, nullptr, S.vpart.p);  // s = T* r (+ ||s||^2 partials)
+    k_fold_beta_w<<<S.B, 32, 0, st>>>(S.vpart.p, n, S.st.p, S.tol, S.hist.p, S.hist_cap);
+    pmark("k_fold_beta_w", st);
+    k_pupdate<<<nblk(TN, 256), 256, 0, st>>>(S.p.p, S.s.p, S.Nc, S.B, S.st.p);
+    pmark("k_pupdate", st);
     CKL();
     return;
   }
@@ -1278,7 +1299,7 @@ void session_iterate(Session& S, cudaStream_t st, int k) {
   }
   uint64_t tol_bits = 0;
   std::memcpy(&tol_bits, &S.tol, sizeof(tol_bits));
-  const std::vector<const void*> sig = {S.p.p, S.q.p, S.r.p, S.s.p, S.x.p, S.st.p, S.n2.p, S.hist.p, S.part.p,
+  const std::vector<const void*> sig = {S.p.p, S.q.p, S.r.p, S.s.p, S.x.p, S.st.p, S.n2.p, S.hist.p, S.part.p, S.vpart.p,
                                         reinterpret_cast<const void*>((intptr_t)S.hist_cap),
                                         reinterpret_cast<const void*>((uintptr_t)tol_bits)};
   if (S.gexec && (sig != S.graph_sig)) {

@@ -87,7 +87,7 @@ __device__ __forceinline__ void uni_fwd_body(const UniP& P, const cplx* __restri
 // launches 256-512 CTAs of 128 threads: one wave on 148 SMs)
 __global__ void __launch_bounds__(256, 2) k_uni_fwd(UniP P, const cplx* __restrict__ x, Strided xs, const cplx* __restrict__ rec,
                           int64_t rec_prob, cplx* __restrict__ y, Strided ys, const double* __restrict__ post,
-                          int64_t post_prob, const cplx* __restrict__ tw, int logLmax) {
+                          int64_t post_prob, const cplx* __restrict__ tw, int logLmax, double* npart) {
   extern __shared__ cplx sm[];  // FFT buffer + (power-of-two N2) N2/2 staged twiddles
   const cplx* twf = tw;
   if (P.logN2 >= 0) {  // visible after the body's first barrier
@@ -96,6 +96,17 @@ __global__ void __launch_bounds__(256, 2) k_uni_fwd(UniP P, const cplx* __restri
     logLmax = P.logN2;
   }
   uni_fwd_body(P, x, xs, rec, rec_prob, y, ys, post, post_prob, twf, logLmax, blockIdx.x, blockIdx.y, sm);
+  if (npart) {  // ||y_vec||^2 of this CTA's output vector (each thread re-reads the entries it wrote)
+    __shared__ double red[32];
+    const cplx* yv = y + blockIdx.y * ys.prob + blockIdx.x * ys.vec;
+    double acc = 0.0;
+    for (int m = threadIdx.x; m < P.M; m += blockDim.x) {
+      const cplx a = yv[m * ys.elem];
+      acc = fma(a.x, a.x, fma(a.y, a.y, acc));
+    }
+    const double v = block_sum(acc, red);
+    if (threadIdx.x == 0) npart[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = v;
+  }
 }
 
 // z = gather_q(FFT_{+}(e^{-i pi N xi} conj(D) o u)) e^{-i phase l}, edge slots
@@ -174,7 +185,8 @@ __device__ __forceinline__ void uni_adj_body(const UniP& P, const cplx* __restri
 
 __global__ void __launch_bounds__(256, 2) k_uni_adj(UniP P, const cplx* __restrict__ y, Strided ys, const double* __restrict__ pre,
                           int64_t pre_prob, const cplx* __restrict__ rec, int64_t rec_prob,
-                          cplx* __restrict__ z, Strided zs, const cplx* __restrict__ tw, int logLmax) {
+                          cplx* __restrict__ z, Strided zs, const cplx* __restrict__ tw, int logLmax,
+                          double* npart) {
   extern __shared__ cplx sm[];  // FFT buffer + (power-of-two N2) N2/2 staged twiddles
   __shared__ double ered[UNI_MAX_WARPS * 32];
   const cplx* twf = tw;
@@ -184,4 +196,15 @@ __global__ void __launch_bounds__(256, 2) k_uni_adj(UniP P, const cplx* __restri
     logLmax = P.logN2;
   }
   uni_adj_body(P, y, ys, pre, pre_prob, rec, rec_prob, z, zs, twf, logLmax, blockIdx.x, blockIdx.y, sm, ered);
+  if (npart) {  // ||z_vec||^2 of this CTA's output vector
+    __syncthreads();  // edge slots written by other threads
+    const cplx* zv = z + blockIdx.y * zs.prob + blockIdx.x * zs.vec;
+    double acc = 0.0;
+    for (int l = threadIdx.x; l < P.n; l += blockDim.x) {
+      const cplx a = zv[l * zs.elem];
+      acc = fma(a.x, a.x, fma(a.y, a.y, acc));
+    }
+    const double v = block_sum(acc, ered);
+    if (threadIdx.x == 0) npart[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = v;
+  }
 }

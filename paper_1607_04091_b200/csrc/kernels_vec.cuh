@@ -182,6 +182,33 @@ __global__ void k_norm2_fold_beta(const double* __restrict__ part, int chunks, i
   st[b] = s;
 }
 
+// many-partial folds (the tensor route's per-vector norms): one warp per
+// problem, lane-strided sums then a fixed-order warp reduction
+__device__ __forceinline__ double fold_warp(const double* __restrict__ part, int chunks) {
+  double a = 0.0;
+  for (int c = threadIdx.x; c < chunks; c += 32) a += part[c];
+  return warp_sum(a);
+}
+__global__ void k_fold_alpha_w(const double* __restrict__ part, int chunks, CgState* st) {
+  const int b = blockIdx.x;
+  const double qq = fold_warp(part + (int64_t)b * chunks, chunks);
+  if (threadIdx.x) return;
+  CgState s = st[b];
+  if (!s.active) return;
+  cg_alpha_dev(s, qq);
+  st[b] = s;
+}
+__global__ void k_fold_beta_w(const double* __restrict__ part, int chunks, CgState* st, double tol, double* hist,
+                              int hist_stride) {
+  const int b = blockIdx.x;
+  const double gn = fold_warp(part + (int64_t)b * chunks, chunks);
+  if (threadIdx.x) return;
+  CgState s = st[b];
+  if (!s.active) return;
+  cg_beta_dev(s, gn, tol, hist, hist_stride, b);
+  st[b] = s;
+}
+
 // x += alpha p (first lenx * B entries of the grid) and r -= alpha q (the next
 // lenr * B) in one launch -- k_axpy_alpha twice
 __global__ void k_axpy_xr(cplx* __restrict__ x, const cplx* __restrict__ p, int64_t lenx, cplx* __restrict__ r,

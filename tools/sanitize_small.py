@@ -1,6 +1,5 @@
-"""Small solves through every route, for compute-sanitizer (memcheck / racecheck /
-synccheck) runs of the kernels: python tools/sanitize_small.py
-(GPU box: compute-sanitizer --tool racecheck python tools/sanitize_small.py)."""
+"""Small solves through every route (uniform 1D, 1D NFFT, tensor, 2D NFFT): a
+debug driver for bounds / assert builds of the kernels: python tools/sanitize_small.py"""
 import os
 import sys
 
