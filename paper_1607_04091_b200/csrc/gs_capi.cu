@@ -840,7 +840,10 @@ void pmark(const char* name, cudaStream_t st) {
 // x, y are device pointers; perm_io: samples in the caller's order (true) or
 // the internal bin-sorted order (false, used inside CGLS).
 // npart (tensor route only): per-vector partials of ||y||^2 from the last pass, [B][Ma]
-void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t st, double* npart = nullptr) {
+// n1q (1D NFFT route inside CGLS): the interpolation applies the deferred r
+// update and writes ||q||^2 partials; the spreading runs the q-step
+void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t st, double* npart = nullptr,
+                 const N1QStep* n1q = nullptr) {
   const int B = op->B;
   switch (op->route) {
     case GS_ROUTE_UNIFORM_1D: {
@@ -869,7 +872,8 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
       k_n1_embed_fft<<<B, 256, n1_fft_smem(P), st>>>(P, x, op->deconv.p, op->G.p, op->tw.p, op->logLmax);
       pmark("k_n1_embed_fft", st);
       k_n1_interp<<<dim3(nblk(op->M, 128), B), 128, 0, st>>>(P, op->base_x.p, op->wts_x.p, op->rec_x.p, op->G.p, x,
-                                                              perm_io ? op->perm.p : nullptr, y);
+                                                              perm_io ? op->perm.p : nullptr, y,
+                                                              n1q ? *n1q : N1QStep{});
       pmark("k_n1_interp", st);
       break;
     }
@@ -941,7 +945,7 @@ struct SStep {
 // returns true when the route ran the s-step `ss` itself (NFFT_1D: in k_n1_ifft_crop)
 // npart (tensor route only): per-vector partials of ||z||^2 from the last pass, [B][n]
 bool adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t st, const SStep* ss = nullptr,
-                 double* npart = nullptr) {
+                 double* npart = nullptr, const N1QStep* n1q = nullptr) {
   bool fused_sstep = false;
   const int B = op->B;
   switch (op->route) {
@@ -970,7 +974,8 @@ bool adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
       const NfP& P = op->np;
       const int nparts = (P.n_ov + N1_SPREAD_CELLS - 1) / N1_SPREAD_CELLS;
       k_n1_spread<<<dim3(nparts, B), N1_SPREAD_THREADS, 0, st>>>(P, op->bins.p, op->wts_x.p, op->rec_x.p, y,
-                                                                perm_io ? op->perm.p : nullptr, op->G.p, op->EP.p);
+                                                                perm_io ? op->perm.p : nullptr, op->G.p, op->EP.p,
+                                                                n1q ? *n1q : N1QStep{});
       pmark("k_n1_spread", st);
       k_n1_ifft_crop<<<B, 256, n1_fft_smem(P), st>>>(P, op->G.p, op->deconv.p, op->EP.p, nparts, z, op->tw.p,
                                                       op->logLmax, ss ? ss->st : nullptr, ss ? ss->p : nullptr,
@@ -1168,6 +1173,7 @@ void session_begin(Session& S, gs_op* op, const cplx* b_raw, bool b_perm, const 
   S.chunks_N = pick_chunks(S.B, S.Nc);
   S.part.alloc((size_t)S.B * std::max(S.chunks_M, S.chunks_N));
   if (op->route == GS_ROUTE_TENSOR_2D) S.vpart.alloc((size_t)S.B * std::max<int64_t>(op->Ma, op->n));
+  if (op->route == GS_ROUTE_NFFT_1D) S.vpart.alloc((size_t)S.B * ((S.M + 127) / 128));  // interpolation CTAs
   S.hist.alloc((size_t)S.B * hist_cap);
   S.flag.alloc(1);
   const bool sorted = op->route == GS_ROUTE_NFFT_1D || op->route == GS_ROUTE_NFFT_2D;
@@ -1210,6 +1216,16 @@ void session_iterate_body(Session& S, cudaStream_t st) {
                                                                  S.s.p, S.r.p, S.q.p, S.st.p, S.tol, S.hist.p,
                                                                  S.hist_cap, op->tw.p, op->logLmax, 1);
     pmark("k_uni_cgls_iter", st);
+    CKL();
+    return;
+  }
+  if (op->route == GS_ROUTE_NFFT_1D && cg_fused_enabled()) {
+    // 4 launches: embed+FFT, interpolation (+ deferred r update, ||q||^2 partials),
+    // spreading (+ q-step), inverse FFT (+ s-step)
+    const N1QStep q1{S.vpart.p, (int)((S.M + 127) / 128), S.q.p, S.r.p, S.st.p, S.x.p, S.p.p};
+    forward_dev(op, S.p.p, S.q.p, false, st, nullptr, &q1);
+    const SStep ss{S.st.p, S.p.p, S.tol, S.hist.p, S.hist_cap};
+    adjoint_dev(op, S.r.p, S.s.p, false, st, &ss, nullptr, &q1);
     CKL();
     return;
   }

@@ -52,32 +52,67 @@ __global__ void k_n1_embed_fft(NfP P, const cplx* __restrict__ x, const double* 
   for (int i = threadIdx.x; i < P.n_ov; i += blockDim.x) G[i] = sm[fpad(i)];
 }
 
-// interpolation + D + L/R  (nufft.cpp:273-284, freq2wave.cpp:232-236)
+// CGLS q-step split over the two 1D gridding kernels (k_cg_qstep's work, no
+// launch of its own).  k_n1_spread: qq from the interpolation's per-CTA
+// partials (the same fixed-order fold in every CTA), alpha, the adjoint's input
+// r - alpha q formed as the samples are read, x <- x + alpha p grid-strided;
+// CTA 0 stores the state with pend_alpha = alpha.  r itself is updated one
+// kernel later, by the next iteration's k_n1_interp: the thread of sample s
+// applies r[s] -= pend_alpha q[s] before it overwrites q[s] (13 spreading CTAs
+// read each r[s], so the spreading cannot store it).
+struct N1QStep {
+  double* qpart;
+  int nqpart;
+  const cplx* q;
+  cplx* r;
+  CgState* st;
+  cplx* x;
+  const cplx* p;
+};
+
+// interpolation + D + L/R  (nufft.cpp:273-284, freq2wave.cpp:232-236);
+// inside CGLS (qpart != nullptr) each CTA also writes its partial ||q||^2
+// (qpart[prob][blockIdx.x]) for the q-step fused into k_n1_spread
 __global__ void k_n1_interp(NfP P, const int* __restrict__ base, const double* __restrict__ wts,
                             const cplx* __restrict__ rec, const cplx* __restrict__ G, const cplx* __restrict__ x,
-                            const int* __restrict__ out_perm, cplx* __restrict__ y) {
+                            const int* __restrict__ out_perm, cplx* __restrict__ y, N1QStep qs) {
   const int prob = blockIdx.y;
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (s >= P.M) return;
-  const int64_t gs = prob * P.M + s;
-  const int Rr = 1 + (P.edges ? 2 * P.p : 0);
-  const cplx* g = G + (int64_t)prob * P.n_ov;
-  const int b = base[gs];
-  const double* w = wts + gs * P.S;
-  cplx acc = mk(0, 0);
-  for (int t = 0; t < P.S; ++t) acc = caxpy(acc, w[t], ldg2(g + ((b + t) & (P.n_ov - 1))));
-  const cplx* r = rec + gs * Rr;
-  cplx ym = cmul(r[0], acc);
-  if (P.edges) {
-    const cplx* xp = x + (int64_t)prob * P.n;
-    cplx a = mk(0, 0), c2 = mk(0, 0);
-    for (int c = 0; c < P.p; ++c) a = cadd(a, cmul(r[1 + c], ldg2(xp + c)));
-    for (int c = 0; c < P.p; ++c) c2 = cadd(c2, cmul(r[1 + P.p + c], ldg2(xp + P.n - P.p + c)));
-    ym = cadd(ym, cadd(a, c2));
+  double nq = 0.0;
+  const double pend = qs.st ? qs.st[prob].pend_alpha : 0.0;
+  if (s < P.M) {
+    if (pend != 0.0) {  // previous iteration's r -= alpha q (sorted order: y[s] is q[s])
+      const int64_t gi = prob * P.M + s;
+      const cplx qv = y[gi], rv = qs.r[gi];
+      qs.r[gi] = mk(fma(-pend, qv.x, rv.x), fma(-pend, qv.y, rv.y));
+    }
+    const int64_t gs = prob * P.M + s;
+    const int Rr = 1 + (P.edges ? 2 * P.p : 0);
+    const cplx* g = G + (int64_t)prob * P.n_ov;
+    const int b = base[gs];
+    const double* w = wts + gs * P.S;
+    cplx acc = mk(0, 0);
+    for (int t = 0; t < P.S; ++t) acc = caxpy(acc, w[t], ldg2(g + ((b + t) & (P.n_ov - 1))));
+    const cplx* r = rec + gs * Rr;
+    cplx ym = cmul(r[0], acc);
+    if (P.edges) {
+      const cplx* xp = x + (int64_t)prob * P.n;
+      cplx a = mk(0, 0), c2 = mk(0, 0);
+      for (int c = 0; c < P.p; ++c) a = cadd(a, cmul(r[1 + c], ldg2(xp + c)));
+      for (int c = 0; c < P.p; ++c) c2 = cadd(c2, cmul(r[1 + P.p + c], ldg2(xp + P.n - P.p + c)));
+      ym = cadd(ym, cadd(a, c2));
+    }
+    const int64_t o = out_perm ? (int64_t)out_perm[gs] : s;
+    y[prob * P.M + o] = ym;
+    nq = fma(ym.x, ym.x, ym.y * ym.y);
   }
-  const int64_t o = out_perm ? (int64_t)out_perm[gs] : s;
-  y[prob * P.M + o] = ym;
+  if (qs.st) {
+    __shared__ double red[32];
+    const double v = block_sum(nq, red);
+    if (threadIdx.x == 0) qs.qpart[(int64_t)prob * gridDim.x + blockIdx.x] = v;
+  }
 }
+
 
 // spreading, owner-computes: cell j sums w_s[t] conj(D_s) y_s over the points
 // whose window base is (j - t) mod n_ov  (transpose of nufft.cpp:313-322).
@@ -92,9 +127,40 @@ constexpr int N1_SPREAD_CELLS = N1_SPREAD_THREADS / 16;
 __global__ void __launch_bounds__(N1_SPREAD_THREADS)
 k_n1_spread(NfP P, const int* __restrict__ cell_start, const double* __restrict__ wts,
             const cplx* __restrict__ rec, const cplx* __restrict__ yin, const int* __restrict__ in_perm,
-            cplx* __restrict__ line, cplx* __restrict__ edge_part) {
+            cplx* __restrict__ line, cplx* __restrict__ edge_part, N1QStep qs) {
   __shared__ cplx esm[N1_SPREAD_THREADS / 32][16];
+  __shared__ double s_alpha;
   const int prob = blockIdx.y;
+  double alpha = 0.0;  // nonzero only while a fused q-step updates r
+  if (qs.st) {
+    if (threadIdx.x < 32) {
+      double a = 0.0;
+      const double* qp = qs.qpart + (int64_t)prob * qs.nqpart;
+      for (int k = threadIdx.x; k < qs.nqpart; k += 32) a += qp[k];
+      a = warp_sum(a);
+      if (threadIdx.x == 0) {
+        CgState cs = qs.st[prob];
+        double al = 0.0;
+        if (cs.active) {
+          cg_alpha_dev(cs, a);  // stops the problem when qq == 0 (no update)
+          if (cs.active) al = cs.alpha;
+        }
+        cs.pend_alpha = al;  // r's deferred update (0: none)
+        if (blockIdx.x == 0) qs.st[prob] = cs;
+        s_alpha = al;
+      }
+    }
+    __syncthreads();
+    alpha = s_alpha;
+    if (alpha != 0.0) {
+      cplx* xp = qs.x + (int64_t)prob * P.n;
+      const cplx* pp = qs.p + (int64_t)prob * P.n;
+      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n; i += gridDim.x * blockDim.x) {
+        const cplx a0 = xp[i], b0 = pp[i];
+        xp[i] = mk(fma(alpha, b0.x, a0.x), fma(alpha, b0.y, a0.y));
+      }
+    }
+  }
   const int lane16 = threadIdx.x & 15;
   const int j = blockIdx.x * N1_SPREAD_CELLS + (threadIdx.x >> 4);  // n_ov is a multiple of the cells per CTA
   const int Rr = 1 + (P.edges ? 2 * P.p : 0);
@@ -110,7 +176,11 @@ k_n1_spread(NfP P, const int* __restrict__ cell_start, const double* __restrict_
     const int s1 = cs[cell + 1];
     for (int s = cs[cell]; s < s1; ++s) {
       const int64_t gs = prob * P.M + s;
-      const cplx yv = ldg2(yp + (in_perm ? (int64_t)in_perm[gs] : s));
+      cplx yv = ldg2(yp + (in_perm ? (int64_t)in_perm[gs] : s));
+      if (alpha != 0.0) {  // r - alpha q (k_axpy_alpha's arithmetic); in CGLS the order is internal
+        const cplx qv = ldg2(qs.q + gs);
+        yv = mk(fma(-alpha, qv.x, yv.x), fma(-alpha, qv.y, yv.y));
+      }
       const cplx* r = rec + gs * Rr;
       const cplx v = cmul(conj_(ldg2(r)), yv);
       acc = caxpy(acc, __ldg(wts + gs * P.S + t), v);

@@ -16,6 +16,7 @@ struct CgState {
   int iterations;
   int converged;
   int hist_len;
+  double pend_alpha;  // 1D NFFT fused q-step: alpha of the r update the next interpolation applies
 };
 
 // out[prob] = sum |v|^2 over len entries (one block per problem; fixed order)
@@ -79,7 +80,7 @@ __global__ void k_cg_ref(CgState* st, const double* __restrict__ n2, int B) {
   if (b >= B) return;
   CgState s;
   s.ref = sqrt(n2[b]);
-  s.gamma = s.gamma_new = s.qq = s.alpha = s.beta = 0.0;
+  s.gamma = s.gamma_new = s.qq = s.alpha = s.beta = s.pend_alpha = 0.0;
   s.iterations = 0;
   s.converged = 0;
   s.hist_len = 0;
