@@ -6,11 +6,11 @@
 // Sample-space data (base cell, 13 window weights, D/L/R record) is held in
 // bin-sorted order ("s" index); perm[s] maps back to the caller's order.
 // Spreading (the adjoint) is output-owned, never a global atomic:
-//   1D  -- one thread per oversampled cell gathers from the sorted bins;
-//   2D  -- one CTA per 16x16 grid tile accumulates its points into
-//          per-warp shared-memory copies of the tile+halo, writes the region
-//          once, and the inverse column FFT gathers the <= 4 overlapping
-//          tile regions that cover each cell while loading.
+//   1D  -- 16 lanes per oversampled cell (one per tap) gather from the
+//          sorted bins and fold by shuffles;
+//   2D  -- per-chunk partial regions (generic k2_spread here, the DMMA
+//          kernels in kernels_nfft2d_fast.cuh), folded per tile from a
+//          source list (k2_fold_src) so every grid cell is written once.
 #pragma once
 #include "gs_common.cuh"
 #include "kernels_vec.cuh"
