@@ -353,8 +353,9 @@ def test_fast2d_tile_path_families_dense_tiles(p):
 
 # ------------------------------------------------------------------ one-launch / two-launch CGLS iterations
 def test_fused_cgls_iterations_match_generic_and_oracle():
-    """The 1D-uniform whole-iteration kernel (k_uni_cgls_iter) and the
-    one-CTA-per-problem q/s steps (k_cg_qstep / k_cg_sstep) against the
+    """The fused CGLS iterations -- 1D uniform in one launch (k_uni_cgls_iter),
+    1D NFFT with the q/s steps inside the gridding kernels, the tensor route's
+    norm partials, the 2D generic 6-launch form -- against the
     generic 11-launch iteration (GS_B200_CG_FUSED=0, subprocess) and the
     oracle: same iterates, iteration counts, converged flags and residual
     histories, including a batch where one problem converges early under the
@@ -370,19 +371,25 @@ def rc(n):
     return (rng.standard_normal(n) + 1j * rng.standard_normal(n)) / np.sqrt(2)
 cases = [("uni_haar", 1, 1, 9, oracle.gen_grid(1024, 1.0), None, 512.0),
          ("uni_db2", 1, 2, 7, oracle.gen_grid(300, 0.5), None, None),
-         ("nfft_db4", 1, 4, 8, oracle.gen_jitter(700, 0.5, 0.2, 5, 1), "voronoi", None)]
+         ("nfft_db4", 1, 4, 8, oracle.gen_jitter(700, 0.5, 0.2, 5, 1), "voronoi", None),
+         ("tensor_db2", 2, 2, 4, oracle.gen_grid(32, 1.0, 2), None, 16.0),
+         ("nfft2d_db4", 2, 4, 5, oracle.gen_jitter(48, 0.5, 0.2, 6, 2), "voronoi", None)]
 for name, dim, p, J, c, w, bw in cases:
     K = bw if bw is not None else float(np.max(np.abs(c))) + 1e-9
-    mu = oracle.voronoi(1, c, K) if w else None
+    mu = oracle.voronoi(dim, c, K) if w else None
     ref = oracle.Op(dim, p, J, c, weights=mu, bandwidth=K)
     op = gs.freq2wave(gs.SamplingSet(dim, c), p, J, bandwidth=K, weights=mu)
     b = ref.forward(rc(ref.cols)) + 1e-3 * rc(ref.rows)
-    x, st = gs.solve_least_squares(op, b, max_iterations=30, tolerance=1e-300)
-    xr, sr = ref.solve(b, max_iterations=30, tolerance=1e-300)
-    assert st.iterations == 30 and oracle.rel_error(x, xr) <= 1e-8, (name, oracle.rel_error(x, xr))
-    x2, st2 = gs.solve_least_squares(op, b)  # default tolerance: stops early
-    xr2, sr2 = ref.solve(b)
-    assert st2.iterations == sr2["iterations"] and st2.converged == sr2["converged"], (name, st2.iterations, sr2)
+    its = 30 if dim == 1 else 12
+    x, st = gs.solve_least_squares(op, b, max_iterations=its, tolerance=1e-300)
+    xr, sr = ref.solve(b, max_iterations=its, tolerance=1e-300)
+    assert st.iterations == its and oracle.rel_error(x, xr) <= 1e-8, (name, oracle.rel_error(x, xr))
+    if dim == 1:
+        x2, st2 = gs.solve_least_squares(op, b)  # default tolerance: stops early
+        xr2, sr2 = ref.solve(b)
+        assert st2.iterations == sr2["iterations"] and st2.converged == sr2["converged"], (name, st2.iterations, sr2)
+    else:
+        x2, st2 = x, st
     out[name] = [x.tolist(), list(st.history), x2.tolist(), st2.iterations]
 # batch: problem 1 has zero data, problem 2 converges early (exact data)
 sets = [gs.SamplingSet(1, oracle.gen_jitter(600, 0.5, 0.2, 30 + i, 1)) for i in range(3)]
