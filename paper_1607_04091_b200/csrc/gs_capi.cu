@@ -402,6 +402,13 @@ void attach_phases(UniP& P, DBuf<cplx>& buf, cudaStream_t st) {
 }
 // tensor-route passes: many CTAs of one short vector each -> small CTAs, one wave
 constexpr int UNI_TENSOR_THREADS = 128;
+// k_uni_cgls_iter with the problem resident in shared memory: FFT buffer +
+// twiddles + p, x, s (n) + r, q (M) + factor records (M x Rr); 0 when it does not fit
+size_t uni_cg_resident_smem(const UniP& P, int Rr) {
+  const size_t buf = P.logN2 >= 0 ? (size_t)fpad_len(P.N2) + P.N2 / 2 : 2 * (size_t)P.N2;
+  const size_t bytes = (buf + 3 * (size_t)P.n + 2 * (size_t)P.M + (size_t)P.M * Rr) * sizeof(cplx);
+  return bytes + UNI_MAX_WARPS * 32 * sizeof(double) <= (size_t)kSmemMax ? bytes : 0;
+}
 // single-CTA 1D FFT kernels: padded line + staged twiddles
 size_t n1_fft_smem(const NfP& P) { return (size_t)(fpad_len(P.n_ov) + P.n_ov / 2) * sizeof(cplx); }
 size_t uni_smem(const UniP& P) { return (size_t)(P.logN2 >= 0 ? fpad_len(P.N2) : 2 * P.N2) * sizeof(cplx); }
@@ -1212,9 +1219,10 @@ void session_iterate_body(Session& S, cudaStream_t st) {
   const int64_t TM = S.M * S.B, TN = S.Nc * S.B;
   if (op->route == GS_ROUTE_UNIFORM_1D && cg_fused_enabled()) {  // whole iteration in one launch
     const UniP& P = op->up;
-    k_uni_cgls_iter<<<S.B, UNI_CG_THREADS, uni_smem_tw(P), st>>>(P, op->rec_u.p, op->M * op->Rr, S.x.p, S.p.p,
-                                                                 S.s.p, S.r.p, S.q.p, S.st.p, S.tol, S.hist.p,
-                                                                 S.hist_cap, op->tw.p, op->logLmax, 1);
+    const size_t rs = uni_cg_resident_smem(P, op->Rr);
+    k_uni_cgls_iter<<<S.B, UNI_CG_THREADS, rs ? rs : uni_smem_tw(P), st>>>(
+        P, op->rec_u.p, op->M * op->Rr, S.x.p, S.p.p, S.s.p, S.r.p, S.q.p, S.st.p, S.tol, S.hist.p, S.hist_cap,
+        op->tw.p, op->logLmax, 1, rs != 0);
     pmark("k_uni_cgls_iter", st);
     CKL();
     return;
@@ -1302,9 +1310,10 @@ void session_iterate(Session& S, cudaStream_t st, int k) {
   if (S.op->route == GS_ROUTE_UNIFORM_1D && cg_fused_enabled() && !g_prof.on) {
     // all k iterations in one launch (k_uni_cgls_iter loops on the device)
     const UniP& P = S.op->up;
-    k_uni_cgls_iter<<<S.B, UNI_CG_THREADS, uni_smem_tw(P), st>>>(P, S.op->rec_u.p, S.op->M * S.op->Rr, S.x.p, S.p.p,
-                                                                 S.s.p, S.r.p, S.q.p, S.st.p, S.tol, S.hist.p,
-                                                                 S.hist_cap, S.op->tw.p, S.op->logLmax, k);
+    const size_t rs = uni_cg_resident_smem(P, S.op->Rr);
+    k_uni_cgls_iter<<<S.B, UNI_CG_THREADS, rs ? rs : uni_smem_tw(P), st>>>(
+        P, S.op->rec_u.p, S.op->M * S.op->Rr, S.x.p, S.p.p, S.s.p, S.r.p, S.q.p, S.st.p, S.tol, S.hist.p,
+        S.hist_cap, S.op->tw.p, S.op->logLmax, k, rs != 0);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     CKL();
     return;
