@@ -608,7 +608,10 @@ gs_op* create(const gs_op_desc* dsc) {
 #ifndef F_CWMAX
 #define F_CWMAX 8
 #endif
-    P.CW = std::max(1, std::min(F_CWMAX, (int)((120 * 1024) / ((fpad_len(n_ov) + 1) * (int)sizeof(cplx)))));
+#ifndef F_CWBUDGET  // shared-memory budget of the column-FFT CTAs (bytes of column lines)
+#define F_CWBUDGET (120 * 1024)
+#endif
+    P.CW = std::max(1, std::min(F_CWMAX, (int)((F_CWBUDGET) / ((fpad_len(n_ov) + 1) * (int)sizeof(cplx)))));
     while (n_ov % P.CW) --P.CW;
     P.RW = std::max(1, std::min(8, 2048 / n_ov));
     d_xi_x.upload(xi_x.data(), total, st);
