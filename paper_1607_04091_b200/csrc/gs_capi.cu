@@ -852,14 +852,16 @@ void pmark(const char* name, cudaStream_t st) {
 // npart (tensor route only): per-vector partials of ||y||^2 from the last pass, [B][Ma]
 // n1q (1D NFFT route inside CGLS): the interpolation applies the deferred r
 // update and writes ||q||^2 partials; the spreading runs the q-step
+// pre_a (tensor route): a CGLS vector update the x-pass CTAs apply first
 void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t st, double* npart = nullptr,
-                 const N1QStep* n1q = nullptr) {
+                 const N1QStep* n1q = nullptr, const UniPre* pre_a = nullptr) {
   const int B = op->B;
   switch (op->route) {
     case GS_ROUTE_UNIFORM_1D: {
       const UniP& P = op->up;
       k_uni_fwd<<<dim3(1, B), 256, uni_smem_tw(P), st>>>(P, x, Strided{op->n, 0, 1}, op->rec_u.p, op->M * op->Rr, y,
-                                                     Strided{op->M, 0, 1}, nullptr, 0, op->tw.p, op->logLmax, nullptr);
+                                                     Strided{op->M, 0, 1}, nullptr, 0, op->tw.p, op->logLmax, nullptr,
+                                                     UniPre{});
       pmark("k_uni_fwd", st);
       break;
     }
@@ -868,12 +870,12 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
       // W(a, j) = sum_i ax_a(i) X(i, j): one vector per column j
       k_uni_fwd<<<dim3((unsigned)n, B), UNI_TENSOR_THREADS, uni_smem_tw(op->upx), st>>>(
           op->upx, x, Strided{n * n, n, 1}, op->rec_ax.p, Ma * op->Rr, op->W.p, Strided{Ma * n, 1, n}, nullptr, 0,
-          op->tw.p, op->logLmax, nullptr);
+          op->tw.p, op->logLmax, nullptr, pre_a ? *pre_a : UniPre{});
       pmark("k_uni_fwd[x-pass]", st);
       // Y(a, b) = sum_j ay_b(j) W(a, j): one vector per row a
       k_uni_fwd<<<dim3((unsigned)Ma, B), UNI_TENSOR_THREADS, uni_smem_tw(op->upy), st>>>(
           op->upy, op->W.p, Strided{Ma * n, n, 1}, op->rec_ay.p, Mb * op->Rr, y, Strided{op->M, Mb, 1},
-          op->weighted ? op->sqrtw.p : nullptr, op->M, op->tw.p, op->logLmax, npart);
+          op->weighted ? op->sqrtw.p : nullptr, op->M, op->tw.p, op->logLmax, npart, UniPre{});
       pmark("k_uni_fwd[y-pass]", st);
       break;
     }
@@ -954,15 +956,18 @@ struct SStep {
 
 // returns true when the route ran the s-step `ss` itself (NFFT_1D: in k_n1_ifft_crop)
 // npart (tensor route only): per-vector partials of ||z||^2 from the last pass, [B][n]
+// pre_a / pre_b (tensor route): CGLS vector updates the y-pass / x-pass CTAs apply first
 bool adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t st, const SStep* ss = nullptr,
-                 double* npart = nullptr, const N1QStep* n1q = nullptr) {
+                 double* npart = nullptr, const N1QStep* n1q = nullptr, const UniPre* pre_a = nullptr,
+                 const UniPre* pre_b = nullptr) {
   bool fused_sstep = false;
   const int B = op->B;
   switch (op->route) {
     case GS_ROUTE_UNIFORM_1D: {
       const UniP& P = op->up;
       k_uni_adj<<<dim3(1, B), 256, uni_smem_tw(P), st>>>(P, y, Strided{op->M, 0, 1}, nullptr, 0, op->rec_u.p,
-                                                     op->M * op->Rr, z, Strided{op->n, 0, 1}, op->tw.p, op->logLmax, nullptr);
+                                                     op->M * op->Rr, z, Strided{op->n, 0, 1}, op->tw.p, op->logLmax, nullptr,
+                                                     UniPre{});
       pmark("k_uni_adj", st);
       break;
     }
@@ -971,12 +976,12 @@ bool adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
       // V(a, j) = sum_b conj(ay_b(j)) (sqrt(mu) y)(a, b): one vector per row a
       k_uni_adj<<<dim3((unsigned)Ma, B), UNI_TENSOR_THREADS, uni_smem_tw(op->upy), st>>>(
           op->upy, y, Strided{op->M, Mb, 1}, op->weighted ? op->sqrtw.p : nullptr, op->M, op->rec_ay.p, Mb * op->Rr,
-          op->W.p, Strided{Ma * n, n, 1}, op->tw.p, op->logLmax, nullptr);
+          op->W.p, Strided{Ma * n, n, 1}, op->tw.p, op->logLmax, nullptr, pre_a ? *pre_a : UniPre{});
       pmark("k_uni_adj[y-pass]", st);
       // X(i, j) = sum_a conj(ax_a(i)) V(a, j): one vector per column j
       k_uni_adj<<<dim3((unsigned)n, B), UNI_TENSOR_THREADS, uni_smem_tw(op->upx), st>>>(
           op->upx, op->W.p, Strided{Ma * n, 1, n}, nullptr, 0, op->rec_ax.p, Ma * op->Rr, z, Strided{n * n, n, 1},
-          op->tw.p, op->logLmax, npart);
+          op->tw.p, op->logLmax, npart, pre_b ? *pre_b : UniPre{});
       pmark("k_uni_adj[x-pass]", st);
       break;
     }
@@ -1255,17 +1260,19 @@ void session_iterate_body(Session& S, cudaStream_t st) {
   }
   if (op->route == GS_ROUTE_TENSOR_2D && cg_fused_enabled()) {
     // the last pass of T / T* writes per-vector norm partials: 4 launches around the 4 passes
-    const int Ma = (int)op->Ma, n = (int)op->n;
-    forward_dev(op, S.p.p, S.q.p, false, st, S.vpart.p);  // q = T p (+ ||q||^2 partials)
+    // and the axpys ride on the passes that own the vectors: the x-pass of T
+    // forms p = s + beta p (deferred from the previous iteration), the y-pass of
+    // T* forms r -= alpha q, the x-pass of T* x += alpha p: 6 launches
+    const int Ma = (int)op->Ma, n = (int)op->n, Mb = (int)op->Mb;
+    const UniPre pre_p{S.st.p, 1, S.p.p, S.s.p, (int64_t)n * n, n, 1, n};
+    const UniPre pre_r{S.st.p, 2, S.r.p, S.q.p, S.M, Mb, 1, Mb};
+    const UniPre pre_x{S.st.p, 3, S.x.p, S.p.p, (int64_t)n * n, n, 1, n};
+    forward_dev(op, S.p.p, S.q.p, false, st, S.vpart.p, nullptr, &pre_p);  // q = T p (+ ||q||^2 partials)
     k_fold_alpha_w<<<S.B, 32, 0, st>>>(S.vpart.p, Ma, S.st.p);
     pmark("k_fold_alpha_w", st);
-    k_axpy_xr<<<nblk(TN + TM, 256), 256, 0, st>>>(S.x.p, S.p.p, S.Nc, S.r.p, S.q.p, S.M, S.B, S.st.p);
-    pmark("k_axpy_xr", st);
-    adjoint_dev(op, S.r.p, S.s.p, false, st, nullptr, S.vpart.p);  // s = T* r (+ ||s||^2 partials)
+    adjoint_dev(op, S.r.p, S.s.p, false, st, nullptr, S.vpart.p, nullptr, &pre_r, &pre_x);  // s = T* r
     k_fold_beta_w<<<S.B, 32, 0, st>>>(S.vpart.p, n, S.st.p, S.tol, S.hist.p, S.hist_cap);
     pmark("k_fold_beta_w", st);
-    k_pupdate<<<nblk(TN, 256), 256, 0, st>>>(S.p.p, S.s.p, S.Nc, S.B, S.st.p);
-    pmark("k_pupdate", st);
     CKL();
     return;
   }

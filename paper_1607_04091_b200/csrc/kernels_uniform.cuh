@@ -7,6 +7,7 @@
 // route T = T_x (x) T_y on a uniform tensor grid.
 #pragma once
 #include "gs_common.cuh"
+#include "kernels_vec.cuh"
 
 struct UniP {
   int n;          // coefficients per vector (N = 2^J)
@@ -87,8 +88,13 @@ __device__ __forceinline__ void uni_fwd_body(const UniP& P, const cplx* __restri
 // launches 256-512 CTAs of 128 threads: one wave on 148 SMs)
 __global__ void __launch_bounds__(256, 2) k_uni_fwd(UniP P, const cplx* __restrict__ x, Strided xs, const cplx* __restrict__ rec,
                           int64_t rec_prob, cplx* __restrict__ y, Strided ys, const double* __restrict__ post,
-                          int64_t post_prob, const cplx* __restrict__ tw, int logLmax, double* npart) {
+                          int64_t post_prob, const cplx* __restrict__ tw, int logLmax, double* npart,
+                          UniPre upd) {
   extern __shared__ cplx sm[];  // FFT buffer + (power-of-two N2) N2/2 staged twiddles
+  if (upd.st) {  // CGLS update of the vector this CTA owns (its input when mode 1)
+    uni_pre_apply(upd, blockIdx.x, blockIdx.y);
+    __syncthreads();
+  }
   const cplx* twf = tw;
   if (P.logN2 >= 0) {  // visible after the body's first barrier
     stage_twiddles(sm + fpad_len(P.N2), tw, P.logN2, logLmax);
@@ -186,9 +192,13 @@ __device__ __forceinline__ void uni_adj_body(const UniP& P, const cplx* __restri
 __global__ void __launch_bounds__(256, 2) k_uni_adj(UniP P, const cplx* __restrict__ y, Strided ys, const double* __restrict__ pre,
                           int64_t pre_prob, const cplx* __restrict__ rec, int64_t rec_prob,
                           cplx* __restrict__ z, Strided zs, const cplx* __restrict__ tw, int logLmax,
-                          double* npart) {
+                          double* npart, UniPre upd) {
   extern __shared__ cplx sm[];  // FFT buffer + (power-of-two N2) N2/2 staged twiddles
   __shared__ double ered[UNI_MAX_WARPS * 32];
+  if (upd.st) {  // CGLS update of a vector this CTA owns (its input when mode 2)
+    uni_pre_apply(upd, blockIdx.x, blockIdx.y);
+    __syncthreads();
+  }
   const cplx* twf = tw;
   if (P.logN2 >= 0) {  // visible after the body's first barrier
     stage_twiddles(sm + fpad_len(P.N2), tw, P.logN2, logLmax);

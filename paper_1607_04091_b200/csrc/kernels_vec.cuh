@@ -17,7 +17,41 @@ struct CgState {
   int converged;
   int hist_len;
   double pend_alpha;  // 1D NFFT fused q-step: alpha of the r update the next interpolation applies
+  double pend_beta;   // tensor route: p = s + pend_beta p still to apply (pend_p) by the next x-pass
+  int pend_p;
 };
+
+// a vector update one CTA of a tensor-route pass applies to the vector it owns
+// before its transform (the CGLS axpys without launches of their own):
+//   mode 1: v = w + pend_beta v (if pend_p)     -- p = s + beta p, deferred
+//   mode 2: v = v - alpha w     (if active)     -- r -= alpha q
+//   mode 3: v = v + alpha w     (if active)     -- x += alpha p
+struct UniPre {
+  const CgState* st;
+  int mode;
+  cplx* v;
+  const cplx* w;
+  int64_t sprob, svec, selem;  // strides of v and w (same layout)
+  int len;
+};
+__device__ __forceinline__ void uni_pre_apply(const UniPre& u, int vec, int prob) {
+  const CgState& c = u.st[prob];
+  double a;
+  if (u.mode == 1) {
+    if (!c.pend_p) return;
+    a = c.pend_beta;
+  } else {
+    if (!c.active) return;
+    a = u.mode == 2 ? -c.alpha : c.alpha;
+  }
+  cplx* v = u.v + prob * u.sprob + vec * u.svec;
+  const cplx* w = u.w + prob * u.sprob + vec * u.svec;
+  for (int i = threadIdx.x; i < u.len; i += blockDim.x) {
+    const cplx vv = v[i * u.selem], ww = w[i * u.selem];
+    v[i * u.selem] = u.mode == 1 ? mk(fma(a, vv.x, ww.x), fma(a, vv.y, ww.y))
+                                 : mk(fma(a, ww.x, vv.x), fma(a, ww.y, vv.y));
+  }
+}
 
 // out[prob] = sum |v|^2 over len entries (one block per problem; fixed order)
 __global__ void k_norm2(const cplx* __restrict__ v, int64_t len, double* __restrict__ out) {
@@ -80,7 +114,8 @@ __global__ void k_cg_ref(CgState* st, const double* __restrict__ n2, int B) {
   if (b >= B) return;
   CgState s;
   s.ref = sqrt(n2[b]);
-  s.gamma = s.gamma_new = s.qq = s.alpha = s.beta = s.pend_alpha = 0.0;
+  s.gamma = s.gamma_new = s.qq = s.alpha = s.beta = s.pend_alpha = s.pend_beta = 0.0;
+  s.pend_p = 0;
   s.iterations = 0;
   s.converged = 0;
   s.hist_len = 0;
@@ -195,8 +230,8 @@ __global__ void k_fold_alpha_w(const double* __restrict__ part, int chunks, CgSt
   const double qq = fold_warp(part + (int64_t)b * chunks, chunks);
   if (threadIdx.x) return;
   CgState s = st[b];
-  if (!s.active) return;
-  cg_alpha_dev(s, qq);
+  s.pend_p = 0;  // the x-pass of this iteration has applied it
+  if (s.active) cg_alpha_dev(s, qq);
   st[b] = s;
 }
 __global__ void k_fold_beta_w(const double* __restrict__ part, int chunks, CgState* st, double tol, double* hist,
@@ -207,6 +242,8 @@ __global__ void k_fold_beta_w(const double* __restrict__ part, int chunks, CgSta
   CgState s = st[b];
   if (!s.active) return;
   cg_beta_dev(s, gn, tol, hist, hist_stride, b);
+  s.pend_p = s.active;  // p = s + beta p, applied by the next x-pass (k_uni_fwd UniPre mode 1)
+  s.pend_beta = s.beta;
   st[b] = s;
 }
 
