@@ -109,7 +109,13 @@ int gs_solve_least_squares(gs_op* op, const double* raw_samples, int64_t samples
  * gs_solve_least_squares): begin = preamble (solver.cpp:28-68, 2 adjoints +
  * 1 forward), step = `iterations` loop bodies (solver.cpp:70-88) enqueued on
  * `stream` with no host synchronisation (converged problems freeze on the
- * device), active = host poll of the device flags, finish = x / stats / history. */
+ * device), active = host poll of the device flags, finish = x / stats / history.
+ * `*out` is write-only (a new session; NULL on failure).  history_capacity
+ * >= 1 is the row stride of `history` in gs_cgls_finish; iterations past it
+ * overwrite the last slot.
+ * Threading: calls on one handle are serialised by the handle, and a handle's
+ * workspaces are shared, so use one handle from one stream at a time (one
+ * handle per concurrent stream; handles are independent). */
 typedef struct gs_cgls_session gs_cgls_session;
 int gs_cgls_begin(gs_op* op, const double* raw_samples, int64_t samples_len, const double* x0,
                   double tolerance, int history_capacity, void* stream, gs_cgls_session** out);

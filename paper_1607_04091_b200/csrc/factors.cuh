@@ -6,7 +6,6 @@
 #include "gs_common.cuh"
 
 #define GS_MAXP 8
-#define GS_MAXDEPTH 64
 
 // Family constants passed by value (kernel parameter bank).
 struct FamDev {
@@ -54,12 +53,13 @@ __device__ cplx d_fourier_scaling(const FamDev& f, double xi, int terms) {
 }
 
 // Edge transforms by the depth-level two-scale recursion (fourier.cpp:85-120).
+// phihat(xi / 2^(l+1)) is carried down the Horner loop instead of stored per
+// level (same products in the same order as fourier.cpp:92-98), so any
+// depth >= 1 is accepted.
 __device__ void d_fourier_boundary(const FamDev& f, int side, double xi, int depth, int terms,
                                    cplx* out /* p */) {
   const int p = f.p;
-  cplx phihat[GS_MAXDEPTH + 1];
-  phihat[depth] = d_fourier_scaling(f, ldexp(xi, -depth), terms);
-  for (int l = depth - 1; l >= 1; --l) phihat[l] = cmul(d_transfer(f, ldexp(xi, -(l + 1))), phihat[l + 1]);
+  cplx amp = d_fourier_scaling(f, ldexp(xi, -depth), terms);  // phihat[depth]
   cplx acc[GS_MAXP], v2[2 * GS_MAXP - 1], nxt[GS_MAXP];
   for (int i = 0; i < p; ++i) acc[i] = mk(f.vz[side][i], 0.0);
   const double* U = f.U[side];
@@ -68,7 +68,6 @@ __device__ void d_fourier_boundary(const FamDev& f, int side, double xi, int dep
     double arg = ldexp(xi, -(l + 1));
     cplx step = side == 0 ? polar1(-GS_TWO_PI * arg) : polar1(GS_TWO_PI * arg);
     cplx phase = side == 0 ? polar1((-GS_TWO_PI * arg) * (double)p) : polar1((GS_TWO_PI * arg) * (double)(p + 1));
-    cplx amp = phihat[l + 1];
     for (int m = 0; m < 2 * p - 1; ++m) {
       v2[m] = cmul(amp, phase);
       phase = cmul(phase, step);
@@ -80,6 +79,7 @@ __device__ void d_fourier_boundary(const FamDev& f, int side, double xi, int dep
       nxt[i] = cadd(s, t);
     }
     for (int i = 0; i < p; ++i) acc[i] = nxt[i];
+    if (l >= 1) amp = cmul(d_transfer(f, arg), amp);  // phihat[l] = m0(xi/2^(l+1)) phihat[l+1]
   }
   for (int i = 0; i < p; ++i) out[i] = acc[i];
 }

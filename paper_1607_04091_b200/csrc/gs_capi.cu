@@ -12,6 +12,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/gs_b200.h"
@@ -249,9 +250,15 @@ void allow_big_smem(K kernel) {
   CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax - (int)a.sharedSizeBytes));
 }
 
+// cudaFuncSetAttribute applies to the current device only: once per device
+// ordinal, serialised across threads (call after cudaSetDevice)
 void set_smem_attrs() {
-  static bool done = false;
-  if (done) return;
+  static std::mutex m;
+  static std::vector<char> done_dev;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(m);
+  if (dev < (int)done_dev.size() && done_dev[dev]) return;
   allow_big_smem(k_uni_fwd);
   allow_big_smem(k_uni_adj);
   allow_big_smem(k_uni_cgls_iter);
@@ -284,7 +291,8 @@ void set_smem_attrs() {
   allow_big_smem(k2f_spread_mma<2>);
   allow_big_smem(k2f_spread_mma<3>);
   allow_big_smem(k2f_spread_mma<4>);
-  done = true;
+  if ((int)done_dev.size() <= dev) done_dev.resize(dev + 1, 0);
+  done_dev[dev] = 1;
 }
 
 void make_twiddles(gs_op* op, long long Lmax, cudaStream_t st) {
@@ -432,10 +440,14 @@ gs_op* create(const gs_op_desc* dsc) {
   op->J = d.J;
   op->B = d.batch <= 0 ? 1 : d.batch;
   op->M = d.M;
-  op->depth = d.boundary_depth > 0 ? d.boundary_depth : 30;
-  op->terms = d.product_terms > 0 ? d.product_terms : 48;
+  op->depth = d.boundary_depth;
+  op->terms = d.product_terms;
   if (d.family_p < 1 || d.family_p > 8) fail(GS_ERR_DOMAIN, "unsupported family");
   op->p = d.family_p;
+  if (op->p >= 2) {  // checked per point by the reference (fourier.cpp:36, 87); haar evaluates neither
+    if (d.product_terms < 1) fail(GS_ERR_DOMAIN, "fourier_scaling: terms must be >= 1");
+    if (d.boundary_depth < 1) fail(GS_ERR_DOMAIN, "fourier_boundary: depth must be >= 1");
+  }
   op->edges = op->p >= 2;
   op->Rr = 1 + (op->edges ? 2 * op->p : 0);
   // freq2wave.cpp:93-102
@@ -499,6 +511,13 @@ gs_op* create(const gs_op_desc* dsc) {
       else if (b == 0) eps0 = e;
       else if (e != eps0) uni = false;
     }
+    if (uni) {
+      try {  // DFT lengths this build's uniform kernels cannot hold take the NFFT route
+        op->up = make_uni(op.get(), M, eps0);
+      } catch (const GsError&) {
+        uni = false;
+      }
+    }
     op->route = uni ? GS_ROUTE_UNIFORM_1D : GS_ROUTE_NFFT_1D;
     op->uniform_eps = uni ? eps0 : 0.0;
   } else {
@@ -546,7 +565,6 @@ gs_op* create(const gs_op_desc* dsc) {
   // ---- per-route construction, all per-point work on the device
   DBuf<double> d_xi_x, d_xi_y, d_sw;
   if (op->route == GS_ROUTE_UNIFORM_1D) {
-    op->up = make_uni(op.get(), M, op->uniform_eps);
     attach_phases(op->up, op->ph_u, st);
     make_twiddles(op.get(), op->up.N2, st);
     d_xi_x.upload(xi_x.data(), total, st);
@@ -1468,18 +1486,21 @@ int gs_apply_adjoint(gs_op* op, const double* samples, int64_t samples_len, doub
 }
 
 // ---- CGLS sessions: begin (preamble), step (n iterations, no host sync), finish
-int gs_cgls_begin(gs_op* op, const double* raw_samples, int64_t samples_len, const double* x0, double tolerance,
-                  int history_capacity, void* stream, gs_cgls_session** out) {
+namespace {
+// preamble of a solve into a new session, or into `reuse` (a session of this
+// op whose device buffers are recycled; consumed either way)
+int cgls_begin_into(gs_op* op, gs_cgls_session* reuse, const double* raw_samples, int64_t samples_len,
+                    const double* x0, double tolerance, int history_capacity, void* stream, gs_cgls_session** out) {
+  std::unique_ptr<gs_cgls_session> R(reuse);
   return guard_call([&] {
     if (!op || !raw_samples || !out) fail(GS_ERR_USAGE, "null argument");
+    *out = nullptr;
     if (samples_len != op->M * op->B) fail(GS_ERR_SHAPE, "sample vector length mismatch");
     if (!(tolerance > 0)) fail(GS_ERR_DOMAIN, "tolerance must be positive");
     std::lock_guard<std::mutex> lk(op->mu);
     CK(cudaSetDevice(op->device));
     cudaStream_t st = (cudaStream_t)stream;
-    // *out may carry an earlier session of this op: its device buffers are reused
-    std::unique_ptr<gs_cgls_session> S((*out && (*out)->s.op == op) ? *out : new gs_cgls_session);
-    *out = nullptr;
+    std::unique_ptr<gs_cgls_session> S((R && R->s.op == op) ? R.release() : new gs_cgls_session);
     const int64_t TM = op->M * op->B, TN = op->Nc * op->B;
     const cplx* b = (const cplx*)raw_samples;
     if (!is_device_ptr(raw_samples)) {
@@ -1491,9 +1512,15 @@ int gs_cgls_begin(gs_op* op, const double* raw_samples, int64_t samples_len, con
       op->stage_b.upload((const cplx*)x0, TN, st);
       xx = op->stage_b.p;
     }
-    session_begin(S->s, op, b, true, xx, tolerance, std::max(2, history_capacity), st);
+    session_begin(S->s, op, b, true, xx, tolerance, std::max(1, history_capacity), st);
     *out = S.release();
   });
+}
+}  // namespace
+
+int gs_cgls_begin(gs_op* op, const double* raw_samples, int64_t samples_len, const double* x0, double tolerance,
+                  int history_capacity, void* stream, gs_cgls_session** out) {
+  return cgls_begin_into(op, nullptr, raw_samples, samples_len, x0, tolerance, history_capacity, stream, out);
 }
 
 int gs_cgls_step(gs_cgls_session* s, int iterations, void* stream) {
@@ -1556,14 +1583,15 @@ int gs_solve_least_squares(gs_op* op, const double* raw_samples, int64_t samples
     return GS_ERR_USAGE;
   }
   // the op keeps its last solve workspace, so repeated solves allocate nothing
-  gs_cgls_session* s = op->solve_cache;
-  op->solve_cache = nullptr;
-  const int max_iter = max_iterations > 0 ? max_iterations : (int)std::min<int64_t>(INT32_MAX / 2, 2 * op->Nc);
-  int rc = gs_cgls_begin(op, raw_samples, samples_len, x0, tolerance, max_iter + 1, stream, &s);
-  if (rc) {
-    gs_cgls_destroy(s);
-    return rc;
+  gs_cgls_session* cached = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(op->mu);
+    cached = std::exchange(op->solve_cache, nullptr);
   }
+  const int max_iter = max_iterations > 0 ? max_iterations : (int)std::min<int64_t>(INT32_MAX / 2, 2 * op->Nc);
+  gs_cgls_session* s = nullptr;
+  int rc = cgls_begin_into(op, cached, raw_samples, samples_len, x0, tolerance, max_iter + 1, stream, &s);
+  if (rc) return rc;
   int done = 0;
   int active = 1;
   rc = gs_cgls_active(s, stream, &active);
@@ -1576,7 +1604,11 @@ int gs_solve_least_squares(gs_op* op, const double* raw_samples, int64_t samples
     chunk = std::min(chunk * 2, 64);
   }
   if (rc == 0) rc = gs_cgls_finish(s, x_out, stats, history, stream);
-  op->solve_cache = s;
+  {
+    std::lock_guard<std::mutex> lk(op->mu);
+    std::swap(op->solve_cache, s);
+  }
+  gs_cgls_destroy(s);  // another thread's session parked meanwhile, if any
   return rc;
 }
 

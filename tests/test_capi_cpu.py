@@ -49,6 +49,8 @@ def test_sass_is_sm_100a():
     (dict(bandwidth=2.0, coords=[0.0, 3.0]), "DomainError"),
     (dict(weights=[1.0, -1.0]), "DomainError"),
     (dict(weights=[1.0]), "ShapeError"),
+    (dict(J=3, family="db2", boundary_depth=0), "DomainError"),   # fourier.cpp:87
+    (dict(J=3, family="db2", product_terms=0), "DomainError"),    # fourier.cpp:36
 ])
 def test_construction_validation_matches_reference(kw, cls):
     gs, _ = _lib()
@@ -75,3 +77,14 @@ def test_no_gpu_fails_loudly():
     gs, _ = _lib()
     with pytest.raises(gs.CudaError):
         gs.freq2wave(gs.SamplingSet(1, np.array([0.0, -4.0])), "haar", 3)
+
+
+def test_haar_ignores_depth_and_terms():
+    """haar evaluates neither the product nor the recursion (fourier.cpp:35),
+    so depth / terms <= 0 pass validation and only the missing GPU fails."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    gs, _ = _lib()
+    with pytest.raises(gs.CudaError):
+        gs.freq2wave(gs.SamplingSet(1, np.array([0.0, -4.0])), "haar", 3, boundary_depth=0, product_terms=0)
