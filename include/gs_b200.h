@@ -38,6 +38,7 @@ extern "C" {
 #define GS_ROUTE_NFFT_1D 2     /* Kaiser-Bessel gridding NFFT, 1D                   */
 #define GS_ROUTE_NFFT_2D 3     /* 2D KB-NFFT + 4p side NFFTs + corners (9 blocks)   */
 #define GS_ROUTE_TENSOR_2D 4   /* exact: T = T_x (x) T_y on a uniform tensor grid   */
+#define GS_ROUTE_NDFT_1D 5     /* exact: direct NDFT core (ndft_forward, a14), 1D   */
 
 typedef struct gs_op gs_op; /* opaque; replaces gs::Freq2WaveOp (freq2wave.hpp:32-55) */
 
@@ -61,6 +62,8 @@ typedef struct {
   int allow_uniform_fast_path; /* default 1                                        */
   int allow_tensor_route;  /* default 1: exact tensor route for uniform 2D grids  */
   int device;              /* CUDA ordinal                                         */
+  int exact_ndft;          /* default 0; 1: 1D non-uniform samples use the direct  */
+                           /* NDFT (exact, O(M N), FP64 pipe) instead of the KB NFFT */
 } gs_op_desc;
 
 typedef struct {
@@ -129,6 +132,16 @@ int gs_cgls_destroy(gs_cgls_session* s);
  * (Freq2WaveOp::Dx/Dy, Lx/Rx/Ly/Ry col-major M x p, freq2wave.hpp:42-43);
  * axis 0 = x, 1 = y.  L, R may be NULL (haar). */
 int gs_op_export_factors(gs_op* op, int b, int axis, double* D, double* L, double* R);
+
+/* gs::ndft_forward / gs::ndft_adjoint (nufft.cpp:74-132, nufft.hpp:25-33):
+ * the direct O(M prod N) transform on the device (blocked complex-exponential
+ * kernel).  N[0] (1D) or N[0], N[1] (2D) modes k = -N/2..N/2-1 per axis, last
+ * axis fastest; points [M][dim] scaled to [-1/2, 1/2) (DomainError outside);
+ * grid [prod N], samples [M].  Host or device pointers. */
+int gs_ndft_forward(int dim, const int* N, const double* points, int64_t M, const double* grid,
+                    int64_t grid_len, double* samples, void* stream);
+int gs_ndft_adjoint(int dim, const int* N, const double* points, int64_t M, const double* samples,
+                    int64_t samples_len, double* grid, void* stream);
 
 /* Per-kernel device time of one T + T* pair (no reference counterpart; the
  * measurement hook bench.py uses for the roofline): `reps` pairs on zeroed

@@ -20,8 +20,8 @@
 //   dyadic.cpp:14-231     integer values, dyadic cascades (interior + edge),
 //                         weval_1d / weval_2d (front-end row SURVEY 8(f)4)
 // Third-party stand-ins: FFTW (unnormalised c2c, FORWARD = -1) is replaced by
-// our own radix-2 FFT (direct DFT for non power-of-two lengths); Eigen by
-// plain loops.  Results agree with the reference to roundoff.
+// our own table-twiddle FFT (radix-2; mixed-radix Cooley-Tukey for other
+// lengths); Eigen by plain loops.  Results agree with the reference to roundoff.
 //
 // Parity pinning: tests/test_oracle_known_answers.py checks this file against
 // every known-answer relation the reference's own tests hold for this path
@@ -206,19 +206,54 @@ std::vector<cd> fourier_boundary(const Family& fam, const Boundary& ctx, double 
 
 // ---------------------------------------------------------------- FFT (FFTW stand-in)
 // Unnormalised c2c transform, sign -1 = FFTW_FORWARD, +1 = FFTW_BACKWARD.
+// Twiddles come from a per-(length, sign) table (polar once per entry, as a
+// planned FFTW does), so the CPU timing is not inflated by sincos per
+// butterfly.  Powers of two: iterative radix-2; other lengths: recursive
+// mixed-radix Cooley-Tukey over the smallest prime factor (direct DFT for a
+// prime length), the same O(n log n) class FFTW's planner reaches.
+const cvec& twiddle_table(int n, int sign) {
+    thread_local std::vector<std::pair<long long, cvec>> cache;
+    const long long key = 2LL * n + (sign > 0);
+    for (auto& e : cache)
+        if (e.first == key) return e.second;
+    cvec t(n);
+    for (int k = 0; k < n; ++k) t[k] = std::polar(1.0, sign * kTwoPi * static_cast<double>(k) / n);
+    cache.emplace_back(key, std::move(t));
+    return cache.back().second;
+}
+
+void fft_mixed(const cd* in, size_t stride, cd* out, int n, const cd* tw, int twstep, cd* tmp) {
+    if (n == 1) {
+        out[0] = in[0];
+        return;
+    }
+    int p = n;
+    for (int f = 2; f * f <= n; ++f)
+        if (n % f == 0) {
+            p = f;
+            break;
+        }
+    const int m = n / p;
+    for (int r = 0; r < p; ++r) fft_mixed(in + r * stride, stride * p, out + r * m, m, tw, twstep * p, tmp);
+    // X[k + q m] = sum_r w_n^{r (k + q m)} Y_r[k], w_n^j = tw[j * twstep]
+    for (int k = 0; k < m; ++k) {
+        for (int q = 0; q < p; ++q) {
+            const int kk = k + q * m;
+            cd acc = out[k];
+            for (int r = 1; r < p; ++r)
+                acc += out[r * m + k] * tw[(static_cast<long long>(r) * kk % n) * twstep];
+            tmp[kk] = acc;
+        }
+    }
+    for (int j = 0; j < n; ++j) out[j] = tmp[j];
+}
+
 void fft_inplace(cd* a, int n, int sign) {
     if (n <= 1) return;
-    if ((n & (n - 1)) != 0) {  // direct DFT for non powers of two
-        cvec out(n);
-        for (int k = 0; k < n; ++k) {
-            cd acc = 0.0;
-            for (int j = 0; j < n; ++j) {
-                long long jk = (static_cast<long long>(j) * k) % n;
-                acc += a[j] * std::polar(1.0, sign * kTwoPi * static_cast<double>(jk) / n);
-            }
-            out[k] = acc;
-        }
-        std::copy(out.begin(), out.end(), a);
+    const cvec& tw = twiddle_table(n, sign);
+    if ((n & (n - 1)) != 0) {
+        cvec in(a, a + n), tmp(n);
+        fft_mixed(in.data(), 1, a, n, tw.data(), 1, tmp.data());
         return;
     }
     for (int i = 1, j = 0; i < n; ++i) {
@@ -228,13 +263,10 @@ void fft_inplace(cd* a, int n, int sign) {
         if (i < j) std::swap(a[i], a[j]);
     }
     for (int len = 2; len <= n; len <<= 1) {
-        int half = len / 2;
-        int stride = n / len;
+        const int half = len / 2, stride = n / len;
         for (int i = 0; i < n; i += len) {
             for (int k = 0; k < half; ++k) {
-                long long t = static_cast<long long>(k) * stride;
-                cd w = std::polar(1.0, sign * kTwoPi * static_cast<double>(t) / n);
-                cd u = a[i + k], v = a[i + k + half] * w;
+                cd u = a[i + k], v = a[i + k + half] * tw[static_cast<size_t>(k) * stride];
                 a[i + k] = u + v;
                 a[i + k + half] = u - v;
             }

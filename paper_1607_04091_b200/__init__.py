@@ -28,7 +28,7 @@ __all__ = [
     "Error", "UsageError", "FileFormatError", "ShapeError", "DomainError", "NumericalError", "CudaError",
     "SamplingSet", "Freq2WaveOptions", "Freq2WaveOp", "SolveOptions", "SolveStats",
     "freq2wave", "apply_forward", "apply_adjoint", "solve_least_squares", "CglsSession",
-    "family_p", "ROUTES", "lib_path", "load_library",
+    "ndft_forward", "ndft_adjoint", "family_p", "ROUTES", "lib_path", "load_library",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -73,14 +73,15 @@ class CudaError(Error):
 
 
 _ERRS = {2: UsageError, 3: FileFormatError, 4: ShapeError, 5: DomainError, 6: NumericalError, 7: CudaError}
-ROUTES = {1: "uniform_1d", 2: "nfft_1d", 3: "nfft_2d", 4: "tensor_2d"}
+ROUTES = {1: "uniform_1d", 2: "nfft_1d", 3: "nfft_2d", 4: "tensor_2d", 5: "ndft_1d"}
 
 
 class _Desc(C.Structure):
     _fields_ = [("dim", C.c_int), ("family_p", C.c_int), ("J", C.c_int), ("M", C.c_int64), ("batch", C.c_int),
                 ("coords", C.POINTER(C.c_double)), ("weights", C.POINTER(C.c_double)), ("bandwidth", C.c_double),
                 ("sigma", C.c_double), ("w", C.c_int), ("boundary_depth", C.c_int), ("product_terms", C.c_int),
-                ("allow_uniform_fast_path", C.c_int), ("allow_tensor_route", C.c_int), ("device", C.c_int)]
+                ("allow_uniform_fast_path", C.c_int), ("allow_tensor_route", C.c_int), ("device", C.c_int),
+                ("exact_ndft", C.c_int)]
 
 
 class _Info(C.Structure):
@@ -116,6 +117,8 @@ def load_library():
     L.gs_cgls_finish.argtypes = [vp, vp, C.POINTER(_Stats), dp, vp]
     L.gs_cgls_destroy.argtypes = [vp]
     L.gs_op_export_factors.argtypes = [vp, C.c_int, C.c_int, dp, dp, dp]
+    L.gs_ndft_forward.argtypes = [C.c_int, C.POINTER(C.c_int), vp, C.c_int64, vp, C.c_int64, vp, vp]
+    L.gs_ndft_adjoint.argtypes = [C.c_int, C.POINTER(C.c_int), vp, C.c_int64, vp, C.c_int64, vp, vp]
     _lib = L
     return L
 
@@ -172,6 +175,7 @@ class Freq2WaveOptions:
     product_terms: int = 48
     allow_uniform_fast_path: bool = True
     allow_tensor_route: bool = True
+    exact_ndft: bool = False  # 1D: direct NDFT core instead of the KB NFFT (GS_ROUTE_NDFT_1D)
 
 
 @dataclass
@@ -317,6 +321,7 @@ def freq2wave(samples, family, J, options: Optional[Freq2WaveOptions] = None, *,
     d.product_terms = opt.product_terms
     d.allow_uniform_fast_path = int(bool(opt.allow_uniform_fast_path))
     d.allow_tensor_route = int(bool(opt.allow_tensor_route))
+    d.exact_ndft = int(bool(opt.exact_ndft))
     d.device = device
     h = C.c_void_p()
     _check(load_library().gs_op_create(C.byref(d), C.byref(h)))
@@ -346,6 +351,29 @@ def apply_adjoint(op: Freq2WaveOp, samples, stream=None):
     q = out.data_ptr() if _is_torch(out) else out.ctypes.data
     _check(load_library().gs_apply_adjoint(op.handle, p, n, q, _stream_ptr(stream)))
     return out
+
+
+def _ndft(adjoint, dim, N, points, data, stream=None):
+    pts = points if _is_torch(points) else np.ascontiguousarray(points, dtype=np.float64).ravel()
+    pp = pts.data_ptr() if _is_torch(pts) else pts.ctypes.data
+    M = (pts.numel() if _is_torch(pts) else pts.size) // dim
+    Nv = (C.c_int * 2)(int(N[0]), int(N[1]) if dim == 2 else 0)
+    q, n, keep = _ptr_len(data)
+    out = _out_like(keep, M if not adjoint else int(N[0]) * (int(N[1]) if dim == 2 else 1))
+    o = out.data_ptr() if _is_torch(out) else out.ctypes.data
+    fn = load_library().gs_ndft_adjoint if adjoint else load_library().gs_ndft_forward
+    _check(fn(int(dim), Nv, pp, M, q, n, o, _stream_ptr(stream)))
+    return out
+
+
+def ndft_forward(dim, N, points, grid, stream=None):
+    """gs::ndft_forward (nufft.cpp:74-101): y_m = sum_k x_k exp(-2 pi i k.xi_m), on the device."""
+    return _ndft(False, dim, N, points, grid, stream)
+
+
+def ndft_adjoint(dim, N, points, samples, stream=None):
+    """gs::ndft_adjoint (nufft.cpp:103-132): z_k = sum_m y_m exp(+2 pi i k.xi_m), on the device."""
+    return _ndft(True, dim, N, points, samples, stream)
 
 
 def solve_least_squares(op: Freq2WaveOp, samples, options: Optional[SolveOptions] = None, stream=None, **kw):

@@ -19,66 +19,17 @@
 #include "factors.cuh"
 #include "family_data.h"
 #include "gs_common.cuh"
+#include "host_common.cuh"
 #include "kernels_nfft.cuh"
 #include "kernels_nfft2d_fast.cuh"
 #include "kernels_uniform.cuh"
 #include "kernels_vec.cuh"
 #include "kernels_cgls_fused.cuh"
+#include "ndft.h"
+
+using namespace gsb;
 
 namespace {
-
-thread_local std::string g_err;
-
-struct GsError {
-  int code;
-  std::string msg;
-};
-[[noreturn]] void fail(int code, const std::string& m) { throw GsError{code, m}; }
-
-#define CK(call)                                                                              \
-  do {                                                                                        \
-    cudaError_t e_ = (call);                                                                  \
-    if (e_ != cudaSuccess) fail(GS_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
-  } while (0)
-#define CKL()                                                                                 \
-  do {                                                                                        \
-    cudaError_t e_ = cudaGetLastError();                                                      \
-    if (e_ != cudaSuccess) fail(GS_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
-  } while (0)
-
-template <class T>
-struct DBuf {
-  T* p = nullptr;
-  size_t n = 0;
-  DBuf() = default;
-  DBuf(const DBuf&) = delete;
-  DBuf& operator=(const DBuf&) = delete;
-  ~DBuf() {
-    if (p) cudaFree(p);
-  }
-  void alloc(size_t count) {
-    if (count <= n && p) return;
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = 0;
-    if (count == 0) return;
-    CK(cudaMalloc(&p, count * sizeof(T)));
-    n = count;
-  }
-  void upload(const T* h, size_t count, cudaStream_t st) {
-    alloc(count);
-    if (count) CK(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, st));
-  }
-  size_t bytes() const { return n * sizeof(T); }
-};
-
-inline int ilog2(long long v) {
-  int l = 0;
-  while ((1LL << l) < v) ++l;
-  return l;
-}
-inline bool is_pow2(long long v) { return v > 0 && (v & (v - 1)) == 0; }
-inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
 // ------------------------------------------------------------------ host math
 double wrap_half_open(double z) {  // freq2wave.cpp:15-19
@@ -227,6 +178,8 @@ struct gs_op {
   // workspace
   DBuf<cplx> G, lines, TB, TL, TLF, TC, TCF, W;
   DBuf<cplx> EP;  // 1D route: per-CTA edge-sum partials of k_n1_spread
+  DBuf<double> nd_pts;  // NDFT_1D route: wrapped scaled points (caller order)
+  DBuf<cplx> nd_part;   // NDFT_1D route: split partial sums
   DBuf<cplx> stage_a, stage_b;
   gs_cgls_session* solve_cache = nullptr;  // workspace of the last gs_solve_least_squares
   std::mutex mu;
@@ -235,7 +188,7 @@ struct gs_op {
     return tw.bytes() + rec_u.bytes() + rec_ax.bytes() + rec_ay.bytes() + deconv.bytes() + perm.bytes() +
            base_x.bytes() + base_y.bytes() + bins.bytes() + wts_x.bytes() + wts_y.bytes() + rec_x.bytes() +
            rec_y.bytes() + sqrtw.bytes() + G.bytes() + lines.bytes() + TB.bytes() + TL.bytes() + TLF.bytes() + TC.bytes() + TCF.bytes() +
-           W.bytes() + stage_a.bytes() + stage_b.bytes();
+           W.bytes() + stage_a.bytes() + stage_b.bytes() + nd_pts.bytes() + nd_part.bytes();
   }
 };
 
@@ -518,7 +471,7 @@ gs_op* create(const gs_op_desc* dsc) {
         uni = false;
       }
     }
-    op->route = uni ? GS_ROUTE_UNIFORM_1D : GS_ROUTE_NFFT_1D;
+    op->route = uni ? GS_ROUTE_UNIFORM_1D : (d.exact_ndft ? GS_ROUTE_NDFT_1D : GS_ROUTE_NFFT_1D);
     op->uniform_eps = uni ? eps0 : 0.0;
   } else {
     bool ten = allow_u && d.allow_tensor_route != 0;
@@ -571,6 +524,19 @@ gs_op* create(const gs_op_desc* dsc) {
     if (op->weighted) op->sqrtw.upload(sw.data(), total, st);
     op->rec_u.alloc(total * op->Rr);
     build_factors(op.get(), d_xi_x.p, op->weighted ? op->sqrtw.p : nullptr, total, op->rec_u.p, st);
+  } else if (op->route == GS_ROUTE_NDFT_1D) {
+    // the reference builds plan_x here (freq2wave.cpp:175-176): same option checks
+    if ((d.sigma > 0 ? d.sigma : 2.0) < 1.25) fail(GS_ERR_DOMAIN, "oversampling factor must be >= 1.25");
+    if ((d.w > 0 ? d.w : 6) < 2) fail(GS_ERR_DOMAIN, "kernel half-width must be >= 2");
+    // direct NDFT on the wrapped scaled points the plan would get (freq2wave.cpp:79-84, 176)
+    std::vector<double> zw(total);
+    for (int64_t i = 0; i < total; ++i) zw[i] = wrap_half_open(std::ldexp(xi_x[i], -d.J));
+    op->nd_pts.upload(zw.data(), total, st);
+    d_xi_x.upload(xi_x.data(), total, st);
+    if (op->weighted) op->sqrtw.upload(sw.data(), total, st);
+    op->rec_x.alloc(total * op->Rr);
+    build_factors(op.get(), d_xi_x.p, op->weighted ? op->sqrtw.p : nullptr, total, op->rec_x.p, st);
+    CK(cudaStreamSynchronize(st));
   } else if (op->route == GS_ROUTE_TENSOR_2D) {
     const int64_t Ma = op->Ma, Mb = op->Mb;
     std::vector<double> ax(B * Ma), ay(B * Mb);
@@ -809,13 +775,6 @@ gs_op* create(const gs_op_desc* dsc) {
 // When armed by gs_profile_pair, every launch in forward_dev / adjoint_dev is
 // followed by an event on the launching stream; consecutive events bracket
 // exactly one kernel.
-struct Prof {
-  bool on = false;
-  std::vector<cudaEvent_t> ev;
-  std::vector<std::string> names;
-};
-Prof g_prof;
-std::atomic<long long> g_launches{0};  // kernels this library has launched (gs_launch_count)
 // 2D spreading variant: FP64 tensor cores (default) or the lane-per-column
 // DFMA kernel (GS_B200_SPREAD=dfma, for A/B measurements)
 bool interp_mma() {
@@ -854,15 +813,6 @@ bool spread_mma() {
   return on;
 }
 
-void pmark(const char* name, cudaStream_t st) {
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  if (!g_prof.on) return;
-  cudaEvent_t e;
-  CK(cudaEventCreate(&e));
-  CK(cudaEventRecord(e, st));
-  g_prof.ev.push_back(e);
-  g_prof.names.push_back(name);
-}
 
 // ------------------------------------------------------------------ applies
 // x, y are device pointers; perm_io: samples in the caller's order (true) or
@@ -895,6 +845,12 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
           op->upy, op->W.p, Strided{Ma * n, n, 1}, op->rec_ay.p, Mb * op->Rr, y, Strided{op->M, Mb, 1},
           op->weighted ? op->sqrtw.p : nullptr, op->M, op->tw.p, op->logLmax, npart, UniPre{});
       pmark("k_uni_fwd[y-pass]", st);
+      break;
+    }
+    case GS_ROUTE_NDFT_1D: {
+      const NdftShape s{1, 1, (int)op->n, op->M, B};
+      const int e = op->edges ? op->p : 0;
+      ndft_forward_launch(s, op->nd_pts.p, x, y, e, (int)op->n - e, op->rec_x.p, op->p, op->edges, op->nd_part, st);
       break;
     }
     case GS_ROUTE_NFFT_1D: {
@@ -1003,6 +959,12 @@ bool adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
       pmark("k_uni_adj[x-pass]", st);
       break;
     }
+    case GS_ROUTE_NDFT_1D: {
+      const NdftShape s{1, 1, (int)op->n, op->M, B};
+      const int e = op->edges ? op->p : 0;
+      ndft_adjoint_launch(s, op->nd_pts.p, y, z, e, (int)op->n - e, op->rec_x.p, op->p, op->edges, op->nd_part, st);
+      break;
+    }
     case GS_ROUTE_NFFT_1D: {
       const NfP& P = op->np;
       const int nparts = (P.n_ov + N1_SPREAD_CELLS - 1) / N1_SPREAD_CELLS;
@@ -1088,31 +1050,6 @@ bool adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
   }
   CKL();
   return fused_sstep;
-}
-
-bool is_device_ptr(const void* p) {
-  cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
-}
-
-int guard_call(const std::function<void()>& f) {
-  try {
-    f();
-    return GS_OK;
-  } catch (const GsError& e) {
-    g_err = e.msg;
-    return e.code;
-  } catch (const std::bad_alloc&) {
-    g_err = "host out of memory";
-    return GS_ERR_CUDA;
-  } catch (const std::exception& e) {
-    g_err = e.what();
-    return GS_ERR_CUDA;
-  }
 }
 
 // ------------------------------------------------------------------ dyadic evaluation
@@ -1673,8 +1610,9 @@ int gs_op_export_factors(gs_op* op, int b, int axis, double* D, double* L, doubl
     const int64_t M = op->M;
     const int Rr = op->Rr, p = op->p;
     std::vector<cplx> recs(M * Rr);  // per point in the caller's order
-    if (op->route == GS_ROUTE_UNIFORM_1D) {
-      CK(cudaMemcpy(recs.data(), op->rec_u.p + b * M * Rr, M * Rr * sizeof(cplx), cudaMemcpyDeviceToHost));
+    if (op->route == GS_ROUTE_UNIFORM_1D || op->route == GS_ROUTE_NDFT_1D) {  // caller order already
+      CK(cudaMemcpy(recs.data(), (op->route == GS_ROUTE_UNIFORM_1D ? op->rec_u.p : op->rec_x.p) + b * M * Rr,
+                    M * Rr * sizeof(cplx), cudaMemcpyDeviceToHost));
     } else if (op->route == GS_ROUTE_TENSOR_2D) {
       const int64_t Ma = op->Ma, Mb = op->Mb;
       const int64_t Ml = axis == 0 ? Ma : Mb;

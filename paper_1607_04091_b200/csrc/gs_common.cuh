@@ -135,7 +135,7 @@ __device__ __forceinline__ int bitrev(int i, int logL) { return (int)(__brev((un
 
 // Direct DFT fallback (non power-of-two lengths, uniform route only):
 // out[k] = sum_j in[j] exp(sign 2 pi i jk / L).
-__device__ void block_dft(const cplx* in, cplx* out, int L, int sign) {
+__device__ inline void block_dft(const cplx* in, cplx* out, int L, int sign) {
   for (int k = threadIdx.x; k < L; k += blockDim.x) {
     cplx acc = mk(0, 0);
     for (int j = 0; j < L; ++j) {
@@ -155,7 +155,7 @@ __device__ __forceinline__ double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
-__device__ double block_sum(double v, double* scratch /* >= 32 doubles */) {
+__device__ inline double block_sum(double v, double* scratch /* >= 32 doubles */) {
   v = warp_sum(v);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   __syncthreads();

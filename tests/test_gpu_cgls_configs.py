@@ -1,0 +1,102 @@
+"""CGLS parity at every config's OWN size and iteration count (north star:
+"<= 1e-8 on the CGLS iterate after the same iteration count" on all five
+configs).  C1 and C2 are covered at full size in test_gpu_parity.py (the
+oracle runs in seconds there); C3, C4 and C5 are checked here against
+committed oracle iterates (tests/golden/cgls_*.npz, made by
+tools/gen_cgls_fixtures.py: the oracle needs ~4 min (C3), ~25 min (C4) and
+~5 min per C5 problem on one core, too slow for the suite).
+
+Each case rebuilds the config's inputs with the harness generators (bench.py
+problem_inputs; SHA-256 of coords / weights must equal the fixture's), forms
+b = T x_true + noise with the GPU operator (checked entrywise against the
+oracle's b on a sample), runs the config's iteration count with tol = 1e-300
+(test_solver.cpp:46 idiom, solver.cpp:70-88 loop) and compares the iterate.
+Every error is printed next to the oracle's own roundoff sensitivity (its
+iterate's movement under a 1e-15 relative data perturbation)."""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+from oracle import rel_error
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = os.path.join(ROOT, "tests", "golden")
+TOL_CGLS = 1e-8
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def load(name):
+    f = np.load(os.path.join(GOLD, name), allow_pickle=False)
+    return {k: f[k] for k in f.files}
+
+
+def inputs(workload, b):
+    import bench
+    dim, p, J, c, mu, bw, sig = bench.problem_inputs(workload, b, bench.ProductGen())
+    return dim, p, J, c, mu, bw, sig
+
+
+def data_vector(gs, workload, b, dim, p, J, c, bw, sig, fx):
+    import bench
+    op_u = gs.freq2wave(gs.SamplingSet(dim, c), p, J, bandwidth=bw)
+    x_true, noise = bench.coeffs_and_noise(b, op_u.cols(), op_u.rows(), sig)
+    data = gs.apply_forward(op_u, x_true) + noise
+    del op_u
+    idx = fx["b_idx"]
+    eb = np.max(np.abs(data[idx] - fx["b_val"])) / float(fx["b_norm"]) * np.sqrt(data.size)
+    assert eb <= 1e-12, eb  # T x_true on the GPU = the oracle's (relative, entrywise sample)
+    return data, eb
+
+
+@pytest.mark.parametrize("workload", ["c3", "c4"])
+def test_cgls_config_full(workload):
+    import paper_1607_04091_b200 as gs
+    fx = load(f"cgls_{workload}.npz")
+    dim, p, J, c, mu, bw, sig = inputs(workload, 0)
+    assert sha(c) == str(fx["coords_sha"])
+    if mu is not None:
+        assert sha(mu) == str(fx["weights_sha"])
+    data, eb = data_vector(gs, workload, 0, dim, p, J, c, bw, sig, fx)
+    op = gs.freq2wave(gs.SamplingSet(dim, c), p, J, bandwidth=bw, weights=mu)
+    K = int(fx["iters"])
+    x, st = gs.solve_least_squares(op, data, max_iterations=K, tolerance=1e-300)
+    assert st.iterations == K
+    e = rel_error(x, fx["x"])
+    h = np.asarray(st.history)
+    eh = np.max(np.abs(h - fx["history"]) / fx["history"])
+    print(f"{workload.upper()} ({op.route}, {K} it): iterate {e:.3e} (oracle sensitivity {float(fx['sens']):.2e}); "
+          f"b sample {eb:.1e}; history max rel dev {eh:.1e}")
+    assert e <= TOL_CGLS
+
+
+def test_cgls_c5_batched_subset():
+    """C5: problems 0, 85, 170, 255 of the 256 in ONE batched handle (the
+    bench's layout), 100 iterations each."""
+    import paper_1607_04091_b200 as gs
+    probs = [0, 85, 170, 255]
+    fxs = [load(f"cgls_c5_b{b}.npz") for b in probs]
+    sets, mus, datas = [], [], []
+    for b, fx in zip(probs, fxs):
+        dim, p, J, c, mu, bw, sig = inputs("c5", b)
+        assert sha(c) == str(fx["coords_sha"]) and sha(mu) == str(fx["weights_sha"])
+        data, _ = data_vector(gs, "c5", b, dim, p, J, c, bw, sig, fx)
+        sets.append(gs.SamplingSet(dim, c))
+        mus.append(mu)
+        datas.append(data)
+        # per-problem bandwidth K_b differs; the batched handle takes the largest
+    bw = max(float(np.max(np.abs(s.coords))) for s in sets)
+    op = gs.freq2wave(sets, p, J, bandwidth=bw, weights=np.concatenate(mus))
+    x, stats = gs.solve_least_squares(op, np.concatenate(datas), max_iterations=100, tolerance=1e-300)
+    n = op.cols()
+    for i, (b, fx) in enumerate(zip(probs, fxs)):
+        assert stats[i].iterations == 100
+        e = rel_error(x[i * n:(i + 1) * n], fx["x"])
+        print(f"C5 problem {b} (batched, {op.route}): iterate {e:.3e} (oracle sensitivity {float(fx['sens']):.2e})")
+        assert e <= TOL_CGLS
