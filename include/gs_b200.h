@@ -60,7 +60,7 @@ typedef struct {
   int boundary_depth;      /* default 30                                           */
   int product_terms;       /* default 48                                           */
   int allow_uniform_fast_path; /* default 1                                        */
-  int allow_tensor_route;  /* default 1: exact tensor route for uniform 2D grids  */
+  int allow_tensor_route;  /* default 0; 1: exact tensor route for uniform 2D grids */
   int device;              /* CUDA ordinal                                         */
   int exact_ndft;          /* default 0; 1: 1D non-uniform samples use the direct  */
                            /* NDFT (exact, O(M N), FP64 pipe) instead of the KB NFFT */
@@ -142,6 +142,31 @@ int gs_ndft_forward(int dim, const int* N, const double* points, int64_t M, cons
                     int64_t grid_len, double* samples, void* stream);
 int gs_ndft_adjoint(int dim, const int* N, const double* points, int64_t M, const double* samples,
                     int64_t samples_len, double* grid, void* stream);
+
+/* gs::NfftPlan / plan_nfft / nfft_forward / nfft_adjoint (nufft.hpp:36-70,
+ * nufft.cpp:138-365): the Kaiser-Bessel plan on the device at any dim 1/2,
+ * even N per axis, sigma >= 1.25 and half-width w >= 2 (general-length FFT
+ * engine), same validation and error classes as the reference constructor.
+ * points [M][dim] scaled to [-1/2, 1/2); grid [N0 (* N1)], last axis fastest. */
+typedef struct gs_nfft_plan gs_nfft_plan;
+int gs_nfft_plan_create(int dim, const int* N, const double* points, int64_t M, double sigma, int w,
+                        int device, gs_nfft_plan** out);
+int gs_nfft_plan_forward(gs_nfft_plan* plan, const double* grid, int64_t grid_len, double* samples,
+                         void* stream);
+int gs_nfft_plan_adjoint(gs_nfft_plan* plan, const double* samples, int64_t samples_len, double* grid,
+                         void* stream);
+/* dim, points_count, grid_size, oversampled_length(axis) for axis 0, 1 (NfftPlan accessors) */
+int gs_nfft_plan_info(const gs_nfft_plan* plan, int* dim, int64_t* points, int64_t* grid_size, int* n_over);
+int gs_nfft_plan_destroy(gs_nfft_plan* plan);
+
+/* gs::uniform_ndft_fft / uniform_ndft_adjoint_fft (nufft.cpp:383-459): the
+ * exact NDFT on xi_m = (eps/N)(m - M/2) through one zero-embedded DFT of any
+ * length q N / eps.  forward: x [x_len <= N] -> out [M]; adjoint: samples [M]
+ * -> out [N]. */
+int gs_uniform_ndft_fft(const double* x, int64_t x_len, int64_t M, double epsilon, int64_t N, double* out,
+                        void* stream);
+int gs_uniform_ndft_adjoint_fft(const double* samples, int64_t M, double epsilon, int64_t N, double* out,
+                                void* stream);
 
 /* Per-kernel device time of one T + T* pair (no reference counterpart; the
  * measurement hook bench.py uses for the roofline): `reps` pairs on zeroed

@@ -28,7 +28,8 @@ __all__ = [
     "Error", "UsageError", "FileFormatError", "ShapeError", "DomainError", "NumericalError", "CudaError",
     "SamplingSet", "Freq2WaveOptions", "Freq2WaveOp", "SolveOptions", "SolveStats",
     "freq2wave", "apply_forward", "apply_adjoint", "solve_least_squares", "CglsSession",
-    "ndft_forward", "ndft_adjoint", "family_p", "ROUTES", "lib_path", "load_library",
+    "ndft_forward", "ndft_adjoint", "NfftPlan", "plan_nfft", "nfft_forward", "nfft_adjoint",
+    "uniform_ndft_fft", "uniform_ndft_adjoint_fft", "family_p", "ROUTES", "lib_path", "load_library",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -117,6 +118,15 @@ def load_library():
     L.gs_cgls_finish.argtypes = [vp, vp, C.POINTER(_Stats), dp, vp]
     L.gs_cgls_destroy.argtypes = [vp]
     L.gs_op_export_factors.argtypes = [vp, C.c_int, C.c_int, dp, dp, dp]
+    L.gs_nfft_plan_create.argtypes = [C.c_int, C.POINTER(C.c_int), vp, C.c_int64, C.c_double, C.c_int, C.c_int,
+                                      C.POINTER(vp)]
+    L.gs_nfft_plan_forward.argtypes = [vp, vp, C.c_int64, vp, vp]
+    L.gs_nfft_plan_adjoint.argtypes = [vp, vp, C.c_int64, vp, vp]
+    L.gs_nfft_plan_info.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                    C.POINTER(C.c_int)]
+    L.gs_nfft_plan_destroy.argtypes = [vp]
+    L.gs_uniform_ndft_fft.argtypes = [vp, C.c_int64, C.c_int64, C.c_double, C.c_int64, vp, vp]
+    L.gs_uniform_ndft_adjoint_fft.argtypes = [vp, C.c_int64, C.c_double, C.c_int64, vp, vp]
     L.gs_ndft_forward.argtypes = [C.c_int, C.POINTER(C.c_int), vp, C.c_int64, vp, C.c_int64, vp, vp]
     L.gs_ndft_adjoint.argtypes = [C.c_int, C.POINTER(C.c_int), vp, C.c_int64, vp, C.c_int64, vp, vp]
     _lib = L
@@ -174,7 +184,7 @@ class Freq2WaveOptions:
     boundary_depth: int = 30
     product_terms: int = 48
     allow_uniform_fast_path: bool = True
-    allow_tensor_route: bool = True
+    allow_tensor_route: bool = False  # opt-in: exact tensor route for uniform 2D grids
     exact_ndft: bool = False  # 1D: direct NDFT core instead of the KB NFFT (GS_ROUTE_NDFT_1D)
 
 
@@ -374,6 +384,90 @@ def ndft_forward(dim, N, points, grid, stream=None):
 def ndft_adjoint(dim, N, points, samples, stream=None):
     """gs::ndft_adjoint (nufft.cpp:103-132): z_k = sum_m y_m exp(+2 pi i k.xi_m), on the device."""
     return _ndft(True, dim, N, points, samples, stream)
+
+
+class NfftPlan:
+    """gs::NfftPlan (nufft.hpp:36-62): Kaiser-Bessel window-gridding NDFT pair on
+    the device; ``points`` scaled to [-1/2, 1/2), point-major."""
+
+    def __init__(self, dim, N, points, sigma=2.0, w=6, device=0):
+        pts = np.ascontiguousarray(points, dtype=np.float64).ravel()
+        Nv = (C.c_int * 2)(int(N[0]), int(N[1]) if dim == 2 and len(N) > 1 else 0)
+        h = C.c_void_p()
+        _check(load_library().gs_nfft_plan_create(int(dim), Nv, pts.ctypes.data, pts.size // max(1, int(dim)),
+                                                  float(sigma), int(w), int(device), C.byref(h)))
+        self._h = h
+        d, m, g, nov = C.c_int(), C.c_int64(), C.c_int64(), (C.c_int * 2)()
+        _check(load_library().gs_nfft_plan_info(h, C.byref(d), C.byref(m), C.byref(g), nov))
+        self._dim, self._m, self._g, self._nov = d.value, m.value, g.value, (nov[0], nov[1])
+
+    def dim(self):
+        return self._dim
+
+    def points_count(self):
+        return self._m
+
+    def grid_size(self):
+        return self._g
+
+    def oversampled_length(self, axis):
+        return self._nov[axis]
+
+    def forward(self, grid, stream=None):
+        q, n, keep = _ptr_len(grid)
+        out = _out_like(keep, self._m)
+        o = out.data_ptr() if _is_torch(out) else out.ctypes.data
+        _check(load_library().gs_nfft_plan_forward(self._h, q, n, o, _stream_ptr(stream)))
+        return out
+
+    def adjoint(self, samples, stream=None):
+        q, n, keep = _ptr_len(samples)
+        out = _out_like(keep, self._g)
+        o = out.data_ptr() if _is_torch(out) else out.ctypes.data
+        _check(load_library().gs_nfft_plan_adjoint(self._h, q, n, o, _stream_ptr(stream)))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load_library().gs_nfft_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def plan_nfft(dim, N, points, sigma=2.0, w=6, device=0):
+    """gs::plan_nfft (nufft.cpp:367-370)."""
+    return NfftPlan(dim, N, points, sigma, w, device)
+
+
+def nfft_forward(plan, grid, stream=None):
+    return plan.forward(grid, stream)
+
+
+def nfft_adjoint(plan, samples, stream=None):
+    return plan.adjoint(samples, stream)
+
+
+def uniform_ndft_fft(x, M, epsilon, N, stream=None):
+    """gs::uniform_ndft_fft (nufft.cpp:402-429) on the device, any DFT length."""
+    q, n, keep = _ptr_len(x)
+    out = _out_like(keep, int(M))
+    o = out.data_ptr() if _is_torch(out) else out.ctypes.data
+    _check(load_library().gs_uniform_ndft_fft(q, n, int(M), float(epsilon), int(N), o, _stream_ptr(stream)))
+    return out
+
+
+def uniform_ndft_adjoint_fft(samples, epsilon, N, stream=None):
+    """gs::uniform_ndft_adjoint_fft (nufft.cpp:431-459) on the device."""
+    q, n, keep = _ptr_len(samples)
+    out = _out_like(keep, int(N))
+    o = out.data_ptr() if _is_torch(out) else out.ctypes.data
+    _check(load_library().gs_uniform_ndft_adjoint_fft(q, n, float(epsilon), int(N), o, _stream_ptr(stream)))
+    return out
 
 
 def solve_least_squares(op: Freq2WaveOp, samples, options: Optional[SolveOptions] = None, stream=None, **kw):

@@ -86,7 +86,7 @@ struct Freq2WaveOptions {  // freq2wave.hpp:12-24
   int boundary_depth = 30;
   int product_terms = 48;
   bool allow_uniform_fast_path = true;
-  bool allow_tensor_route = true;  // B200 addition: exact route for uniform 2D grids
+  bool allow_tensor_route = false;  // B200 addition (opt-in): exact route for uniform 2D grids
   int device = 0;
 };
 

@@ -26,43 +26,12 @@
 #include "kernels_vec.cuh"
 #include "kernels_cgls_fused.cuh"
 #include "ndft.h"
+#include "host_math.h"
+#include "plan.h"
 
 using namespace gsb;
 
 namespace {
-
-// ------------------------------------------------------------------ host math
-double wrap_half_open(double z) {  // freq2wave.cpp:15-19
-  double w = z - std::floor(z + 0.5);
-  if (w >= 0.5) w -= 1.0;
-  return w;
-}
-
-bool detect_uniform(const double* zeta, size_t M, long long n, double* eps_out) {  // freq2wave.cpp:22-37
-  if (M < 2 || (long long)M < n) return false;
-  double spacing = zeta[1] - zeta[0];
-  if (spacing <= 0.0) return false;
-  double eps = spacing * (double)n;
-  double inv = 1.0 / eps;
-  if (std::abs(inv - std::round(inv)) > 1e-9 || std::round(inv) < 1.0) return false;
-  double half_m = (double)M / 2.0;
-  for (size_t m = 0; m < M; ++m) {
-    double expect = eps / (double)n * ((double)m - half_m);
-    if (std::abs(zeta[m] - expect) > 1e-12) return false;
-  }
-  *eps_out = eps;
-  return true;
-}
-
-double kb_transform(double nu, int w, double beta) {  // nufft.cpp:163-171
-  double t = beta * beta - (GS_TWO_PI * w * nu) * (GS_TWO_PI * w * nu);
-  if (t > 0) {
-    double s = std::sqrt(t);
-    return 2.0 * w * std::sinh(s) / s;
-  }
-  double s = std::sqrt(-t);
-  return 2.0 * w * std::sin(s) / s;
-}
 
 // v_zero = (I - U)^{-1} V 1 by partial-pivot LU (fourier.cpp:60-72)
 bool fixed_point(const double* U, const double* V, int p, double* v) {
@@ -121,20 +90,6 @@ FamDev make_family(int p) {
     }
   }
   return f;
-}
-
-struct UniSetup {
-  long long inv_eps, q, n2;
-};
-UniSetup uniform_setup(long long M, double eps, long long N) {  // nufft.cpp:389-400
-  if (eps <= 0.0) fail(GS_ERR_DOMAIN, "epsilon must be positive");
-  double inv = 1.0 / eps;
-  long long inv_eps = std::llround(inv);
-  if (inv_eps < 1 || std::abs(inv - (double)inv_eps) > 1e-9) fail(GS_ERR_DOMAIN, "1/epsilon must be a positive integer");
-  if (M < N) fail(GS_ERR_DOMAIN, "uniform reduction requires M >= N");
-  long long per = N * inv_eps;
-  long long q = (M + per - 1) / per;
-  return {inv_eps, q, q * per};
 }
 
 }  // namespace

@@ -46,7 +46,7 @@ void ndft_forward_launch(const NdftShape& s, const double* pts, const cplx* x, c
   part.alloc((size_t)s.batch * ks * s.M);
   k_ndft_fwd<<<dim3((unsigned)nb, ks, s.batch), ND_FTHREADS, 0, st>>>(g, pts, x, ups, part.p);
   pmark("k_ndft_fwd", st);
-  k_ndft_fwd_reduce<<<dim3(nblk(s.M, 256), s.batch), 256, 0, st>>>(s.M, ks, part.p, rec, p, edges, x, s.N1, y);
+  k_ndft_fwd_reduce<<<dim3(nblk(s.M * 32, 256), s.batch), 256, 0, st>>>(s.M, ks, part.p, rec, p, edges, x, s.N1, y);
   pmark("k_ndft_fwd_reduce", st);
   CKL();
 }
@@ -54,7 +54,9 @@ void ndft_forward_launch(const NdftShape& s, const double* pts, const cplx* x, c
 void ndft_adjoint_launch(const NdftShape& s, const double* pts, const cplx* y, cplx* z, int lo, int hi,
                          const cplx* rec, int p, int edges, DBuf<cplx>& part, cudaStream_t st) {
   const NdGeom g = geom(s, 0, s.N1);
-  const int groups = g.N0 * ((g.runs + ND_AUPT - 1) / ND_AUPT);
+  // two units per thread (giant-step chained) once there are enough of them
+  const int aupt = (int64_t)g.N0 * g.runs * s.batch >= 8192 ? 2 : 1;
+  const int groups = g.N0 * ((g.runs + aupt - 1) / aupt);
   const int64_t nb = (groups + ND_ATHREADS - 1) / ND_ATHREADS;
   const int64_t want = (int64_t)4 * sm_count();
   int64_t ms = std::max<int64_t>(1, std::min<int64_t>(want / std::max<int64_t>(1, nb * s.batch),
@@ -65,9 +67,12 @@ void ndft_adjoint_launch(const NdftShape& s, const double* pts, const cplx* y, c
   const int64_t nmodes = (int64_t)s.N0 * s.N1;
   part.alloc((size_t)s.batch * ms * nmodes);
   const int Rr = 1 + (edges ? 2 * p : 0);
-  k_ndft_adj<<<dim3((unsigned)nb, (unsigned)ms, s.batch), ND_ATHREADS, 0, st>>>(g, pts, y, rec, Rr, pps, part.p);
+  if (aupt == 2)
+    k_ndft_adj<2><<<dim3((unsigned)nb, (unsigned)ms, s.batch), ND_ATHREADS, 0, st>>>(g, pts, y, rec, Rr, pps, part.p);
+  else
+    k_ndft_adj<1><<<dim3((unsigned)nb, (unsigned)ms, s.batch), ND_ATHREADS, 0, st>>>(g, pts, y, rec, Rr, pps, part.p);
   pmark("k_ndft_adj", st);
-  k_ndft_adj_reduce<<<dim3(nblk(nmodes, 256), s.batch), 256, 0, st>>>(nmodes, (int)ms, part.p, lo, hi, z);
+  k_ndft_adj_reduce<<<dim3(nblk(nmodes * 32, 256), s.batch), 256, 0, st>>>(nmodes, (int)ms, part.p, lo, hi, z);
   pmark("k_ndft_adj_reduce", st);
   if (rec && edges) {
     k_ndft_adj_edges<<<dim3(2 * p, s.batch), 256, 0, st>>>(s.M, rec, p, y, s.N1, z);
@@ -98,9 +103,16 @@ __global__ void k_check_points(const double* __restrict__ pts, int64_t n, int* _
   if (i < n && !(pts[i] >= -0.5 && pts[i] < 0.5)) *bad = 1;
 }
 
+// per-thread workspaces of the C-ABI calls (grown, never freed per call: a
+// cudaFree per call would synchronise the device)
+thread_local DBuf<int> t_bad;
+thread_local DBuf<cplx> t_part, t_in, t_out;
+thread_local DBuf<double> t_pts;
+
 const double* stage_points(const double* pts, int64_t n, Staged& S, cudaStream_t st) {
+  (void)S;
   if (is_device_ptr(pts)) {
-    DBuf<int> bad;
+    DBuf<int>& bad = t_bad;
     bad.alloc(1);
     CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
     k_check_points<<<nblk(n, 256), 256, 0, st>>>(pts, n, bad.p);
@@ -112,8 +124,8 @@ const double* stage_points(const double* pts, int64_t n, Staged& S, cudaStream_t
     return pts;
   }
   check_points_host(pts, n);
-  S.pts.upload(pts, n, st);
-  return S.pts.p;
+  t_pts.upload(pts, n, st);
+  return t_pts.p;
 }
 
 int ndft_call(bool adjoint, int dim, const int* N, const double* points, int64_t M, const double* in, int64_t in_len,
@@ -139,16 +151,16 @@ int ndft_call(bool adjoint, int dim, const int* N, const double* points, int64_t
     const int64_t out_len = adjoint ? nmodes : M;
     const cplx* din = (const cplx*)in;
     if (!is_device_ptr(in)) {
-      S.in.upload((const cplx*)in, in_len, st);
-      din = S.in.p;
+      t_in.upload((const cplx*)in, in_len, st);
+      din = t_in.p;
     }
     const bool dev_out = is_device_ptr(out);
     cplx* dout = (cplx*)out;
     if (!dev_out) {
-      S.out.alloc(out_len);
-      dout = S.out.p;
+      t_out.alloc(out_len);
+      dout = t_out.p;
     }
-    DBuf<cplx> part;
+    DBuf<cplx>& part = t_part;
     if (adjoint) ndft_adjoint_launch(s, dp, din, dout, 0, s.N1 * s.N0, nullptr, 1, 0, part, st);
     else ndft_forward_launch(s, dp, din, dout, 0, s.N1, nullptr, 1, 0, part, st);
     if (!dev_out) CK(cudaMemcpyAsync(out, dout, out_len * sizeof(cplx), cudaMemcpyDeviceToHost, st));

@@ -28,7 +28,6 @@
 #define ND_FPPT 2
 #define ND_FTILE 128  // units staged per forward tile (ND_FTILE * ND_RUN complex = 32 KB)
 #define ND_ATHREADS 128
-#define ND_AUPT 2
 #define ND_ATILE 64   // points staged per adjoint tile (P_t table 16 KB)
 
 struct NdGeom {
@@ -127,11 +126,25 @@ __global__ void __launch_bounds__(ND_FTHREADS) k_ndft_fwd(NdGeom g, const double
   }
 }
 
-// fixed-order sum of the k-splits + optional operator epilogue (1D T, freq2wave.cpp:232-236):
-// y_m = D_m acc + sum_c L_mc x_c + sum_c R_mc x_{n-p+c}; rec = [D, L_0..L_{p-1}, R_0..R_{p-1}] per point
+// fixed-order sum of the k-splits (one warp per output: lane l takes splits
+// l, l+32, ..., then a shuffle tree -- deterministic) + optional operator
+// epilogue (1D T, freq2wave.cpp:232-236): y_m = D_m acc + sum_c L_mc x_c +
+// sum_c R_mc x_{n-p+c}; rec = [D, L_0..L_{p-1}, R_0..R_{p-1}] per point
+__device__ __forceinline__ cplx nd_warp_split_sum(const cplx* __restrict__ part, int64_t stride, int nsplit, int64_t i) {
+  const int lane = threadIdx.x & 31;
+  cplx acc = mk(0, 0);
+  for (int s = lane; s < nsplit; s += 32) acc = cadd(acc, part[(int64_t)s * stride + i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    acc.x += __shfl_down_sync(0xffffffffu, acc.x, o);
+    acc.y += __shfl_down_sync(0xffffffffu, acc.y, o);
+  }
+  return acc;
+}
+
 __global__ void k_ndft_fwd_reduce(int64_t M, int nsplit, const cplx* __restrict__ part, const cplx* __restrict__ rec,
                                   int p, int edges, const cplx* __restrict__ x, int n, cplx* __restrict__ y) {
-  const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t m = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (m >= M) return;
   part += (int64_t)blockIdx.y * nsplit * M;
   y += (int64_t)blockIdx.y * M;
@@ -139,8 +152,8 @@ __global__ void k_ndft_fwd_reduce(int64_t M, int nsplit, const cplx* __restrict_
     rec += (int64_t)blockIdx.y * M * (1 + (edges ? 2 * p : 0));
     x += (int64_t)blockIdx.y * n;
   }
-  cplx acc = part[m];
-  for (int s = 1; s < nsplit; ++s) acc = cadd(acc, part[(int64_t)s * M + m]);
+  cplx acc = nd_warp_split_sum(part, M, nsplit, m);
+  if ((threadIdx.x & 31) != 0) return;
   if (rec) {
     const int Rr = 1 + (edges ? 2 * p : 0);
     const cplx* r = rec + m * Rr;
@@ -159,6 +172,7 @@ __global__ void k_ndft_fwd_reduce(int64_t M, int nsplit, const cplx* __restrict_
 // part[ms][mode]: a thread owns ND_AUPT consecutive units of one row; the CTA
 // walks the points [m0, m1) of this blockIdx.y in staged tiles.
 // rec (1D operator use): the staged sample value is conj(D_m) y_m.
+template <int ND_AUPT>
 __global__ void __launch_bounds__(ND_ATHREADS) k_ndft_adj(NdGeom g, const double* __restrict__ pts,
                                                            const cplx* __restrict__ y, const cplx* __restrict__ rec,
                                                            int Rr, int64_t points_per_split, cplx* __restrict__ out) {
@@ -227,18 +241,17 @@ __global__ void __launch_bounds__(ND_ATHREADS) k_ndft_adj(NdGeom g, const double
     }
 }
 
-// fixed-order sum of the point splits; 1D operator use keeps only [lo, hi)
-// (edge slots are filled by k_ndft_adj_edges)
+// fixed-order sum of the point splits (one warp per mode); 1D operator use
+// keeps only [lo, hi) (edge slots are filled by k_ndft_adj_edges)
 __global__ void k_ndft_adj_reduce(int64_t nmodes, int nsplit, const cplx* __restrict__ part, int lo, int hi,
                                   cplx* __restrict__ z) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (k >= nmodes) return;
   if (k < lo || k >= hi) return;
   part += (int64_t)blockIdx.y * nsplit * nmodes;
   z += (int64_t)blockIdx.y * nmodes;
-  cplx acc = part[k];
-  for (int s = 1; s < nsplit; ++s) acc = cadd(acc, part[(int64_t)s * nmodes + k]);
-  z[k] = acc;
+  const cplx acc = nd_warp_split_sum(part, nmodes, nsplit, k);
+  if ((threadIdx.x & 31) == 0) z[k] = acc;
 }
 
 // edge columns of the 1D adjoint: z_c = sum_m conj(L_mc) y_m, z_{n-p+c} = sum_m conj(R_mc) y_m

@@ -88,3 +88,26 @@ def test_haar_ignores_depth_and_terms():
     gs, _ = _lib()
     with pytest.raises(gs.CudaError):
         gs.freq2wave(gs.SamplingSet(1, np.array([0.0, -4.0])), "haar", 3, boundary_depth=0, product_terms=0)
+
+
+@pytest.mark.parametrize("args", [
+    (1, [16], [0.5], 2.0, 6), (1, [15], [0.1], 2.0, 6), (1, [16], [0.1], 1.1, 6), (1, [16], [0.1], 2.0, 1),
+    (3, [16], [0.1], 2.0, 6)])
+def test_nfft_plan_validation_matches_reference(args):
+    """NfftPlan ctor checks (nufft.cpp:181-188) raise before the device is touched."""
+    gs, _ = _lib()
+    dim, N, p, sigma, w = args
+    with pytest.raises(gs.DomainError):
+        gs.plan_nfft(dim, N, np.array(p), sigma, w)
+
+
+def test_uniform_reduction_validation():
+    """uniform_setup (nufft.cpp:389-400): 1/epsilon integer, M >= N, x length <= N."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    gs, _ = _lib()
+    x = np.ones(8, complex)
+    for args in ((x, 16, 0.3, 8), (x, 4, 0.5, 8), (np.ones(9, complex), 16, 0.5, 8)):
+        with pytest.raises(gs.DomainError):
+            gs.uniform_ndft_fft(*args)

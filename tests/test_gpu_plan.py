@@ -1,0 +1,136 @@
+"""GPU NfftPlan / plan_nfft and the uniform-grid reduction (the lower-level API
+of nufft.hpp:36-77) through the C-ABI.
+
+Restates the reference's tests/test_nufft.cpp:62-185 (plan preconditions and
+accessors, fast vs direct at 1e-7, exact-transpose pairing at 1e-12,
+linearity, the acceptance-size sweep, uniform reduction = direct NDFT at
+1e-12) and checks the general engine against the oracle's restatement of the
+same plan (nufft.cpp:138-365) at 1e-12 where the reference's build is limited
+by nothing: sigma = 1.25 / 1.5 (non-power-of-two oversampled lengths), kernel
+half-widths w = 2..10, odd-factor N, the four-step FFT (n_ov > 6144) and
+uniform DFT lengths beyond one CTA."""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import rel_error
+
+pytestmark = pytest.mark.gpu
+
+
+def gs():
+    import paper_1607_04091_b200 as m
+    return m
+
+
+def rc(n, rng):
+    return rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+
+
+def pts(m, rng, dim=1):
+    return rng.uniform(-0.5, 0.4999, m * dim)
+
+
+def test_plan_construction_and_preconditions():  # test_nufft.cpp:62-75
+    g = gs()
+    rng = np.random.default_rng(23)
+    p = pts(5, rng)
+    plan = g.plan_nfft(1, [16], p, 2.0, 6)
+    assert plan.oversampled_length(0) == 32 and plan.points_count() == 5 and plan.grid_size() == 16
+    for args in (([16], np.array([0.5]), 2.0, 6), ([15], p, 2.0, 6), ([16], p, 1.1, 6), ([16], p, 2.0, 1)):
+        with pytest.raises(g.DomainError):
+            g.plan_nfft(1, *args)
+
+
+def test_fast_tracks_direct_and_pairs_exactly():  # test_nufft.cpp:77-108
+    g = gs()
+    rng = np.random.default_rng(24)
+    p = pts(100, rng)
+    plan = g.plan_nfft(1, [64], p, 2.0, 6)
+    imp = np.zeros(64, complex)
+    imp[32] = 1
+    assert np.max(np.abs(plan.forward(imp) - 1)) < 1e-7
+    x, y = rc(64, rng), rc(100, rng)
+    fast = plan.forward(x)
+    assert rel_error(fast, g.ndft_forward(1, [64], p, x)) < 1e-7
+    fa = plan.adjoint(y)
+    assert rel_error(fa, g.ndft_adjoint(1, [64], p, y)) < 1e-7
+    assert abs(np.vdot(y, fast) - np.vdot(fa, x)) / (np.linalg.norm(x) * np.linalg.norm(y)) < 1e-12
+    p2 = pts(10, rng, 2)
+    plan2 = g.plan_nfft(2, [8, 8], p2, 2.0, 6)
+    x2, y2 = rc(64, rng), rc(10, rng)
+    assert rel_error(plan2.forward(x2), g.ndft_forward(2, [8, 8], p2, x2)) < 1e-7
+    assert rel_error(plan2.adjoint(y2), g.ndft_adjoint(2, [8, 8], p2, y2)) < 1e-7
+
+
+def test_linearity():  # test_nufft.cpp:110-122
+    g = gs()
+    rng = np.random.default_rng(25)
+    plan = g.plan_nfft(1, [32], pts(40, rng), 2.0, 6)
+    a, b = rc(32, rng), rc(32, rng)
+    al, be = 0.3 - 1.1j, -0.8 + 0.2j
+    d = plan.forward(al * a + be * b) - al * plan.forward(a) - be * plan.forward(b)
+    assert np.max(np.abs(d)) < 1e-12
+
+
+@pytest.mark.parametrize("n,m", [(64, 1000), (256, 4096)])
+def test_acceptance_sweep(n, m):  # test_nufft.cpp:174-185
+    g = gs()
+    rng = np.random.default_rng(28 + n)
+    p = pts(m, rng)
+    x = rc(n, rng)
+    assert rel_error(g.plan_nfft(1, [n], p, 2.0, 6).forward(x), g.ndft_forward(1, [n], p, x)) < 1e-7
+
+
+@pytest.mark.parametrize("dim,N,M,sigma,w", [
+    (1, [64], 500, 2.0, 6), (1, [64], 500, 1.25, 6), (1, [96], 700, 1.5, 4), (1, [30], 300, 2.0, 10),
+    (1, [512], 3000, 1.25, 2), (1, [8192], 20000, 2.0, 6),  # n_ov 16384: four-step FFT
+    (2, [32, 32], 2000, 2.0, 6), (2, [24, 40], 1500, 1.5, 5), (2, [64, 64], 4000, 1.25, 8)])
+def test_plan_vs_oracle_plan(dim, N, M, sigma, w):
+    """Same algorithm as the reference's NfftPlan (oracle restatement) at 1e-12."""
+    g = gs()
+    rng = np.random.default_rng(M + 7 * w)
+    p = pts(M, rng, dim)
+    NN = N if dim == 2 else [N[0], 0]
+    plan = g.plan_nfft(dim, N, p, sigma, w)
+    x, y = rc(int(np.prod(N)), rng), rc(M, rng)
+    fo, nov = oracle.nfft(dim, NN, p, x, sigma=sigma, w=w)
+    ao, _ = oracle.nfft(dim, NN, p, y, adjoint=True, sigma=sigma, w=w)
+    assert plan.oversampled_length(0) == nov[0]
+    ef, ea = rel_error(plan.forward(x), fo), rel_error(plan.adjoint(y), ao)
+    print(f"plan dim={dim} N={N} sigma={sigma} w={w} n_ov={nov}: fwd {ef:.2e} adj {ea:.2e}")
+    assert ef < 1e-12 and ea < 1e-12
+
+
+def test_uniform_reduction_cases():  # test_nufft.cpp:124-172
+    g = gs()
+    rng = np.random.default_rng(26)
+    assert np.all(g.uniform_ndft_fft(np.zeros(8, complex), 16, 0.5, 8) == 0)
+    x = rc(8, rng)
+    p16 = np.array([(m - 9) / 16.0 for m in range(1, 17)])
+    assert rel_error(g.uniform_ndft_fft(x, 16, 0.5, 8), g.ndft_forward(1, [8], p16, x)) < 1e-12
+    x4 = rc(4, rng)
+    p8 = np.array([(m - 5) / 8.0 for m in range(1, 9)])
+    want4 = np.array([sum(x4[k + 2] * np.exp(-2j * np.pi * k * q) for k in range(-2, 2)) for q in p8])
+    assert rel_error(g.uniform_ndft_fft(x4, 8, 1.0, 8), want4) < 1e-12
+    with pytest.raises(g.DomainError):
+        g.uniform_ndft_fft(x, 16, 0.3, 8)
+    with pytest.raises(g.DomainError):
+        g.uniform_ndft_fft(x, 4, 0.5, 8)
+    rng = np.random.default_rng(27)
+    N, M, eps = 16, 40, 0.25
+    pa = np.array([eps / N * (m - 1 - M / 2) for m in range(1, M + 1)])
+    y = rc(M, rng)
+    assert rel_error(g.uniform_ndft_adjoint_fft(y, eps, N), g.ndft_adjoint(1, [16], pa, y)) < 1e-12
+
+
+@pytest.mark.parametrize("N,M,eps", [(512, 1024, 1.0), (300, 900, 1.0 / 3), (4096, 10000, 0.5), (6000, 6000, 1.0)])
+def test_uniform_reduction_any_length(N, M, eps):
+    """DFT lengths q N / eps beyond the fused single-CTA kernels (non-power-of-two, > 8192)."""
+    g = gs()
+    rng = np.random.default_rng(N)
+    x, y = rc(N, rng), rc(M, rng)
+    ef = rel_error(g.uniform_ndft_fft(x, M, eps, N), oracle.uniform_fft(x, M, eps, N))
+    ea = rel_error(g.uniform_ndft_adjoint_fft(y, eps, N), oracle.uniform_adjoint_fft(y, eps, N))
+    print(f"uniform N={N} M={M} eps={eps}: fwd {ef:.2e} adj {ea:.2e}")
+    assert ef < 1e-12 and ea < 1e-12
