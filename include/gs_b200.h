@@ -168,6 +168,26 @@ int gs_uniform_ndft_fft(const double* x, int64_t x_len, int64_t M, double epsilo
 int gs_uniform_ndft_adjoint_fft(const double* samples, int64_t M, double epsilon, int64_t N, double* out,
                                 void* stream);
 
+/* Family data and transforms (scaling.hpp / fourier.hpp; scaling.cpp:29-75,
+ * fourier.cpp:34-130).  taps [2p] (filter_coefficients, k = -p+1..p);
+ * boundary filters of one side (left != 0): H [p*p], h [p*(2p-1)] (columns
+ * m = p..3p-2), integer values [p*2p], row-major, any pointer may be NULL;
+ * v [p] = boundary_fourier_at_zero.  The evaluations run on the device: out
+ * [n] complex (scaling) or [n][p] complex (boundary transforms at xi[i]). */
+int gs_family_filter(int family_p, double* taps);
+int gs_boundary_filter_set(int family_p, int left, double* H, double* h, double* integer_values);
+int gs_boundary_at_zero(int family_p, int left, double* v);
+int gs_fourier_scaling_eval(int family_p, int64_t n, const double* xi, int terms, double* out, void* stream);
+int gs_fourier_boundary_eval(int family_p, int left, int64_t n, const double* xi, int depth, int terms,
+                             double* out, void* stream);
+
+/* gs::densify (freq2wave.cpp:389-450): the dense M x cols section assembled
+ * on the device from the transform formulas (column-major like
+ * Eigen::MatrixXcd); coords [M][dim] natural frequencies, sqrt_weights [M]
+ * or NULL; DomainError past entry_cap entries. */
+int gs_densify(int dim, int family_p, int J, int64_t M, const double* coords, const double* sqrt_weights,
+               int64_t entry_cap, double* out, void* stream);
+
 /* Per-kernel device time of one T + T* pair (no reference counterpart; the
  * measurement hook bench.py uses for the roofline): `reps` pairs on zeroed
  * buffers, CUDA events between consecutive launches on `stream`.  Writes up

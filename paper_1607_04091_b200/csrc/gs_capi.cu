@@ -338,6 +338,60 @@ bool spread_mma();
 static_assert(F_T / F_WARPS == F_T / F_IWARPS, "the DMMA kernels share the in-tile band order");
 bool fold_src();
 
+
+// ------------------------------------------------------------------ family / transform evaluation
+// (fourier.cpp:34-130 at caller frequencies; densify, freq2wave.cpp:389-450)
+__global__ void k_eval_scaling(FamDev f, const double* __restrict__ xi, int64_t n, int terms, cplx* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = d_fourier_scaling(f, xi[i], terms);
+}
+__global__ void k_eval_boundary(FamDev f, int side, const double* __restrict__ xi, int64_t n, int depth, int terms,
+                                cplx* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) d_fourier_boundary(f, side, xi[i], depth, terms, out + i * f.p);
+}
+// dense_axis_row (freq2wave.cpp:392-418) for every point: rows[m][c], unweighted,
+// default depth / terms as the reference's densify uses
+__global__ void k_densify_axis(FamDev f, const double* __restrict__ coords, int dim, int axis, int64_t M, int J,
+                               int n, cplx* __restrict__ rows) {
+  const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  const double xi = coords[m * dim + axis];
+  const double scaled = ldexp(xi, -J);
+  const double amp = exp2(-0.5 * (double)J);
+  const cplx interior = cscale(d_fourier_scaling(f, scaled, 48), amp);
+  cplx* row = rows + m * n;
+  for (int c = 0; c < n; ++c) {
+    const long long k = (long long)c - n / 2;
+    row[c] = cmul(interior, polar1((-GS_TWO_PI * (double)k) * scaled));
+  }
+  if (f.p >= 2) {
+    cplx vl[GS_MAXP], vr[GS_MAXP];
+    d_fourier_boundary(f, 0, scaled, 30, 48, vl);
+    d_fourier_boundary(f, 1, scaled, 30, 48, vr);
+    const cplx pl = cscale(polar1(GS_PI * xi), amp), pr = cscale(polar1(-GS_PI * xi), amp);
+    for (int c = 0; c < f.p; ++c) {
+      row[c] = cmul(pl, vl[c]);
+      row[n - f.p + c] = cmul(pr, vr[f.p - 1 - c]);
+    }
+  }
+}
+// out (M x cols, column-major): 1D weight * rx(c); 2D (weight * rx(i)) * ry(j) at column j n + i
+__global__ void k_densify_out(int dim, int64_t M, int n, const cplx* __restrict__ rx, const cplx* __restrict__ ry,
+                              const double* __restrict__ sw, cplx* __restrict__ out) {
+  const int64_t cols = dim == 1 ? n : (int64_t)n * n;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= M * cols) return;
+  const int64_t m = e % M, col = e / M;
+  const double w = sw ? sw[m] : 1.0;
+  if (dim == 1) {
+    out[e] = cscale(rx[m * n + col], w);
+    return;
+  }
+  const int64_t i = col % n, j = col / n;
+  out[e] = cmul(cscale(rx[m * n + i], w), ry[m * n + j]);
+}
+
 // ------------------------------------------------------------------ construction
 gs_op* create(const gs_op_desc* dsc) {
   if (!dsc) fail(GS_ERR_USAGE, "null descriptor");
@@ -1653,6 +1707,117 @@ int gs_boundary_dyadic(int family_p, int left, int R, int k, double* values, int
 int gs_weval(int dim, int family_p, int J, int R, const double* coeffs, int64_t coeffs_len, double* out,
              void* stream) {
   return guard_call([&] { dy_weval(dim, family_p, J, R, coeffs, coeffs_len, out, as_stream(stream)); });
+}
+
+
+// ---------------------------------------------------------------- family data / transforms (scaling.hpp, fourier.hpp)
+int gs_family_filter(int family_p, double* taps) {
+  return guard_call([&] {
+    if (family_p < 1 || family_p > 8) fail(GS_ERR_DOMAIN, "unsupported family");
+    if (!taps) fail(GS_ERR_USAGE, "null output");
+    const gsdata::FamilyData& src = gsdata::kFamilies[family_p - 1];
+    for (int i = 0; i < 2 * family_p; ++i) taps[i] = src.taps[i];
+  });
+}
+
+int gs_boundary_filter_set(int family_p, int left, double* H, double* h, double* integer_values) {
+  return guard_call([&] {
+    if (family_p < 1 || family_p > 8) fail(GS_ERR_DOMAIN, "unsupported family");
+    if (family_p < 2) fail(GS_ERR_DOMAIN, "haar has no boundary corrections (p = 1)");
+    const gsdata::FamilyData& src = gsdata::kFamilies[family_p - 1];
+    const int p = family_p;
+    if (H) std::memcpy(H, left ? src.left_H : src.right_H, sizeof(double) * p * p);
+    if (h) std::memcpy(h, left ? src.left_h : src.right_h, sizeof(double) * p * (2 * p - 1));
+    if (integer_values) std::memcpy(integer_values, left ? src.left_seed : src.right_seed, sizeof(double) * p * 2 * p);
+  });
+}
+
+int gs_boundary_at_zero(int family_p, int left, double* v) {
+  return guard_call([&] {
+    if (family_p < 1 || family_p > 8) fail(GS_ERR_DOMAIN, "unsupported family");
+    if (family_p < 2) fail(GS_ERR_DOMAIN, "haar has no boundary corrections (p = 1)");
+    if (!v) fail(GS_ERR_USAGE, "null output");
+    const FamDev f = make_family(family_p);  // NumericalError if the fixed point is singular
+    for (int i = 0; i < family_p; ++i) v[i] = f.vz[left ? 0 : 1][i];
+  });
+}
+
+namespace {
+int eval_call(int family_p, int side, int64_t n, const double* xi, int depth, int terms, double* out, void* stream) {
+  return guard_call([&] {
+    if (family_p < 1 || family_p > 8) fail(GS_ERR_DOMAIN, "unsupported family");
+    if (side >= 0 && family_p < 2) fail(GS_ERR_DOMAIN, "haar has no boundary corrections (p = 1)");
+    if (family_p >= 2 && terms < 1) fail(GS_ERR_DOMAIN, "fourier_scaling: terms must be >= 1");
+    if (side >= 0 && depth < 1) fail(GS_ERR_DOMAIN, "fourier_boundary: depth must be >= 1");
+    if (n < 0 || (n > 0 && (!xi || !out))) fail(GS_ERR_USAGE, "null argument");
+    if (n == 0) return;
+    cudaStream_t st = (cudaStream_t)stream;
+    const FamDev f = make_family(family_p);
+    const int per = side >= 0 ? family_p : 1;
+    DBuf<double> dx;
+    DBuf<cplx> dout;
+    const double* px = xi;
+    if (!is_device_ptr(xi)) {
+      dx.upload(xi, n, st);
+      px = dx.p;
+    }
+    const bool dev_out = is_device_ptr(out);
+    cplx* po = (cplx*)out;
+    if (!dev_out) {
+      dout.alloc(n * per);
+      po = dout.p;
+    }
+    if (side >= 0) k_eval_boundary<<<nblk(n, 128), 128, 0, st>>>(f, side, px, n, depth, terms, po);
+    else k_eval_scaling<<<nblk(n, 128), 128, 0, st>>>(f, px, n, terms, po);
+    pmark(side >= 0 ? "k_eval_boundary" : "k_eval_scaling", st);
+    CKL();
+    if (!dev_out) CK(cudaMemcpyAsync(out, po, n * per * sizeof(cplx), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+}  // namespace
+
+int gs_fourier_scaling_eval(int family_p, int64_t n, const double* xi, int terms, double* out, void* stream) {
+  return eval_call(family_p, -1, n, xi, 1, terms, out, stream);
+}
+
+int gs_fourier_boundary_eval(int family_p, int left, int64_t n, const double* xi, int depth, int terms, double* out,
+                             void* stream) {
+  return eval_call(family_p, left ? 0 : 1, n, xi, depth, terms, out, stream);
+}
+
+int gs_densify(int dim, int family_p, int J, int64_t M, const double* coords, const double* sqrt_weights,
+               int64_t entry_cap, double* out, void* stream) {
+  return guard_call([&] {
+    if (dim != 1 && dim != 2) fail(GS_ERR_DOMAIN, "sampling set must be 1D or 2D");
+    if (family_p < 1 || family_p > 8) fail(GS_ERR_DOMAIN, "unsupported family");
+    if (J < 0 || J > 24) fail(GS_ERR_DOMAIN, "scale J out of range");
+    if (M <= 0 || !coords || !out) fail(GS_ERR_USAGE, "null argument");
+    const int64_t n = 1LL << J;
+    const int64_t cols = dim == 1 ? n : n * n;
+    if ((double)M * (double)cols > (double)entry_cap) fail(GS_ERR_DOMAIN, "densify: matrix exceeds the entry cap");
+    cudaStream_t st = (cudaStream_t)stream;
+    const FamDev f = make_family(family_p);
+    DBuf<double> dc, dw;
+    dc.upload(coords, M * dim, st);
+    if (sqrt_weights) dw.upload(sqrt_weights, M, st);
+    DBuf<cplx> rx, ry, dout;
+    rx.alloc(M * n);
+    k_densify_axis<<<nblk(M, 128), 128, 0, st>>>(f, dc.p, dim, 0, M, J, (int)n, rx.p);
+    pmark("k_densify_axis", st);
+    if (dim == 2) {
+      ry.alloc(M * n);
+      k_densify_axis<<<nblk(M, 128), 128, 0, st>>>(f, dc.p, dim, 1, M, J, (int)n, ry.p);
+      pmark("k_densify_axis", st);
+    }
+    dout.alloc(M * cols);
+    k_densify_out<<<nblk(M * cols, 256), 256, 0, st>>>(dim, M, (int)n, rx.p, ry.p, sqrt_weights ? dw.p : nullptr,
+                                                        dout.p);
+    pmark("k_densify_out", st);
+    CKL();
+    CK(cudaMemcpyAsync(out, dout.p, M * cols * sizeof(cplx), cudaMemcpyDefault, st));
+    CK(cudaStreamSynchronize(st));
+  });
 }
 
 #ifdef F_TIMELINE

@@ -21,6 +21,10 @@ not run at test time -- C4 takes ~25 min on one core):
 
 Usage: python tools/gen_cgls_fixtures.py c3 | c4 | c5:0 | c5:85 | ...
 (each config in its own process; they are independent).
+      python tools/gen_cgls_fixtures.py --checkpoints 10,25,50 c4
+stores the oracle iterates after those (shorter) iteration counts instead
+(cgls_c4_ckpt.npz): how the GPU / oracle gap grows with the iteration count
+on an ill-conditioned config.
 """
 import hashlib
 import os
@@ -47,6 +51,31 @@ def b_sample_idx(M):
     head = np.arange(min(64, M))
     stride = np.linspace(0, M - 1, 1024).astype(np.int64)
     return np.unique(np.concatenate([head, stride]))
+
+
+def checkpoints(spec, ks):
+    workload, _, b = spec.partition(":")
+    b = int(b or 0)
+    t0 = time.time()
+    dim, p, J, c, mu, bw, sig = bench.problem_inputs(workload, b, bench.ProductGen())
+    op_u = oracle.Op(dim, p, J, c, bandwidth=bw)
+    x_true, noise = bench.coeffs_and_noise(b, op_u.cols, op_u.rows, sig)
+    data = op_u.forward(x_true) + noise
+    del op_u
+    op = oracle.Op(dim, p, J, c, weights=mu, bandwidth=bw)
+    res = {}
+
+    def run(k):
+        res[k] = op.solve(data, max_iterations=k, tolerance=1e-300)[0]
+
+    ths = [threading.Thread(target=run, args=(k,)) for k in ks]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    name = f"cgls_{workload}_ckpt.npz"
+    np.savez(os.path.join(OUT, name), iters=np.array(ks), **{f"x{k}": res[k] for k in ks})
+    print(f"{spec}: checkpoints {ks} in {time.time() - t0:.0f} s -> {name}", flush=True)
 
 
 def main(spec):
@@ -87,5 +116,11 @@ def main(spec):
 
 
 if __name__ == "__main__":
-    for s in sys.argv[1:]:
-        main(s)
+    args = sys.argv[1:]
+    if args and args[0] == "--checkpoints":
+        ks = [int(v) for v in args[1].split(",")]
+        for s in args[2:]:
+            checkpoints(s, ks)
+    else:
+        for s in args:
+            main(s)
