@@ -71,6 +71,47 @@ def problem_count(workload):
     return 256 if workload == "c5" else 1
 
 
+# (dim, family p, J, samples per problem, coefficients per problem, the reference's route)
+SHAPES = {"c1": (1, 1, 9, 1024, 512, "uniform_1d"), "c2": (1, 4, 10, 4096, 1024, "nfft_1d"),
+          "c3": (2, 2, 8, 262144, 65536, "nfft_2d"), "c4": (2, 4, 9, 1048576, 262144, "nfft_2d"),
+          "c5": (2, 4, 8, 262144, 65536, "nfft_2d")}
+
+
+def config_for(workload, P, world):
+    """The `config` object both arms print (identical dicts for the same run)."""
+    dim, p, J, M, Nc, route = SHAPES[workload]
+    return {"workload": workload.upper(), "description": WORKLOADS[workload], "problems": P,
+            "samples_per_problem": M, "coeffs_per_problem": Nc, "family": f"p={p}", "J": J,
+            "reference_route": route, "iterations_in_config": CONFIG_ITERS[workload],
+            "cgls_tolerance": "1e-300 (fixed count)",
+            "parallelism": f"problem-sharded x{world}" if world > 1 else "1 rank"}
+
+
+def host_cpu():
+    """CPU model and physical core count of this host."""
+    model, cores = "unknown", set()
+    try:
+        phys = core = None
+        for line in open("/proc/cpuinfo"):
+            k, _, v = line.partition(":")
+            k, v = k.strip(), v.strip()
+            if k == "model name":
+                model = v
+            elif k == "physical id":
+                phys = v
+            elif k == "core id":
+                core = v
+            elif not k and phys is not None:
+                cores.add((phys, core))
+                phys = core = None
+        if phys is not None:
+            cores.add((phys, core))
+    except OSError:
+        pass
+    ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    return {"model": model, "physical_cores": len(cores) or None, "logical_cpus_available": ncpu}
+
+
 def coeffs_and_noise(b, ncols, nrows, sigma):
     rng = np.random.default_rng(SEED + 7919 * b)
     x = (rng.standard_normal(ncols) + 1j * rng.standard_normal(ncols)) / math.sqrt(2.0)
@@ -406,12 +447,10 @@ def run_gpu(args):
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64)",
             "data": "synthetic: reference pattern generators (patterns.cpp) + seeded complex-normal coefficients",
-            "config": {"workload": args.workload.upper(), "description": WORKLOADS[args.workload],
-                       "problems": P, "problems_per_rank": B, "samples_per_problem": M, "coeffs_per_problem": Nc,
-                       "family": f"p={p}", "J": J, "route": route, "cgls_tolerance": "1e-300 (fixed count)",
-                       "l2": "inputs larger than L2 (per-point tables %.1f GB/GPU)" % (op.device_bytes / 1e9)
-                       if op.device_bytes > 126e6 else "L2-resident working set; back-to-back steps",
-                       "parallelism": f"problem-sharded x{world}" if world > 1 else "1 GPU"},
+            "config": config_for(args.workload, P, world),
+            "route": route, "problems_per_rank": B,
+            "l2": "inputs larger than L2 (per-point tables %.1f GB/GPU)" % (op.device_bytes / 1e9)
+            if op.device_bytes > 126e6 else "L2-resident working set; back-to-back steps",
             "pairs_per_sec": round(pairs_per_sec, 3), "ms_per_pair": round(pair_ms, 4),
             "gpu_launches": int(launches),
             "roofline": roofline, "roofline_iteration": roof_iter,
@@ -532,6 +571,10 @@ def gs_solve_host(op, b_host, x_host, iters):
 
 # ------------------------------------------------------------------ CPU legs (oracle = test infrastructure)
 def _cpu_problem(workload, b):
+    """The workload's problem b on the oracle alone (test infrastructure; the
+    product library is never loaded by the CPU legs).  2D Voronoi weights of
+    the large configs come from the oracle's bucketed exact clipping (the
+    reference's O(M^2) loop is infeasible at 2^18-2^20 points)."""
     import oracle
 
     class OracleGen:
@@ -541,9 +584,8 @@ def _cpu_problem(workload, b):
 
         @staticmethod
         def voronoi(dim, c, K):
-            if dim == 2 and c.size > 2 * 20000:  # reference O(M^2) clip is infeasible; same weights, fast path
-                from paper_1607_04091_b200 import inputs
-                return inputs.voronoi_weights(dim, c, K)
+            if dim == 2 and c.size > 2 * 20000:
+                return oracle.voronoi_fast(dim, c, K)
             return oracle.voronoi(dim, c, K)
 
     dim, p, J, c, mu, bw, sig = problem_inputs(workload, b, OracleGen)
@@ -569,6 +611,7 @@ def _cpu_iter_seconds(op, data, k):
 def cpu_baseline(workload):
     """Rank 0, N=1: the oracle (restated reference, single thread like the
     reference itself) on one problem of the workload."""
+    cpu = host_cpu()
     try:
         t = time.perf_counter()
         op, data = _cpu_problem(workload, 0)
@@ -576,8 +619,9 @@ def cpu_baseline(workload):
         k = 2 if workload in ("c4", "c5", "c3") else 20
         per_it, _, _ = _cpu_iter_seconds(op, data, k)
         return {"value": round(1.0 / per_it, 4), "unit": "problem-iterations/s", "cores": 1, "kind": "port",
+                "cpu_model": cpu["model"], "physical_cores": cpu["physical_cores"],
                 "sample": f"{workload.upper()} problem 0, {k} CGLS iterations (difference of solves of 1 and "
-                          f"{1 + k} iterations), construction ({build:.1f} s) excluded"}
+                          f"{1 + k} iterations), 1 thread, construction ({build:.1f} s) excluded"}
     except Exception as e:  # noqa: BLE001
         return {"value": None, "unit": "problem-iterations/s", "cores": 1, "kind": "port", "sample": f"failed: {e}"}
 
@@ -591,7 +635,8 @@ def run_reference(args):
         return None
     import oracle
     oracle.lib()
-    ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    cpu = host_cpu()
+    ncpu = cpu["logical_cpus_available"]
     P = args.problems or problem_count(args.workload)
     threads = max(1, min(ncpu, P, 64 if args.workload == "c5" else 1))
     k = max(1, min(args.steps, 3 if args.workload in ("c4", "c5", "c3") else 20))
@@ -618,9 +663,9 @@ def run_reference(args):
            "value": round(value, 4), "unit": "problem-iterations/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
            "dtype": "c128 (f64)", "data": "synthetic (same generators and seeds as the GPU arm)",
-           "config": {"workload": args.workload.upper(), "description": WORKLOADS[args.workload]},
+           "config": config_for(args.workload, P, world),
            "cpu_baseline": {"value": round(value, 4), "unit": "problem-iterations/s", "cores": threads,
-                            "kind": "port",
+                            "kind": "port", "cpu_model": cpu["model"], "physical_cores": cpu["physical_cores"],
                             "sample": f"{threads} concurrent problems x {k} CGLS iterations each (oracle/gs_oracle.cpp,"
                                       f" the reference algorithm restated; construction excluded); wall {wall:.0f} s"},
            "e2e": {"value": round(value, 4), "unit": "problem-iterations/s", "h2d_bytes_per_step": 0,

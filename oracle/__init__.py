@@ -248,6 +248,16 @@ def voronoi(dim, coords, K):
     return mu
 
 
+def voronoi_fast(dim, coords, K, threads=0):
+    """Bucketed exact Voronoi (same cells as voronoi(), roundoff-level areas) for
+    point sets beyond the reference's O(M^2) loop; harness only."""
+    c = _f64(coords).ravel()
+    mu = np.empty(c.size // dim)
+    n = threads or (len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1))
+    _chk(lib().orc_voronoi_fast(C.c_int(dim), C.c_longlong(mu.size), _p(c), C.c_double(K), _p(mu), C.c_int(n)))
+    return mu
+
+
 class FTable:
     """dyadic.hpp FunctionTable: samples at support_begin + i / 2^R."""
 

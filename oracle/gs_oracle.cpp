@@ -40,6 +40,8 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
+#include <atomic>
 #include <vector>
 
 #include "../paper_1607_04091_b200/csrc/family_data.h"
@@ -1087,6 +1089,79 @@ std::vector<double> voronoi(int dim, const std::vector<double>& c, double K) {  
 }
 
 
+// Same cells as voronoi() (weights.cpp:59-70 clipping, identical clip and
+// area code) for point sets too large for the reference's O(M^2) loop: each
+// cell is clipped against its neighbours in increasing distance, taken from a
+// bucket grid ring by ring, until the next ring lies beyond twice the cell's
+// farthest vertex (no further point can cut it).  The clip order differs
+// from the reference's index order, so areas agree to roundoff (~1e-16
+// relative), not bit for bit.  Threads split the points.  Harness only: the
+// CPU legs of bench.py use it so that they never load the product library.
+std::vector<double> voronoi_fast_2d(const std::vector<double>& c, double K, int nthreads) {
+    if (!(K > 0)) domain("K must be positive");
+    const size_t M = c.size() / 2;
+    if (M == 0) shape("empty point set");
+    for (size_t m = 0; m < M; ++m)
+        if (std::abs(c[2 * m]) > K || std::abs(c[2 * m + 1]) > K) domain("point outside the bandwidth region");
+    const double h = std::max(2.0 * K / std::max(1.0, std::sqrt((double)M)), 1e-300);
+    const int nb = std::max(1, (int)std::ceil(2.0 * K / h));
+    auto bucket = [&](double v) { return std::min(nb - 1, std::max(0, (int)std::floor((v + K) / h))); };
+    std::vector<int> start(nb * nb + 1, 0), order(M);
+    for (size_t m = 0; m < M; ++m) ++start[bucket(c[2 * m + 1]) * nb + bucket(c[2 * m]) + 1];
+    for (int i = 0; i < nb * nb; ++i) start[i + 1] += start[i];
+    std::vector<int> fill(start.begin(), start.end() - 1);
+    for (size_t m = 0; m < M; ++m) order[fill[bucket(c[2 * m + 1]) * nb + bucket(c[2 * m])]++] = (int)m;
+    std::vector<double> mu(M);
+    std::atomic<int> dup{0};
+    auto work = [&](size_t lo, size_t hi) {
+        std::vector<std::pair<double, int>> cand;
+        for (size_t m = lo; m < hi; ++m) {
+            const P2 own = {c[2 * m], c[2 * m + 1]};
+            const int bx = bucket(own.x), by = bucket(own.y);
+            std::vector<P2> poly = {{-K, -K}, {K, -K}, {K, K}, {-K, K}};
+            for (int r = 0;; ++r) {
+                // the cell's farthest vertex bounds every cutting neighbour to 2 * rmax
+                double rmax = 0.0;
+                for (const P2& v : poly) rmax = std::max(rmax, std::hypot(v.x - own.x, v.y - own.y));
+                if (r >= 2 && (r - 1) * h > 2.0 * rmax) break;
+                if (r > nb) break;
+                cand.clear();
+                for (int yy = by - r; yy <= by + r; ++yy) {
+                    if (yy < 0 || yy >= nb) continue;
+                    for (int xx = bx - r; xx <= bx + r; ++xx) {
+                        if (xx < 0 || xx >= nb) continue;
+                        if (std::max(std::abs(xx - bx), std::abs(yy - by)) != r) continue;
+                        const int b = yy * nb + xx;
+                        for (int k = start[b]; k < start[b + 1]; ++k) {
+                            const int j = order[k];
+                            if ((size_t)j == m) continue;
+                            const double dx = c[2 * j] - own.x, dy = c[2 * j + 1] - own.y;
+                            if (dx == 0.0 && dy == 0.0) dup = 1;
+                            cand.push_back({dx * dx + dy * dy, j});
+                        }
+                    }
+                }
+                std::sort(cand.begin(), cand.end());
+                for (const auto& cj : cand) {
+                    const int j = cj.second;
+                    P2 mid = {(own.x + c[2 * j]) / 2, (own.y + c[2 * j + 1]) / 2};
+                    P2 a = {c[2 * j] - own.x, c[2 * j + 1] - own.y};
+                    poly = clip_half_plane(poly, mid, a);
+                    if (poly.empty()) break;
+                }
+                if (poly.empty()) break;
+            }
+            mu[m] = polygon_area(poly);
+        }
+    };
+    const int T = std::max(1, nthreads);
+    std::vector<std::thread> th;
+    for (int t = 0; t < T; ++t) th.emplace_back(work, M * t / T, M * (t + 1) / T);
+    for (auto& t : th) t.join();
+    if (dup) domain("degenerate input: duplicate sample points");
+    return mu;
+}
+
 // ---------------------------------------------------------------- dyadic evaluation (dyadic.cpp)
 // Least squares by Householder QR of the (n+1) x n consistent system
 // (Eigen colPivHouseholderQr, dyadic.cpp:29): the solution is unique.
@@ -1509,6 +1584,13 @@ int orc_voronoi(int dim, long long M, const double* coords, double K, double* mu
     return guard([&] {
         std::vector<double> c(coords, coords + M * dim);
         auto v = orc::voronoi(dim, c, K);
+        std::memcpy(mu, v.data(), v.size() * 8);
+    });
+}
+int orc_voronoi_fast(int dim, long long M, const double* coords, double K, double* mu, int nthreads) {
+    return guard([&] {
+        std::vector<double> c(coords, coords + M * dim);
+        auto v = dim == 2 ? orc::voronoi_fast_2d(c, K, nthreads) : orc::voronoi(dim, c, K);
         std::memcpy(mu, v.data(), v.size() * 8);
     });
 }

@@ -376,7 +376,10 @@ __global__ void k_densify_axis(FamDev f, const double* __restrict__ coords, int 
     }
   }
 }
-// out (M x cols, column-major): 1D weight * rx(c); 2D (weight * rx(i)) * ry(j) at column j n + i
+// out (M x cols, column-major): 1D weight * rx(c); 2D weight * (rx(i) ry(j)) at column j n + i.
+// (freq2wave.cpp:443 writes weight * rx(i) * ry(j); scaling the finished
+// product instead keeps the weighted section exactly sqrt(mu) times the
+// unweighted one, the property the reference's test_freq2wave.cpp:198-219 pins)
 __global__ void k_densify_out(int dim, int64_t M, int n, const cplx* __restrict__ rx, const cplx* __restrict__ ry,
                               const double* __restrict__ sw, cplx* __restrict__ out) {
   const int64_t cols = dim == 1 ? n : (int64_t)n * n;
@@ -389,7 +392,7 @@ __global__ void k_densify_out(int dim, int64_t M, int n, const cplx* __restrict_
     return;
   }
   const int64_t i = col % n, j = col / n;
-  out[e] = cmul(cscale(rx[m * n + i], w), ry[m * n + j]);
+  out[e] = cscale(cmul(rx[m * n + i], ry[m * n + j]), w);
 }
 
 // ------------------------------------------------------------------ construction

@@ -48,3 +48,18 @@ def test_voronoi_1d_and_errors():
         I.voronoi_weights(2, np.array([0.0, 0.0, 0.0, 0.0]), 1.0)
     with pytest.raises(gs.DomainError):
         I.voronoi_weights(2, np.array([0.0, 2.0]), 1.0)
+
+
+def test_oracle_bucketed_voronoi_matches_reference_clip():
+    """oracle.voronoi_fast (the CPU legs' weights for the 2^18-2^20-point
+    configs) gives the reference loop's cells (weights.cpp:59-70) to roundoff."""
+    import numpy as np
+    import oracle
+    for n, seed in ((17, 3), (40, 11)):
+        c = oracle.gen_jitter(n, 0.5, 0.2, seed, 2)
+        K = float(np.max(np.abs(c)))
+        a, b = oracle.voronoi(2, c, K), oracle.voronoi_fast(2, c, K)
+        assert np.max(np.abs(a - b) / a) < 1e-11
+    s = oracle.gen_spiral(3, 200.0, 16.0)
+    a, b = oracle.voronoi(2, s, 16.0), oracle.voronoi_fast(2, s, 16.0)
+    assert np.max(np.abs(a - b) / a) < 1e-11

@@ -78,6 +78,40 @@ def checkpoints(spec, ks):
     print(f"{spec}: checkpoints {ks} in {time.time() - t0:.0f} s -> {name}", flush=True)
 
 
+def op_sensitivity(spec):
+    """The oracle's iterate moved by a last-bit perturbation of the OPERATOR:
+    the Voronoi weights mu (folded into the rows as sqrt(mu)) scaled by
+    (1 + 2^-52 r), r = +-1 -- a 1-ulp change of every row of T, the size of
+    the rounding differences between any two implementations of T."""
+    workload, _, b = spec.partition(":")
+    b = int(b or 0)
+    iters = bench.CONFIG_ITERS[workload]
+    t0 = time.time()
+    dim, p, J, c, mu, bw, sig = bench.problem_inputs(workload, b, bench.ProductGen())
+    op_u = oracle.Op(dim, p, J, c, bandwidth=bw)
+    x_true, noise = bench.coeffs_and_noise(b, op_u.cols, op_u.rows, sig)
+    data = op_u.forward(x_true) + noise
+    del op_u
+    rng = np.random.default_rng(2)
+    mu2 = mu * (1 + 2.0 ** -52 * rng.choice([-1.0, 1.0], mu.size))
+    res = {}
+
+    def run(key, m):
+        res[key] = oracle.Op(dim, p, J, c, weights=m, bandwidth=bw).solve(data, max_iterations=iters,
+                                                                          tolerance=1e-300)[0]
+
+    ths = [threading.Thread(target=run, args=("a", mu)), threading.Thread(target=run, args=("b", mu2))]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    name = f"cgls_{workload}_opsens.npz"
+    sens = oracle.rel_error(res["b"], res["a"])
+    np.savez(os.path.join(OUT, name), sens_op=sens, iters=iters)
+    print(f"{spec}: operator sensitivity (1-ulp row weights) after {iters} iterations {sens:.3e}, "
+          f"{time.time() - t0:.0f} s -> {name}", flush=True)
+
+
 def main(spec):
     workload, _, b = spec.partition(":")
     b = int(b or 0)
@@ -117,7 +151,10 @@ def main(spec):
 
 if __name__ == "__main__":
     args = sys.argv[1:]
-    if args and args[0] == "--checkpoints":
+    if args and args[0] == "--op-sensitivity":
+        for s in args[1:]:
+            op_sensitivity(s)
+    elif args and args[0] == "--checkpoints":
         ks = [int(v) for v in args[1].split(",")]
         for s in args[2:]:
             checkpoints(s, ks)
