@@ -94,6 +94,8 @@ FamDev make_family(int p) {
 
 }  // namespace
 
+#include "general_route.cuh"
+
 // ====================================================================== op
 struct gs_op {
   gs_op_desc d{};
@@ -133,6 +135,8 @@ struct gs_op {
   // workspace
   DBuf<cplx> G, lines, TB, TL, TLF, TC, TCF, W;
   DBuf<cplx> EP;  // 1D route: per-CTA edge-sum partials of k_n1_spread
+  bool general = false;  // general route (general_route.cuh): caller-order samples, plan-based T / T*
+  GeneralRoute gen;
   DBuf<double> nd_pts;  // NDFT_1D route: wrapped scaled points (caller order)
   DBuf<cplx> nd_part;   // NDFT_1D route: split partial sums
   DBuf<cplx> stage_a, stage_b;
@@ -477,10 +481,10 @@ gs_op* create(const gs_op_desc* dsc) {
       else if (e != eps0) uni = false;
     }
     if (uni) {
-      try {  // DFT lengths this build's uniform kernels cannot hold take the NFFT route
+      try {  // DFT lengths the fused single-CTA kernels cannot hold take the general uniform route
         op->up = make_uni(op.get(), M, eps0);
       } catch (const GsError&) {
-        uni = false;
+        op->general = true;
       }
     }
     op->route = uni ? GS_ROUTE_UNIFORM_1D : (d.exact_ndft ? GS_ROUTE_NDFT_1D : GS_ROUTE_NFFT_1D);
@@ -529,7 +533,14 @@ gs_op* create(const gs_op_desc* dsc) {
 
   // ---- per-route construction, all per-point work on the device
   DBuf<double> d_xi_x, d_xi_y, d_sw;
-  if (op->route == GS_ROUTE_UNIFORM_1D) {
+  if (op->route == GS_ROUTE_UNIFORM_1D && op->general) {
+    op->gen.uni = uniform_build(M, op->uniform_eps, op->n, (int)B);  // uniform_ndft_fft at any length
+    d_xi_x.upload(xi_x.data(), total, st);
+    if (op->weighted) op->sqrtw.upload(sw.data(), total, st);
+    op->rec_u.alloc(total * op->Rr);
+    build_factors(op.get(), d_xi_x.p, op->weighted ? op->sqrtw.p : nullptr, total, op->rec_u.p, st);
+    CK(cudaStreamSynchronize(st));
+  } else if (op->route == GS_ROUTE_UNIFORM_1D) {
     attach_phases(op->up, op->ph_u, st);
     make_twiddles(op.get(), op->up.N2, st);
     d_xi_x.upload(xi_x.data(), total, st);
@@ -575,10 +586,53 @@ gs_op* create(const gs_op_desc* dsc) {
     const int w = d.w > 0 ? d.w : 6;
     if (sigma < 1.25) fail(GS_ERR_DOMAIN, "oversampling factor must be >= 1.25");
     if (w < 2) fail(GS_ERR_DOMAIN, "kernel half-width must be >= 2");
-    if (2 * w + 1 > 16) fail(GS_ERR_DOMAIN, "kernel half-width > 7 unsupported on this build");
     const int n_ov = (int)std::ceil(sigma * (double)op->n / 2.0) * 2;
-    if (!is_pow2(n_ov)) fail(GS_ERR_DOMAIN, "oversampled length must be a power of two on this build");
-    if (n_ov > 4096) fail(GS_ERR_DOMAIN, "oversampled length > 4096 unsupported on this build");
+    if (!is_pow2(n_ov) || n_ov > 4096 || 2 * w + 1 > 16) {
+      // option values the fused gridding kernels do not take: the general route
+      op->general = true;
+      op->np.n = (int)op->n;
+      op->np.n_ov = n_ov;
+      op->np.p = op->p;
+      op->np.edges = op->edges;
+      op->np.S = 2 * w + 1;
+      op->np.M = M;
+      std::vector<double> zx(total), zy(d.dim == 2 ? total : 0);
+      for (int64_t i = 0; i < total; ++i) zx[i] = wrap_half_open(std::ldexp(xi_x[i], -d.J));
+      for (int64_t i = 0; i < (int64_t)zy.size(); ++i) zy[i] = wrap_half_open(std::ldexp(xi_y[i], -d.J));
+      const int e = op->edges ? op->p : 0;
+      const int Nn[2] = {(int)op->n, (int)op->n};
+      if (d.dim == 1) {
+        op->gen.px = nfft_plan_build(1, Nn, M, (int)B, zx.data(), sigma, w, st);
+      } else {
+        std::vector<double> pts(2 * total);  // 2D plan axes: 0 = y, 1 = x (freq2wave.cpp:183-190)
+        for (int64_t i = 0; i < total; ++i) {
+          pts[2 * i] = zy[i];
+          pts[2 * i + 1] = zx[i];
+        }
+        op->gen.p2 = nfft_plan_build(2, Nn, M, (int)B, pts.data(), sigma, w, st);
+        if (op->edges) {
+          op->gen.px = nfft_plan_build(1, Nn, M, (int)B, zx.data(), sigma, w, st, 2 * op->p);
+          op->gen.py = nfft_plan_build(1, Nn, M, (int)B, zy.data(), sigma, w, st, 2 * op->p);
+        }
+      }
+      NfftPlanDev* core = d.dim == 1 ? op->gen.px.get() : op->gen.p2.get();
+      if (op->edges) {
+        core->lo = e;
+        core->hi = (int)op->n - e;
+      }
+      d_xi_x.upload(xi_x.data(), total, st);
+      if (op->weighted) op->sqrtw.upload(sw.data(), total, st);
+      op->rec_x.alloc(total * op->Rr);
+      build_factors(op.get(), d_xi_x.p, op->weighted ? op->sqrtw.p : nullptr, total, op->rec_x.p, st);
+      if (d.dim == 2) {
+        d_xi_y.upload(xi_y.data(), total, st);
+        op->rec_y.alloc(total * op->Rr);
+        build_factors(op.get(), d_xi_y.p, nullptr, total, op->rec_y.p, st);
+      }
+      CK(cudaStreamSynchronize(st));
+      CKL();
+      return op.release();
+    }
     {
       double width = 2.0 * w;
       double t = (width / sigma) * (width / sigma) * (sigma - 0.5) * (sigma - 0.5) - 0.8;
@@ -826,6 +880,80 @@ bool spread_mma() {
 }
 
 
+
+// ------------------------------------------------------------------ general routes (general_route.cuh)
+void general_forward(gs_op* op, const cplx* x, cplx* y, cudaStream_t st) {
+  GeneralRoute& G = op->gen;
+  const int B = op->B, n = (int)op->n, p = op->p, e = op->edges ? p : 0;
+  const int64_t M = op->M;
+  if (op->dim == 1) {
+    G.u.alloc((size_t)B * M);
+    if (G.uni) uniform_forward(*G.uni, x, e, n - e, G.u.p, st);
+    else nfft_plan_forward(*G.px, x, G.u.p, st);
+    op1d_epilogue_launch(M, B, G.u.p, op->route == GS_ROUTE_UNIFORM_1D ? op->rec_u.p : op->rec_x.p, p, op->edges, x,
+                         n, y, st);
+    return;
+  }
+  const int E = op->edges ? 2 * p : 0;
+  G.u.alloc((size_t)B * M);
+  nfft_plan_forward(*G.p2, x, G.u.p, st);
+  if (E) {
+    G.ly.alloc((size_t)B * E * n);
+    G.lx.alloc((size_t)B * E * n);
+    G.uy.alloc((size_t)B * E * M);
+    G.ux.alloc((size_t)B * E * M);
+    k_g2_lines_in<<<dim3(nblk((int64_t)E * n, 256), B), 256, 0, st>>>(n, p, x, G.ly.p, G.lx.p);
+    pmark("k_g2_lines_in", st);
+    nfft_plan_forward(*G.py, G.ly.p, G.uy.p, st);
+    nfft_plan_forward(*G.px, G.lx.p, G.ux.p, st);
+  }
+  k_g2_fwd_combine<<<dim3(nblk(M, 128), B), 128, 0, st>>>(M, n, op->edges ? p : 1, op->Rr, op->rec_x.p, op->rec_y.p,
+                                                           G.u.p, G.uy.p, G.ux.p, x, y);
+  pmark("k_g2_fwd_combine", st);
+  CKL();
+}
+
+void general_adjoint(gs_op* op, const cplx* y, cplx* z, cudaStream_t st) {
+  GeneralRoute& G = op->gen;
+  const int B = op->B, n = (int)op->n, p = op->p;
+  const int64_t M = op->M;
+  if (op->dim == 1) {
+    const cplx* rec = op->route == GS_ROUTE_UNIFORM_1D ? op->rec_u.p : op->rec_x.p;
+    G.v.alloc((size_t)B * M);
+    k_g_conjd<<<dim3(nblk(M, 256), B), 256, 0, st>>>(M, op->Rr, rec, y, G.v.p);
+    pmark("k_g_conjd", st);
+    if (G.uni) uniform_adjoint(*G.uni, G.v.p, z, st);
+    else nfft_plan_adjoint(*G.px, G.v.p, z, st);
+    if (op->edges) op1d_edges_launch(M, B, rec, p, y, n, z, st);
+    CKL();
+    return;
+  }
+  const int E = op->edges ? 2 * p : 0;
+  G.v.alloc((size_t)B * M);
+  G.u.alloc(std::max((size_t)B * M, (size_t)B * n * n));
+  if (E) {
+    G.uy.alloc((size_t)B * E * M);
+    G.ux.alloc((size_t)B * E * M);
+    G.ly.alloc((size_t)B * E * n);
+    G.lx.alloc((size_t)B * E * n);
+  }
+  k_g2_adj_prep<<<dim3(nblk(M, 128), B), 128, 0, st>>>(M, op->edges ? p : 0, op->Rr, op->rec_x.p, op->rec_y.p, y,
+                                                        G.v.p, G.uy.p, G.ux.p);
+  pmark("k_g2_adj_prep", st);
+  nfft_plan_adjoint(*G.p2, G.v.p, G.u.p, st);  // W
+  if (E) {
+    nfft_plan_adjoint(*G.py, G.uy.p, G.ly.p, st);  // side lines along y (x-edge rows)
+    nfft_plan_adjoint(*G.px, G.ux.p, G.lx.p, st);  // side lines along x (y-edge columns)
+  }
+  k_g2_adj_assemble<<<dim3(nblk((int64_t)n * n, 256), B), 256, 0, st>>>(n, op->edges ? p : 1, G.u.p, G.ly.p, G.lx.p, z);
+  pmark("k_g2_adj_assemble", st);
+  if (E) {
+    k_g2_adj_corners<<<dim3(E * E, B), 256, 0, st>>>(M, n, p, op->Rr, op->rec_x.p, op->rec_y.p, y, z);
+    pmark("k_g2_adj_corners", st);
+  }
+  CKL();
+}
+
 // ------------------------------------------------------------------ applies
 // x, y are device pointers; perm_io: samples in the caller's order (true) or
 // the internal bin-sorted order (false, used inside CGLS).
@@ -836,6 +964,10 @@ bool spread_mma() {
 void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t st, double* npart = nullptr,
                  const N1QStep* n1q = nullptr, const UniPre* pre_a = nullptr) {
   const int B = op->B;
+  if (op->general) {
+    general_forward(op, x, y, st);
+    return;
+  }
   switch (op->route) {
     case GS_ROUTE_UNIFORM_1D: {
       const UniP& P = op->up;
@@ -948,6 +1080,10 @@ bool adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
                  const UniPre* pre_b = nullptr) {
   bool fused_sstep = false;
   const int B = op->B;
+  if (op->general) {
+    general_adjoint(op, y, z, st);
+    return false;
+  }
   switch (op->route) {
     case GS_ROUTE_UNIFORM_1D: {
       const UniP& P = op->up;
@@ -1158,7 +1294,7 @@ void session_begin(Session& S, gs_op* op, const cplx* b_raw, bool b_perm, const 
   if (op->route == GS_ROUTE_NFFT_1D) S.vpart.alloc((size_t)S.B * ((S.M + 127) / 128));  // interpolation CTAs
   S.hist.alloc((size_t)S.B * hist_cap);
   S.flag.alloc(1);
-  const bool sorted = op->route == GS_ROUTE_NFFT_1D || op->route == GS_ROUTE_NFFT_2D;
+  const bool sorted = !op->general && (op->route == GS_ROUTE_NFFT_1D || op->route == GS_ROUTE_NFFT_2D);
   // b = sqrt(mu) o b_raw in internal order (solver.cpp:30-33); the tensor route
   // applies sqrt(mu) inside T, so it takes the raw data scaled here as well.
   k_gather_scale<<<nblk(TM, 256), 256, 0, st>>>(b_raw, (sorted && b_perm) ? op->perm.p : nullptr,
@@ -1192,7 +1328,7 @@ bool cg_fused_enabled() {  // GS_B200_CG_FUSED=0: the generic multi-kernel itera
 void session_iterate_body(Session& S, cudaStream_t st) {
   gs_op* op = S.op;
   const int64_t TM = S.M * S.B, TN = S.Nc * S.B;
-  if (op->route == GS_ROUTE_UNIFORM_1D && cg_fused_enabled()) {  // whole iteration in one launch
+  if (op->route == GS_ROUTE_UNIFORM_1D && !op->general && cg_fused_enabled()) {  // whole iteration in one launch
     const UniP& P = op->up;
     const size_t rs = uni_cg_resident_smem(P, op->Rr);
     k_uni_cgls_iter<<<S.B, UNI_CG_THREADS, rs ? rs : uni_smem_tw(P), st>>>(
@@ -1202,7 +1338,7 @@ void session_iterate_body(Session& S, cudaStream_t st) {
     CKL();
     return;
   }
-  if (op->route == GS_ROUTE_NFFT_1D && cg_fused_enabled()) {
+  if (op->route == GS_ROUTE_NFFT_1D && !op->general && cg_fused_enabled()) {
     // 4 launches: embed+FFT, interpolation (+ deferred r update, ||q||^2 partials),
     // spreading (+ q-step), inverse FFT (+ s-step)
     const N1QStep q1{S.vpart.p, (int)((S.M + 127) / 128), S.q.p, S.r.p, S.st.p, S.x.p, S.p.p};
@@ -1284,7 +1420,7 @@ bool graphs_enabled() {
 void session_iterate(Session& S, cudaStream_t st, int k) {
   if (k <= 0) return;
   S.it += k;
-  if (S.op->route == GS_ROUTE_UNIFORM_1D && cg_fused_enabled() && !g_prof.on) {
+  if (S.op->route == GS_ROUTE_UNIFORM_1D && !S.op->general && cg_fused_enabled() && !g_prof.on) {
     // all k iterations in one launch (k_uni_cgls_iter loops on the device)
     const UniP& P = S.op->up;
     const size_t rs = uni_cg_resident_smem(P, S.op->Rr);
@@ -1622,9 +1758,9 @@ int gs_op_export_factors(gs_op* op, int b, int axis, double* D, double* L, doubl
     const int64_t M = op->M;
     const int Rr = op->Rr, p = op->p;
     std::vector<cplx> recs(M * Rr);  // per point in the caller's order
-    if (op->route == GS_ROUTE_UNIFORM_1D || op->route == GS_ROUTE_NDFT_1D) {  // caller order already
-      CK(cudaMemcpy(recs.data(), (op->route == GS_ROUTE_UNIFORM_1D ? op->rec_u.p : op->rec_x.p) + b * M * Rr,
-                    M * Rr * sizeof(cplx), cudaMemcpyDeviceToHost));
+    if (op->route == GS_ROUTE_UNIFORM_1D || op->route == GS_ROUTE_NDFT_1D || op->general) {  // caller order already
+      const cplx* src = op->route == GS_ROUTE_UNIFORM_1D ? op->rec_u.p : (axis == 0 ? op->rec_x.p : op->rec_y.p);
+      CK(cudaMemcpy(recs.data(), src + b * M * Rr, M * Rr * sizeof(cplx), cudaMemcpyDeviceToHost));
     } else if (op->route == GS_ROUTE_TENSOR_2D) {
       const int64_t Ma = op->Ma, Mb = op->Mb;
       const int64_t Ml = axis == 0 ? Ma : Mb;

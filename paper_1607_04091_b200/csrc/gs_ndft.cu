@@ -81,6 +81,19 @@ void ndft_adjoint_launch(const NdftShape& s, const double* pts, const cplx* y, c
   CKL();
 }
 
+void op1d_epilogue_launch(int64_t M, int batch, const cplx* u, const cplx* rec, int p, int edges, const cplx* x, int n,
+                          cplx* y, cudaStream_t st) {
+  k_ndft_fwd_reduce<<<dim3(nblk(M * 32, 256), batch), 256, 0, st>>>(M, 1, u, rec, p, edges, x, n, y);
+  pmark("k_op1d_epilogue", st);
+  CKL();
+}
+
+void op1d_edges_launch(int64_t M, int batch, const cplx* rec, int p, const cplx* y, int n, cplx* z, cudaStream_t st) {
+  k_ndft_adj_edges<<<dim3(2 * p, batch), 256, 0, st>>>(M, rec, p, y, n, z);
+  pmark("k_op1d_edges", st);
+  CKL();
+}
+
 }  // namespace gsb
 
 using namespace gsb;

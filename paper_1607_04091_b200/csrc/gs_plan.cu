@@ -170,12 +170,13 @@ void nfft_plan_validate(int dim, const int* N, int64_t M, int batch, const doubl
 }
 
 std::unique_ptr<NfftPlanDev> nfft_plan_build(int dim, const int* N, int64_t M, int batch, const double* h_points,
-                                             double sigma, int w, cudaStream_t st) {
+                                             double sigma, int w, cudaStream_t st, int vps) {
   nfft_plan_validate(dim, N, M, batch, h_points, sigma, w);
   const int64_t cnt = M * dim * batch;
   auto P = std::make_unique<NfftPlanDev>();
   P->dim = dim;
   P->batch = batch;
+  P->vps = vps;
   P->M = M;
   P->w = w;
   P->S = 2 * w + 1;
@@ -204,7 +205,7 @@ std::unique_ptr<NfftPlanDev> nfft_plan_build(int dim, const int* N, int64_t M, i
     double one = 1.0;
     P->dec1.upload(&one, 1, st);
   }
-  P->G.alloc((size_t)batch * P->over_size());
+  P->G.alloc((size_t)batch * vps * P->over_size());
   P->f0 = std::make_unique<FftG>(P->nov[0]);
   if (dim == 2) P->f1 = std::make_unique<FftG>(P->nov[1]);
   CK(cudaStreamSynchronize(st));
@@ -221,28 +222,32 @@ PlanDev pdev(const NfftPlanDev& P) {
   d.n1 = P.dim == 2 ? P.nov[1] : 1;
   d.S = P.S;
   d.M = P.M;
+  d.vps = P.vps;
+  d.lo = P.hi >= 0 ? P.lo : 0;
+  d.hi = P.hi >= 0 ? P.hi : (P.dim == 2 ? std::max(P.N[0], P.N[1]) : P.N[0]);
   return d;
 }
 void grid_fft(NfftPlanDev& P, int sign, cudaStream_t st) {
   const int64_t over = P.over_size();
+  const int64_t nv = (int64_t)P.batch * P.vps;
   if (P.dim == 1) {
-    P.f0->run1d(P.G.p, P.G.p, P.batch, sign, st);
+    P.f0->run1d(P.G.p, P.G.p, nv, sign, st);
     return;
   }
   const int n0 = P.nov[0], n1 = P.nov[1];
   // rows (last axis, contiguous) then columns (stride n1): FFTW's 2D c2c
-  P.f1->run(P.G.p, P.G.p, n0, P.batch, n1, 1, over, n1, 1, over, sign, st);
-  P.f0->run(P.G.p, P.G.p, n1, P.batch, 1, n1, over, 1, n1, over, sign, st);
+  P.f1->run(P.G.p, P.G.p, n0, nv, n1, 1, over, n1, 1, over, sign, st);
+  P.f0->run(P.G.p, P.G.p, n1, nv, 1, n1, over, 1, n1, over, sign, st);
 }
 }  // namespace
 
 void nfft_plan_forward(NfftPlanDev& P, const cplx* x, cplx* y, cudaStream_t st) {
   const PlanDev d = pdev(P);
   CK(cudaMemsetAsync(P.G.p, 0, P.G.bytes(), st));
-  k_plan_embed<<<dim3(nblk(P.grid_size(), 256), P.batch), 256, 0, st>>>(d, x, P.dec0.p, P.dec1.p, P.G.p);
+  k_plan_embed<<<dim3(nblk(P.grid_size(), 256), P.batch * P.vps), 256, 0, st>>>(d, x, P.dec0.p, P.dec1.p, P.G.p);
   pmark("k_plan_embed", st);
   grid_fft(P, -1, st);
-  k_plan_interp<<<dim3(nblk(P.M, 128), P.batch), 128, 0, st>>>(d, P.base.p, P.wts.p, P.G.p, y);
+  k_plan_interp<<<dim3(nblk(P.M, 128), P.batch * P.vps), 128, 0, st>>>(d, P.base.p, P.wts.p, P.G.p, y);
   pmark("k_plan_interp", st);
   CKL();
 }
@@ -250,11 +255,105 @@ void nfft_plan_forward(NfftPlanDev& P, const cplx* x, cplx* y, cudaStream_t st) 
 void nfft_plan_adjoint(NfftPlanDev& P, const cplx* y, cplx* z, cudaStream_t st) {
   const PlanDev d = pdev(P);
   CK(cudaMemsetAsync(P.G.p, 0, P.G.bytes(), st));
-  k_plan_spread<<<dim3(nblk(P.M, 128), P.batch), 128, 0, st>>>(d, P.base.p, P.wts.p, y, P.G.p);
+  k_plan_spread<<<dim3(nblk(P.M, 128), P.batch * P.vps), 128, 0, st>>>(d, P.base.p, P.wts.p, y, P.G.p);
   pmark("k_plan_spread", st);
   grid_fft(P, +1, st);
-  k_plan_crop<<<dim3(nblk(P.grid_size(), 256), P.batch), 256, 0, st>>>(d, P.G.p, P.dec0.p, P.dec1.p, z);
+  k_plan_crop<<<dim3(nblk(P.grid_size(), 256), P.batch * P.vps), 256, 0, st>>>(d, P.G.p, P.dec0.p, P.dec1.p, z);
   pmark("k_plan_crop", st);
+  CKL();
+}
+
+
+// ------------------------------------------------------------------ uniform reduction, any length
+__global__ void k_uni_embed(const cplx* __restrict__ x, int64_t n1, int64_t q, double phase_step, int64_t n2,
+                            cplx* __restrict__ z, int lo, int hi) {
+  // z[q l] = x_l e^{i phase_step l} (nufft.cpp:410-415), zeros elsewhere; batch = blockIdx.y
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n2) return;
+  x += (int64_t)blockIdx.y * n1;
+  z += (int64_t)blockIdx.y * n2;
+  cplx v = mk(0, 0);
+  if (i % q == 0 && i / q < n1 && i / q >= lo && i / q < hi) {
+    const int64_t l = i / q;
+    double s, c;
+    sincos(phase_step * (double)l, &s, &c);
+    v = cmul(x[l], mk(c, s));
+  }
+  z[i] = v;
+}
+__global__ void k_uni_out(const cplx* __restrict__ t, int64_t M, double eps, int64_t N, int64_t n1, cplx* __restrict__ y,
+                          int64_t n2) {
+  // y_m = e^{i pi n1 xi_m} FFT(z)_m, xi_m = eps / N (m - M/2) (nufft.cpp:421-427)
+  const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  t += (int64_t)blockIdx.y * n2;
+  y += (int64_t)blockIdx.y * M;
+  const double xi = eps / (double)N * ((double)m - (double)M / 2.0);
+  double s, c;
+  sincos(GS_PI * (double)n1 * xi, &s, &c);
+  y[m] = cmul(mk(c, s), t[m]);
+}
+__global__ void k_uni_adj_in(const cplx* __restrict__ y, int64_t M, double eps, int64_t N, int64_t n2,
+                             cplx* __restrict__ z) {
+  // padded[m] = y_m e^{-i pi N xi_m} (nufft.cpp:438-444), zeros past M
+  const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (m >= n2) return;
+  y += (int64_t)blockIdx.y * M;
+  z += (int64_t)blockIdx.y * n2;
+  cplx v = mk(0, 0);
+  if (m < M) {
+    const double xi = eps / (double)N * ((double)m - (double)M / 2.0);
+    double s, c;
+    sincos(-GS_PI * (double)N * xi, &s, &c);
+    v = cmul(y[m], mk(c, s));
+  }
+  z[m] = v;
+}
+__global__ void k_uni_adj_out(const cplx* __restrict__ t, int64_t q, double phase_step, int64_t N, cplx* __restrict__ out,
+                              int64_t n2) {
+  // out_l = FFT+(padded)[q l] e^{-i phase_step l} (nufft.cpp:452-456)
+  const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (l >= N) return;
+  t += (int64_t)blockIdx.y * n2;
+  out += (int64_t)blockIdx.y * N;
+  double s, c;
+  sincos(-phase_step * (double)l, &s, &c);
+  out[l] = cmul(t[q * l], mk(c, s));
+}
+
+
+std::unique_ptr<UniformDev> uniform_build(int64_t M, double eps, int64_t N, int batch) {
+  const UniSetup s = uniform_setup(M, eps, N);
+  if (s.n2 > (int64_t)INT32_MAX) fail(GS_ERR_DOMAIN, "DFT length too large");
+  auto U = std::make_unique<UniformDev>();
+  U->M = M;
+  U->N = N;
+  U->eps = eps;
+  U->q = s.q;
+  U->n2 = s.n2;
+  U->batch = batch;
+  U->fft = std::make_unique<FftG>((int)s.n2);
+  U->z.alloc((size_t)batch * s.n2);
+  return U;
+}
+
+void uniform_forward(UniformDev& U, const cplx* x, int lo, int hi, cplx* y, cudaStream_t st) {
+  const double phase_step = GS_PI * U.eps * (double)U.M / (double)U.N;  // nufft.cpp:412
+  k_uni_embed<<<dim3(nblk(U.n2, 256), U.batch), 256, 0, st>>>(x, U.N, U.q, phase_step, U.n2, U.z.p, lo, hi);
+  pmark("k_uni_embed", st);
+  U.fft->run1d(U.z.p, U.z.p, U.batch, -1, st);
+  k_uni_out<<<dim3(nblk(U.M, 256), U.batch), 256, 0, st>>>(U.z.p, U.M, U.eps, U.N, U.N, y, U.n2);
+  pmark("k_uni_out", st);
+  CKL();
+}
+
+void uniform_adjoint(UniformDev& U, const cplx* y, cplx* z, cudaStream_t st) {
+  const double phase_step = GS_PI * U.eps * (double)U.M / (double)U.N;
+  k_uni_adj_in<<<dim3(nblk(U.n2, 256), U.batch), 256, 0, st>>>(y, U.M, U.eps, U.N, U.n2, U.z.p);
+  pmark("k_uni_adj_in", st);
+  U.fft->run1d(U.z.p, U.z.p, U.batch, +1, st);
+  k_uni_adj_out<<<dim3(nblk(U.N, 256), U.batch), 256, 0, st>>>(U.z.p, U.q, phase_step, U.N, z, U.n2);
+  pmark("k_uni_adj_out", st);
   CKL();
 }
 
@@ -272,52 +371,6 @@ struct gs_nfft_plan {
 
 namespace plan_capi {
 
-__global__ void k_uni_embed(const cplx* __restrict__ x, int64_t n1, int64_t q, double phase_step, int64_t n2,
-                            cplx* __restrict__ z) {
-  // z[q l] = x_l e^{i phase_step l} (nufft.cpp:410-415), zeros elsewhere
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n2) return;
-  cplx v = mk(0, 0);
-  if (i % q == 0 && i / q < n1) {
-    const int64_t l = i / q;
-    double s, c;
-    sincos(phase_step * (double)l, &s, &c);
-    v = cmul(x[l], mk(c, s));
-  }
-  z[i] = v;
-}
-__global__ void k_uni_out(const cplx* __restrict__ t, int64_t M, double eps, int64_t N, int64_t n1, cplx* __restrict__ y) {
-  // y_m = e^{i pi n1 xi_m} FFT(z)_m, xi_m = eps / N (m - M/2) (nufft.cpp:421-427)
-  const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (m >= M) return;
-  const double xi = eps / (double)N * ((double)m - (double)M / 2.0);
-  double s, c;
-  sincos(GS_PI * (double)n1 * xi, &s, &c);
-  y[m] = cmul(mk(c, s), t[m]);
-}
-__global__ void k_uni_adj_in(const cplx* __restrict__ y, int64_t M, double eps, int64_t N, int64_t n2,
-                             cplx* __restrict__ z) {
-  // padded[m] = y_m e^{-i pi N xi_m} (nufft.cpp:438-444), zeros past M
-  const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (m >= n2) return;
-  cplx v = mk(0, 0);
-  if (m < M) {
-    const double xi = eps / (double)N * ((double)m - (double)M / 2.0);
-    double s, c;
-    sincos(-GS_PI * (double)N * xi, &s, &c);
-    v = cmul(y[m], mk(c, s));
-  }
-  z[m] = v;
-}
-__global__ void k_uni_adj_out(const cplx* __restrict__ t, int64_t q, double phase_step, int64_t N, cplx* __restrict__ out) {
-  // out_l = FFT+(padded)[q l] e^{-i phase_step l} (nufft.cpp:452-456)
-  const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (l >= N) return;
-  double s, c;
-  sincos(-phase_step * (double)l, &s, &c);
-  out[l] = cmul(t[q * l], mk(c, s));
-}
-
 // host or device vector -> device pointer (staged copy in `buf` when host)
 const cplx* dev_in(const double* p, int64_t n, DBuf<cplx>& buf, cudaStream_t st) {
   if (is_device_ptr(p)) return (const cplx*)p;
@@ -331,31 +384,29 @@ int uniform_call(bool adjoint, const double* in, int64_t in_len, int64_t M, doub
     if (!in || !out) fail(GS_ERR_USAGE, "null argument");
     cudaStream_t st = (cudaStream_t)stream;
     if (!adjoint && in_len > N) fail(GS_ERR_DOMAIN, "signal length must not exceed N");
-    const UniSetup s = uniform_setup(adjoint ? in_len : M, eps, N);
-    if (s.n2 > (int64_t)INT32_MAX) fail(GS_ERR_DOMAIN, "DFT length too large");
-    thread_local DBuf<cplx> t_in, t_z, t_out;
-    FftG fft((int)s.n2);
+    auto U = uniform_build(adjoint ? in_len : M, eps, N, 1);
+    thread_local DBuf<cplx> t_in, t_x, t_out;
     const cplx* din = dev_in(in, in_len, t_in, st);
-    t_z.alloc(s.n2);
     const int64_t out_len = adjoint ? N : M;
     const bool dev_out = is_device_ptr(out);
     if (!dev_out) t_out.alloc(out_len);
     cplx* dout = dev_out ? (cplx*)out : t_out.p;
-    const double phase_step = GS_PI * eps * (double)(adjoint ? in_len : M) / (double)N;
     if (!adjoint) {
-      k_uni_embed<<<nblk(s.n2, 256), 256, 0, st>>>(din, in_len, s.q, phase_step, s.n2, t_z.p);
+      // x shorter than N: zero-extend (nufft.cpp:408-415 embeds only l < n1, and the
+      // output phase uses n1, not N)
+      t_x.alloc(N);
+      CK(cudaMemsetAsync(t_x.p, 0, N * sizeof(cplx), st));
+      CK(cudaMemcpyAsync(t_x.p, din, in_len * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+      const double phase_step = GS_PI * eps * (double)M / (double)N;
+      k_uni_embed<<<dim3(nblk(U->n2, 256), 1), 256, 0, st>>>(t_x.p, N, U->q, phase_step, U->n2, U->z.p, 0, (int)in_len);
       pmark("k_uni_embed", st);
-      fft.run1d(t_z.p, t_z.p, 1, -1, st);
-      k_uni_out<<<nblk(M, 256), 256, 0, st>>>(t_z.p, M, eps, N, in_len, dout);
+      U->fft->run1d(U->z.p, U->z.p, 1, -1, st);
+      k_uni_out<<<dim3(nblk(M, 256), 1), 256, 0, st>>>(U->z.p, M, eps, N, in_len, dout, U->n2);
       pmark("k_uni_out", st);
+      CKL();
     } else {
-      k_uni_adj_in<<<nblk(s.n2, 256), 256, 0, st>>>(din, in_len, eps, N, s.n2, t_z.p);
-      pmark("k_uni_adj_in", st);
-      fft.run1d(t_z.p, t_z.p, 1, +1, st);
-      k_uni_adj_out<<<nblk(N, 256), 256, 0, st>>>(t_z.p, s.q, phase_step, N, dout);
-      pmark("k_uni_adj_out", st);
+      uniform_adjoint(*U, din, dout, st);
     }
-    CKL();
     if (!dev_out) CK(cudaMemcpyAsync(out, dout, out_len * sizeof(cplx), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
   });

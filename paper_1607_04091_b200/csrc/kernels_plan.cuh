@@ -14,6 +14,8 @@ struct PlanDev {
   int n0, n1;      // oversampled lengths (n1 = 1 in 1D)
   int S;           // 2w + 1
   int64_t M;
+  int vps;         // vectors per point set: blockIdx.y = set * vps + vector
+  int lo, hi;      // embed mask: mode indices [lo, hi) of every axis enter (operator interiors); 0, N
 };
 
 // deconvolve and embed I_N into the zeroed oversampled grid (nufft.cpp:247-265)
@@ -27,12 +29,14 @@ __global__ void k_plan_embed(PlanDev P, const cplx* __restrict__ x, const double
   G += (int64_t)b * P.n0 * P.n1;
   if (P.dim == 1) {
     const int k = (int)idx - P.N0 / 2;
-    G[(k + P.n0) % P.n0] = cscale(x[idx], dec0[idx]);
+    const bool in = idx >= P.lo && idx < P.hi;
+    G[(k + P.n0) % P.n0] = in ? cscale(x[idx], dec0[idx]) : mk(0, 0);
     return;
   }
   const int i0 = (int)(idx / P.N1), i1 = (int)(idx % P.N1);
   const int k0 = i0 - P.N0 / 2, k1 = i1 - P.N1 / 2;
-  G[(int64_t)((k0 + P.n0) % P.n0) * P.n1 + (k1 + P.n1) % P.n1] = cscale(x[idx], dec0[i0] * dec1[i1]);
+  const bool in = i0 >= P.lo && i0 < P.hi && i1 >= P.lo && i1 < P.hi;
+  G[(int64_t)((k0 + P.n0) % P.n0) * P.n1 + (k1 + P.n1) % P.n1] = in ? cscale(x[idx], dec0[i0] * dec1[i1]) : mk(0, 0);
 }
 
 // crop + deconvolve after the backward FFT (nufft.cpp:339-364)
@@ -60,8 +64,8 @@ __global__ void k_plan_interp(PlanDev P, const int* __restrict__ base, const dou
   const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (m >= P.M) return;
   const int b = blockIdx.y;
-  base += (int64_t)b * P.M * P.dim;
-  wts += (int64_t)b * P.M * P.dim * P.S;
+  base += (int64_t)(b / P.vps) * P.M * P.dim;
+  wts += (int64_t)(b / P.vps) * P.M * P.dim * P.S;
   G += (int64_t)b * P.n0 * P.n1;
   y += (int64_t)b * P.M;
   cplx acc = mk(0, 0);
@@ -69,24 +73,16 @@ __global__ void k_plan_interp(PlanDev P, const int* __restrict__ base, const dou
     const int b0 = base[m];
     const double* w = wts + m * P.S;
     for (int t = 0; t < P.S; ++t) {
-      int j = b0 + t;
-      if (j >= P.n0) j -= P.n0;
-      acc = caxpy(acc, w[t], G[j]);
+      acc = caxpy(acc, w[t], G[(b0 + t) % P.n0]);
     }
   } else {
     const int b0 = base[2 * m], b1 = base[2 * m + 1];
     const double* w0 = wts + (2 * m) * P.S;
     const double* w1 = wts + (2 * m + 1) * P.S;
     for (int t0 = 0; t0 < P.S; ++t0) {
-      int j0 = b0 + t0;
-      if (j0 >= P.n0) j0 -= P.n0;
-      const cplx* row = G + (int64_t)j0 * P.n1;
+      const cplx* row = G + (int64_t)((b0 + t0) % P.n0) * P.n1;
       cplx ra = mk(0, 0);
-      for (int t1 = 0; t1 < P.S; ++t1) {
-        int j1 = b1 + t1;
-        if (j1 >= P.n1) j1 -= P.n1;
-        ra = caxpy(ra, w1[t1], row[j1]);
-      }
+      for (int t1 = 0; t1 < P.S; ++t1) ra = caxpy(ra, w1[t1], row[(b1 + t1) % P.n1]);
       acc = caxpy(acc, w0[t0], ra);
     }
   }
@@ -104,17 +100,15 @@ __global__ void k_plan_spread(PlanDev P, const int* __restrict__ base, const dou
   const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (m >= P.M) return;
   const int b = blockIdx.y;
-  base += (int64_t)b * P.M * P.dim;
-  wts += (int64_t)b * P.M * P.dim * P.S;
+  base += (int64_t)(b / P.vps) * P.M * P.dim;
+  wts += (int64_t)(b / P.vps) * P.M * P.dim * P.S;
   G += (int64_t)b * P.n0 * P.n1;
   const cplx s = v[(int64_t)b * P.M + m];
   if (P.dim == 1) {
     const int b0 = base[m];
     const double* w = wts + m * P.S;
     for (int t = 0; t < P.S; ++t) {
-      int j = b0 + t;
-      if (j >= P.n0) j -= P.n0;
-      atomic_add_c(G + j, cscale(s, w[t]));
+      atomic_add_c(G + (b0 + t) % P.n0, cscale(s, w[t]));
     }
     return;
   }
@@ -122,15 +116,9 @@ __global__ void k_plan_spread(PlanDev P, const int* __restrict__ base, const dou
   const double* w0 = wts + (2 * m) * P.S;
   const double* w1 = wts + (2 * m + 1) * P.S;
   for (int t0 = 0; t0 < P.S; ++t0) {
-    int j0 = b0 + t0;
-    if (j0 >= P.n0) j0 -= P.n0;
     const cplx v0 = cscale(s, w0[t0]);
-    cplx* row = G + (int64_t)j0 * P.n1;
-    for (int t1 = 0; t1 < P.S; ++t1) {
-      int j1 = b1 + t1;
-      if (j1 >= P.n1) j1 -= P.n1;
-      atomic_add_c(row + j1, cscale(v0, w1[t1]));
-    }
+    cplx* row = G + (int64_t)((b0 + t0) % P.n0) * P.n1;
+    for (int t1 = 0; t1 < P.S; ++t1) atomic_add_c(row + (b1 + t1) % P.n1, cscale(v0, w1[t1]));
   }
 }
 

@@ -28,4 +28,10 @@ void ndft_forward_launch(const NdftShape& s, const double* pts, const cplx* x, c
 void ndft_adjoint_launch(const NdftShape& s, const double* pts, const cplx* y, cplx* z, int lo, int hi,
                          const cplx* rec, int p, int edges, DBuf<cplx>& part, cudaStream_t st);
 
+// the 1D operator algebra around any core transform u = F(x~) (freq2wave.cpp:232-236,
+// 318-324): y = D o u + L x[0:p] + R x[n-p:n]; edge columns z_c = L^H y, R^H y
+void op1d_epilogue_launch(int64_t M, int batch, const cplx* u, const cplx* rec, int p, int edges, const cplx* x, int n,
+                          cplx* y, cudaStream_t st);
+void op1d_edges_launch(int64_t M, int batch, const cplx* rec, int p, const cplx* y, int n, cplx* z, cudaStream_t st);
+
 }  // namespace gsb

@@ -44,6 +44,8 @@ class FftG {
 // sharing N, sigma, w.  Points are scaled to [-1/2, 1/2), point-major.
 struct NfftPlanDev {
   int dim = 1, batch = 1;
+  int vps = 1;          // vectors per point set (forward / adjoint take [batch][vps][...])
+  int lo = 0, hi = -1;  // forward embed mask on every axis (operator interiors); -1 = none
   int N[2] = {0, 1};
   int nov[2] = {0, 1};
   int w = 6, S = 13;
@@ -62,8 +64,22 @@ struct NfftPlanDev {
 // d_points: [B][M][dim] device array of scaled points (checked on the host copy h_points)
 void nfft_plan_validate(int dim, const int* N, int64_t M, int batch, const double* h_points, double sigma, int w);
 std::unique_ptr<NfftPlanDev> nfft_plan_build(int dim, const int* N, int64_t M, int batch, const double* h_points,
-                                             double sigma, int w, cudaStream_t st);
+                                             double sigma, int w, cudaStream_t st, int vps = 1);
 void nfft_plan_forward(NfftPlanDev& P, const cplx* x, cplx* y, cudaStream_t st);   // nufft.cpp:244-306
 void nfft_plan_adjoint(NfftPlanDev& P, const cplx* y, cplx* z, cudaStream_t st);   // nufft.cpp:308-365
+
+// The uniform-grid reduction (nufft.cpp:383-459) at any DFT length, batched:
+// forward x [batch][N] (only indices [lo, hi) enter; edge slots of an
+// operator) -> y [batch][M]; adjoint y [batch][M] -> z [batch][N].
+struct UniformDev {
+  int64_t M = 0, N = 0, q = 0, n2 = 0;
+  double eps = 0;
+  int batch = 1;
+  std::unique_ptr<FftG> fft;
+  DBuf<cplx> z;
+};
+std::unique_ptr<UniformDev> uniform_build(int64_t M, double eps, int64_t N, int batch);
+void uniform_forward(UniformDev& U, const cplx* x, int lo, int hi, cplx* y, cudaStream_t st);
+void uniform_adjoint(UniformDev& U, const cplx* y, cplx* z, cudaStream_t st);
 
 }  // namespace gsb
