@@ -128,6 +128,27 @@ int gs_cgls_finish(gs_cgls_session* s, double* x_out, gs_solve_stats* stats, dou
                    void* stream);
 int gs_cgls_destroy(gs_cgls_session* s);
 
+/* Sample-sharded CGLS over several GPUs (the C4 row): each rank
+ * builds an operator from ITS contiguous slice of the samples (rows of T);
+ * coefficient vectors stay replicated; per iteration the library sums
+ * ||q||^2 (B doubles) and the adjoint partials T_g* r_g (B x cols complex)
+ * over the ranks with NCCL on `stream` -- no host round trip.  The
+ * communicator wraps an NCCL communicator (libnccl.so.2, opened on first
+ * use): rank 0 makes a unique id, every rank calls gs_comm_init with it.
+ * gs_cgls_step / active / finish / destroy work on sharded sessions too;
+ * all ranks must call them in the same order (they stay in lockstep). */
+#define GS_COMM_ID_BYTES 128
+typedef struct gs_comm gs_comm;
+int gs_comm_unique_id(unsigned char* id);
+int gs_comm_init(int nranks, int rank, const unsigned char* id, int device, gs_comm** out);
+int gs_comm_destroy(gs_comm* comm);
+int gs_cgls_begin_sharded(gs_op* op, gs_comm* comm, const double* raw_samples, int64_t samples_len,
+                          const double* x0, double tolerance, int history_capacity, void* stream,
+                          gs_cgls_session** out);
+int gs_solve_least_squares_sharded(gs_op* op, gs_comm* comm, const double* raw_samples, int64_t samples_len,
+                                   const double* x0, int max_iterations, double tolerance, double* x_out,
+                                   gs_solve_stats* stats, double* history, void* stream);
+
 /* Host copies of the per-axis factors of problem `b` in the reference layout
  * (Freq2WaveOp::Dx/Dy, Lx/Rx/Ly/Ry col-major M x p, freq2wave.hpp:42-43);
  * axis 0 = x, 1 = y.  L, R may be NULL (haar). */

@@ -3,6 +3,8 @@
 // apply_forward / apply_adjoint, the device-resident CGLS loop and the C-ABI
 // declared in include/gs_b200.h.  No torch types anywhere: plain CUDA runtime.
 #include <cub/cub.cuh>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <atomic>
@@ -1203,9 +1205,68 @@ bool adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
 // ------------------------------------------------------------------ dyadic evaluation
 #include "dyadic_host.cuh"
 
+// ------------------------------------------------------------------ NCCL (sample-sharded CGLS)
+// libnccl.so.2 is opened on first use (the copy torch already loaded when there
+// is one), so the library itself loads on hosts without NCCL.
+struct NcclApi {
+  bool ok = false;
+  std::string err;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*errorString)(ncclResult_t) = nullptr;
+};
+const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      a.err = std::string("libnccl.so.2 not loadable: ") + dlerror();
+      return a;
+    }
+    a.getUniqueId = (decltype(a.getUniqueId))dlsym(h, "ncclGetUniqueId");
+    a.commInitRank = (decltype(a.commInitRank))dlsym(h, "ncclCommInitRank");
+    a.allReduce = (decltype(a.allReduce))dlsym(h, "ncclAllReduce");
+    a.commDestroy = (decltype(a.commDestroy))dlsym(h, "ncclCommDestroy");
+    a.errorString = (decltype(a.errorString))dlsym(h, "ncclGetErrorString");
+    a.ok = a.getUniqueId && a.commInitRank && a.allReduce && a.commDestroy && a.errorString;
+    if (!a.ok) a.err = "libnccl.so.2 lacks the expected symbols";
+    return a;
+  }();
+  if (!api.ok) fail(GS_ERR_CUDA, api.err);
+  return api;
+}
+#define NCK(call)                                                                                        \
+  do {                                                                                                   \
+    ncclResult_t r_ = (call);                                                                            \
+    if (r_ != ncclSuccess) fail(GS_ERR_CUDA, std::string(#call) + ": " + nccl().errorString(r_));        \
+  } while (0)
+
+}  // namespace
+
+struct gs_comm {
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0, device = 0;
+  ~gs_comm() {
+    if (comm) nccl().commDestroy(comm);
+  }
+};
+
+namespace {
+
+// in-place sum over the ranks of a sharded session (doubles; complex = 2 doubles)
+void comm_sum(gs_comm* c, double* v, size_t n, cudaStream_t st) {
+  if (!c || c->nranks == 1) return;  // one rank: the sum is the vector itself
+  NCK(nccl().allReduce(v, v, n, ncclFloat64, ncclSum, c->comm, st));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
 // ------------------------------------------------------------------ CGLS
 struct Session {
   gs_op* op = nullptr;
+  gs_comm* comm = nullptr;  // sample-sharded solve: T* r and ||q||^2 summed over the ranks
   int B = 1;
   int64_t M = 0, Nc = 0;
   double tol = 1e-10;
@@ -1300,8 +1361,9 @@ void session_begin(Session& S, gs_op* op, const cplx* b_raw, bool b_perm, const 
   k_gather_scale<<<nblk(TM, 256), 256, 0, st>>>(b_raw, (sorted && b_perm) ? op->perm.p : nullptr,
                                                 op->weighted ? op->sqrtw.p : nullptr, S.M, S.B, S.b.p);
   CKL();
-  // ref = ||T* b||   (solver.cpp:42)
+  // ref = ||T* b||   (solver.cpp:42); sharded: T* b = sum over ranks of T_g* b_g
   adjoint_dev(op, S.b.p, S.s.p, false, st);
+  comm_sum(S.comm, reinterpret_cast<double*>(S.s.p), 2 * (size_t)TN, st);
   norm2(S, S.s.p, S.Nc, S.chunks_N, st);
   k_cg_ref<<<nblk(S.B, 128), 128, 0, st>>>(S.st.p, S.n2.p, S.B);
   // x = x0 or 0; r = b - T x; s = T* r; gamma; p = s   (solver.cpp:35-68)
@@ -1310,6 +1372,7 @@ void session_begin(Session& S, gs_op* op, const cplx* b_raw, bool b_perm, const 
   forward_dev(op, S.x.p, S.q.p, false, st);
   k_sub<<<nblk(TM, 256), 256, 0, st>>>(S.b.p, S.q.p, TM, S.r.p);
   adjoint_dev(op, S.r.p, S.s.p, false, st);
+  comm_sum(S.comm, reinterpret_cast<double*>(S.s.p), 2 * (size_t)TN, st);
   norm2(S, S.s.p, S.Nc, S.chunks_N, st);
   k_cg_gamma0<<<nblk(S.B, 128), 128, 0, st>>>(S.st.p, S.n2.p, tol, S.hist.p, hist_cap, S.B);
   CK(cudaMemcpyAsync(S.p.p, S.s.p, TN * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
@@ -1328,6 +1391,28 @@ bool cg_fused_enabled() {  // GS_B200_CG_FUSED=0: the generic multi-kernel itera
 void session_iterate_body(Session& S, cudaStream_t st) {
   gs_op* op = S.op;
   const int64_t TM = S.M * S.B, TN = S.Nc * S.B;
+  if (S.comm) {
+    // sample-sharded iteration: rows local, x / p / s replicated;
+    // two exchanges per iteration, both on the device stream (no host sync)
+    forward_dev(op, S.p.p, S.q.p, false, st);                            // q_g = T_g p
+    norm2(S, S.q.p, S.M, S.chunks_M, st);                                // ||q_g||^2
+    comm_sum(S.comm, S.n2.p, (size_t)S.B, st);                           // qq = sum_g ||q_g||^2
+    k_cg_alpha<<<nblk(S.B, 128), 128, 0, st>>>(S.st.p, S.n2.p, S.B);    // alpha (or stop)
+    pmark("k_cg_alpha", st);
+    k_axpy_alpha<<<nblk(TN, 256), 256, 0, st>>>(S.x.p, S.p.p, S.Nc, S.B, S.st.p, 1.0);   // x += alpha p
+    pmark("k_axpy_x", st);
+    k_axpy_alpha<<<nblk(TM, 256), 256, 0, st>>>(S.r.p, S.q.p, S.M, S.B, S.st.p, -1.0);   // r_g -= alpha q_g
+    pmark("k_axpy_r", st);
+    adjoint_dev(op, S.r.p, S.s.p, false, st);                            // T_g* r_g
+    comm_sum(S.comm, reinterpret_cast<double*>(S.s.p), 2 * (size_t)TN, st);  // s = sum_g T_g* r_g
+    norm2(S, S.s.p, S.Nc, S.chunks_N, st);
+    k_cg_beta<<<nblk(S.B, 128), 128, 0, st>>>(S.st.p, S.n2.p, S.tol, S.hist.p, S.hist_cap, S.B);
+    pmark("k_cg_beta", st);
+    k_pupdate<<<nblk(TN, 256), 256, 0, st>>>(S.p.p, S.s.p, S.Nc, S.B, S.st.p);  // p = s + beta p
+    pmark("k_pupdate", st);
+    CKL();
+    return;
+  }
   if (op->route == GS_ROUTE_UNIFORM_1D && !op->general && cg_fused_enabled()) {  // whole iteration in one launch
     const UniP& P = op->up;
     const size_t rs = uni_cg_resident_smem(P, op->Rr);
@@ -1420,7 +1505,7 @@ bool graphs_enabled() {
 void session_iterate(Session& S, cudaStream_t st, int k) {
   if (k <= 0) return;
   S.it += k;
-  if (S.op->route == GS_ROUTE_UNIFORM_1D && !S.op->general && cg_fused_enabled() && !g_prof.on) {
+  if (S.op->route == GS_ROUTE_UNIFORM_1D && !S.op->general && !S.comm && cg_fused_enabled() && !g_prof.on) {
     // all k iterations in one launch (k_uni_cgls_iter loops on the device)
     const UniP& P = S.op->up;
     const size_t rs = uni_cg_resident_smem(P, S.op->Rr);
@@ -1431,7 +1516,7 @@ void session_iterate(Session& S, cudaStream_t st, int k) {
     CKL();
     return;
   }
-  if (!graphs_enabled() || g_prof.on) {
+  if (!graphs_enabled() || g_prof.on || S.comm) {
     for (int i = 0; i < k; ++i) session_iterate_body(S, st);
     return;
   }
@@ -1575,7 +1660,8 @@ namespace {
 // preamble of a solve into a new session, or into `reuse` (a session of this
 // op whose device buffers are recycled; consumed either way)
 int cgls_begin_into(gs_op* op, gs_cgls_session* reuse, const double* raw_samples, int64_t samples_len,
-                    const double* x0, double tolerance, int history_capacity, void* stream, gs_cgls_session** out) {
+                    const double* x0, double tolerance, int history_capacity, void* stream, gs_cgls_session** out,
+                    gs_comm* comm = nullptr) {
   std::unique_ptr<gs_cgls_session> R(reuse);
   return guard_call([&] {
     if (!op || !raw_samples || !out) fail(GS_ERR_USAGE, "null argument");
@@ -1597,6 +1683,8 @@ int cgls_begin_into(gs_op* op, gs_cgls_session* reuse, const double* raw_samples
       op->stage_b.upload((const cplx*)x0, TN, st);
       xx = op->stage_b.p;
     }
+    S->s.comm = comm;
+    if (comm && comm->device != op->device) fail(GS_ERR_USAGE, "communicator and operator are on different devices");
     session_begin(S->s, op, b, true, xx, tolerance, std::max(1, history_capacity), st);
     *out = S.release();
   });
@@ -1694,6 +1782,74 @@ int gs_solve_least_squares(gs_op* op, const double* raw_samples, int64_t samples
     std::swap(op->solve_cache, s);
   }
   gs_cgls_destroy(s);  // another thread's session parked meanwhile, if any
+  return rc;
+}
+
+// ---------------------------------------------------------------- sample-sharded CGLS
+int gs_comm_unique_id(unsigned char* id) {
+  return guard_call([&] {
+    if (!id) fail(GS_ERR_USAGE, "null argument");
+    ncclUniqueId u;
+    NCK(nccl().getUniqueId(&u));
+    static_assert(sizeof(u.internal) == GS_COMM_ID_BYTES, "ncclUniqueId size");
+    std::memcpy(id, u.internal, sizeof(u.internal));
+  });
+}
+
+int gs_comm_init(int nranks, int rank, const unsigned char* id, int device, gs_comm** out) {
+  return guard_call([&] {
+    if (!id || !out) fail(GS_ERR_USAGE, "null argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) fail(GS_ERR_USAGE, "bad rank / size");
+    *out = nullptr;
+    CK(cudaSetDevice(device));
+    std::unique_ptr<gs_comm> c(new gs_comm);
+    c->nranks = nranks;
+    c->rank = rank;
+    c->device = device;
+    ncclUniqueId u;
+    std::memcpy(u.internal, id, sizeof(u.internal));
+    NCK(nccl().commInitRank(&c->comm, nranks, u, rank));
+    *out = c.release();
+  });
+}
+
+int gs_comm_destroy(gs_comm* c) {
+  delete c;
+  return GS_OK;
+}
+
+int gs_cgls_begin_sharded(gs_op* op, gs_comm* comm, const double* raw_samples, int64_t samples_len, const double* x0,
+                          double tolerance, int history_capacity, void* stream, gs_cgls_session** out) {
+  if (!comm) {
+    g_err = "null communicator";
+    return GS_ERR_USAGE;
+  }
+  return cgls_begin_into(op, nullptr, raw_samples, samples_len, x0, tolerance, history_capacity, stream, out, comm);
+}
+
+int gs_solve_least_squares_sharded(gs_op* op, gs_comm* comm, const double* raw_samples, int64_t samples_len,
+                                   const double* x0, int max_iterations, double tolerance, double* x_out,
+                                   gs_solve_stats* stats, double* history, void* stream) {
+  if (!op || !comm) {
+    g_err = "null handle";
+    return GS_ERR_USAGE;
+  }
+  const int max_iter = max_iterations > 0 ? max_iterations : (int)std::min<int64_t>(INT32_MAX / 2, 2 * op->Nc);
+  gs_cgls_session* s = nullptr;
+  int rc = gs_cgls_begin_sharded(op, comm, raw_samples, samples_len, x0, tolerance, max_iter + 1, stream, &s);
+  if (rc) return rc;
+  // every rank holds the same (all-reduced) scalars, so the ranks step in lockstep
+  int done = 0, active = 1, chunk = 4;
+  rc = gs_cgls_active(s, stream, &active);
+  while (rc == 0 && active && done < max_iter) {
+    const int k = std::min(chunk, max_iter - done);
+    rc = gs_cgls_step(s, k, stream);
+    done += k;
+    if (rc == 0) rc = gs_cgls_active(s, stream, &active);
+    chunk = std::min(chunk * 2, 64);
+  }
+  if (rc == 0) rc = gs_cgls_finish(s, x_out, stats, history, stream);
+  gs_cgls_destroy(s);
   return rc;
 }
 

@@ -12,9 +12,16 @@ needs exactly two exchanges:
     gamma', beta, p = s + beta p      local, replicated
 
 Summing coefficient-space adjoint partials equals summing the oversampled
-grids by linearity and is (sigma^dim =) 4x smaller.  The loop is written
-against three callables so the same code drives the GPU operator with NCCL
-and, in the CPU tests, the oracle with gloo.
+grids by linearity and is (sigma^dim =) 4x smaller.
+
+Two implementations of the same iteration:
+  * the product path -- `Communicator` + `ShardedSession` /
+    `solve_least_squares_sharded`: the library runs the loop resident on the
+    GPU and issues both sums as NCCL allreduces on its own stream
+    (gs_cgls_begin_sharded / gs_solve_least_squares_sharded, include/gs_b200.h);
+    no host round trip per iteration;
+  * `cgls_sharded` / `ShardedCGLS`: the loop written against three callables,
+    so the CPU tests drive the oracle with gloo through the same algebra.
 """
 from __future__ import annotations
 
@@ -142,3 +149,132 @@ def torch_collectives(group=None):
             float(torch.sum(v * v).item())
 
     return allreduce_sum, norm2
+
+
+# ------------------------------------------------------------------ library (NCCL) path
+class Communicator:
+    """NCCL communicator owned by libgs_b200.so (gs_comm_init).  Rank 0 makes
+    the unique id; `from_torch` ships it with torch.distributed (any backend)."""
+
+    def __init__(self, nranks, rank, uid: bytes, device=0):
+        import ctypes as C
+
+        from . import _check, load_library
+        L = load_library()
+        L.gs_comm_init.argtypes = [C.c_int, C.c_int, C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]
+        L.gs_comm_destroy.argtypes = [C.c_void_p]
+        h = C.c_void_p()
+        _check(L.gs_comm_init(int(nranks), int(rank), uid, int(device), C.byref(h)))
+        self._h, self.nranks, self.rank, self.device = h, nranks, rank, device
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes as C
+
+        from . import _check, load_library
+        buf = (C.c_ubyte * 128)()
+        _check(load_library().gs_comm_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def from_torch(cls, device=0, group=None):
+        import torch.distributed as dist
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        obj = [cls.unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(world, rank, obj[0], device)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            from . import load_library
+            load_library().gs_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class ShardedSession:
+    """gs_cgls_begin_sharded / step / finish: the resident CGLS loop of
+    solver.cpp:19-91 over this rank's rows, both sums by NCCL on the device."""
+
+    def __init__(self, op, comm: Communicator, samples_local, tolerance=1e-300, history_capacity=2,
+                 initial_guess=None, stream=None):
+        import ctypes as C
+
+        from . import _check, _ptr_len, _stream_ptr, load_library
+        L = load_library()
+        L.gs_cgls_begin_sharded.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_double,
+                                            C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]
+        self.op = op
+        p, n, self._keep = _ptr_len(samples_local)
+        x0p = None
+        if initial_guess is not None:
+            x0p, _, self._keep0 = _ptr_len(initial_guess)
+        self._cap = max(2, history_capacity)
+        h = C.c_void_p()
+        _check(L.gs_cgls_begin_sharded(op.handle, comm.handle, p, n, x0p, float(tolerance), self._cap,
+                                       _stream_ptr(stream), C.byref(h)))
+        self._h = h
+
+    def step(self, iterations, stream=None):
+        from . import _check, _stream_ptr, load_library
+        _check(load_library().gs_cgls_step(self._h, int(iterations), _stream_ptr(stream)))
+
+    def result(self, stream=None):
+        import numpy as np
+
+        from . import CglsSession
+        return CglsSession.result(self, None, stream)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            from . import load_library
+            load_library().gs_cgls_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def solve_least_squares_sharded(op, comm: Communicator, samples_local, max_iterations=0, tolerance=1e-10,
+                                initial_guess=None, stream=None):
+    """gs::solve_least_squares over the rows of all ranks (every rank passes its
+    own operator / raw samples; x and the stats come back replicated)."""
+    import ctypes as C
+
+    import numpy as np
+
+    from . import SolveStats, _check, _ptr_len, _Stats, _stream_ptr, load_library
+    L = load_library()
+    L.gs_solve_least_squares_sharded.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int,
+                                                 C.c_double, C.c_void_p, C.POINTER(_Stats),
+                                                 C.POINTER(C.c_double), C.c_void_p]
+    p, n, keep = _ptr_len(samples_local)
+    x0p = None
+    keep0 = None
+    if initial_guess is not None:
+        x0p, _, keep0 = _ptr_len(initial_guess)
+    B = op.batch
+    mi = max_iterations if max_iterations > 0 else 2 * op.cols()
+    x = np.empty(op.cols() * B, np.complex128)
+    stats = (_Stats * B)()
+    hist = np.zeros(B * (mi + 1), np.float64)
+    _check(L.gs_solve_least_squares_sharded(op.handle, comm.handle, p, n, x0p, int(max_iterations), float(tolerance),
+                                            x.ctypes.data, stats, hist.ctypes.data_as(C.POINTER(C.c_double)),
+                                            _stream_ptr(stream)))
+    out = [SolveStats(s.iterations, s.residual, hist[b * (mi + 1):b * (mi + 1) + s.iterations + 1].tolist(),
+                      bool(s.converged)) for b, s in enumerate(stats)]
+    return (x, out[0]) if B == 1 else (x, out)
