@@ -235,6 +235,11 @@ int gs_gen_grid(int64_t M, double eps, int dim, double* out);
 int gs_gen_jitter(int64_t M, double eps, double eta, uint64_t seed, int dim, double* out);
 int gs_gen_spiral(int turns, double points_per_turn, double K, double* out);
 int gs_voronoi_weights(int dim, int64_t M, const double* coords, double K, double* mu, int nthreads);
+/* voronoi_weights on the GPU: 2D cells one thread each, the
+ * host routine's arithmetic without FMA contraction -> bit-identical mu;
+ * dim 1 falls back to the host.  coords / mu host pointers. */
+int gs_voronoi_weights_gpu(int dim, int64_t M, const double* coords, double K, double* mu, int device,
+                           void* stream);
 /* density(samples, K).delta_raw (weights.cpp:135-176; replaces gs::density) */
 int gs_density(int dim, int64_t M, const double* coords, double K, double* delta_raw, int nthreads);
 /* bench harness right-hand side: n seeded coefficients, interleaved re,im

@@ -22,6 +22,8 @@
 #include <thread>
 #include <vector>
 
+#include "voronoi_common.h"
+
 namespace {
 
 struct P2 {
@@ -119,6 +121,38 @@ int gs_gen_spiral(int turns, double ppt, double K, double* out) {
 // mu[m] = cell measure; rad[m] (optional) = farthest cell vertex from point m,
 // i.e. the largest distance from a vertex of cell m to its nearest sample
 // (weights.cpp:135-171 takes the supremum of these over all cells).
+// bucket grid of the 2D cells (~2 points per bucket) + the reference's input
+// checks (weights.cpp:73-90: range, duplicates); shared with gs_voronoi.cu
+extern "C++" int vor_grid_build(int64_t M, const double* coords, double K, std::vector<int64_t>& start,
+                                std::vector<int64_t>& idx, int& G, double& h) {
+  for (int64_t m = 0; m < M; ++m)
+    if (std::abs(coords[2 * m]) > K || std::abs(coords[2 * m + 1]) > K) {
+      g_in_err = "point outside the bandwidth region";
+      return 5;
+    }
+  // bucket grid, ~2 points per bucket on average
+  G = std::max(1, (int)std::sqrt((double)M / 2.0));
+  h = 2.0 * K / G;
+  auto cell = [&](double v) { return std::min(G - 1, std::max(0, (int)std::floor((v + K) / h))); };
+  start.assign((size_t)G * G + 1, 0);
+  idx.assign(M, 0);
+  for (int64_t m = 0; m < M; ++m) start[(size_t)cell(coords[2 * m + 1]) * G + cell(coords[2 * m]) + 1]++;
+  for (size_t i = 1; i < start.size(); ++i) start[i] += start[i - 1];
+  {
+    std::vector<int64_t> fill(start.begin(), start.end() - 1);
+    for (int64_t m = 0; m < M; ++m) idx[fill[(size_t)cell(coords[2 * m + 1]) * G + cell(coords[2 * m])]++] = m;
+  }
+  // duplicates (same bucket) -> reference DomainError
+  for (size_t b = 0; b + 1 < start.size(); ++b)
+    for (int64_t i = start[b]; i < start[b + 1]; ++i)
+      for (int64_t j = i + 1; j < start[b + 1]; ++j)
+        if (coords[2 * idx[i]] == coords[2 * idx[j]] && coords[2 * idx[i] + 1] == coords[2 * idx[j] + 1]) {
+          g_in_err = "degenerate input: duplicate sample points";
+          return 5;
+        }
+  return 0;
+}
+
 static int voronoi_cells(int dim, int64_t M, const double* coords, double K, double* mu, double* rad, int nthreads) {
   if (!(K > 0)) {
     g_in_err = "K must be positive";
@@ -152,82 +186,41 @@ static int voronoi_cells(int dim, int64_t M, const double* coords, double K, dou
     }
     return 0;
   }
-  for (int64_t m = 0; m < M; ++m)
-    if (std::abs(coords[2 * m]) > K || std::abs(coords[2 * m + 1]) > K) {
-      g_in_err = "point outside the bandwidth region";
-      return 5;
-    }
-  // bucket grid, ~2 points per bucket on average
-  const int G = std::max(1, (int)std::sqrt((double)M / 2.0));
-  const double h = 2.0 * K / G;
-  auto cell = [&](double v) { return std::min(G - 1, std::max(0, (int)std::floor((v + K) / h))); };
-  std::vector<int64_t> start((size_t)G * G + 1, 0), idx(M);
-  for (int64_t m = 0; m < M; ++m) start[(size_t)cell(coords[2 * m + 1]) * G + cell(coords[2 * m]) + 1]++;
-  for (size_t i = 1; i < start.size(); ++i) start[i] += start[i - 1];
+  std::vector<int64_t> start, idx;
+  int G = 1;
+  double h = 0.0;
   {
-    std::vector<int64_t> fill(start.begin(), start.end() - 1);
-    for (int64_t m = 0; m < M; ++m) idx[fill[(size_t)cell(coords[2 * m + 1]) * G + cell(coords[2 * m])]++] = m;
+    const int rc = vor_grid_build(M, coords, K, start, idx, G, h);
+    if (rc) return rc;
   }
-  // duplicates (same bucket) -> reference DomainError
-  for (size_t b = 0; b + 1 < start.size(); ++b)
-    for (int64_t i = start[b]; i < start[b + 1]; ++i)
-      for (int64_t j = i + 1; j < start[b + 1]; ++j)
-        if (coords[2 * idx[i]] == coords[2 * idx[j]] && coords[2 * idx[i] + 1] == coords[2 * idx[j] + 1]) {
-          g_in_err = "degenerate input: duplicate sample points";
-          return 5;
-        }
   if (nthreads <= 0) nthreads = (int)std::max(1u, std::thread::hardware_concurrency());
   std::atomic<int64_t> next(0);
+  const VorGrid grid{coords, start.data(), idx.data(), M, G, K, h};
   auto worker = [&]() {
-    std::vector<P2> poly, tmp;
-    std::vector<std::pair<double, int64_t>> cand;
+    // per-cell routine shared with the GPU kernel (voronoi_common.h); buffers grow on overflow
+    int capv = 256, capc = 1024;
+    std::vector<double> px(capv), py(capv), qx(capv), qy(capv), cd(capc);
+    std::vector<int64_t> cj(capc);
     const int64_t chunk = 256;
     for (;;) {
       int64_t lo = next.fetch_add(chunk);
       if (lo >= M) break;
       int64_t hi = std::min(M, lo + chunk);
       for (int64_t m = lo; m < hi; ++m) {
-        const P2 own{coords[2 * m], coords[2 * m + 1]};
-        const int cx = cell(own.x), cy = cell(own.y);
-        poly = {{-K, -K}, {K, -K}, {K, K}, {-K, K}};
-        for (int ring = 0;; ++ring) {
-          cand.clear();
-          for (int gy = cy - ring; gy <= cy + ring; ++gy) {
-            if (gy < 0 || gy >= G) continue;
-            for (int gx = cx - ring; gx <= cx + ring; ++gx) {
-              if (gx < 0 || gx >= G) continue;
-              if (std::max(std::abs(gx - cx), std::abs(gy - cy)) != ring) continue;
-              const size_t b = (size_t)gy * G + gx;
-              for (int64_t i = start[b]; i < start[b + 1]; ++i) {
-                int64_t j = idx[i];
-                if (j == m) continue;
-                double dx = coords[2 * j] - own.x, dy = coords[2 * j + 1] - own.y;
-                cand.push_back({dx * dx + dy * dy, j});
-              }
-            }
-          }
-          std::sort(cand.begin(), cand.end());
-          for (auto& c : cand) {
-            const P2 q{coords[2 * c.second], coords[2 * c.second + 1]};
-            clip(poly, tmp, P2{(own.x + q.x) / 2, (own.y + q.y) / 2}, P2{q.x - own.x, q.y - own.y});
-            if (poly.empty()) break;
-          }
-          if (poly.empty()) break;
-          // every point outside rings <= ring is at least this far from own
-          double dxm = std::min(own.x - (-K + (cx - ring) * h), (-K + (cx + ring + 1) * h) - own.x);
-          double dym = std::min(own.y - (-K + (cy - ring) * h), (-K + (cy + ring + 1) * h) - own.y);
-          double reach = std::min(dxm, dym);
-          bool covers_all = cx - ring <= 0 && cy - ring <= 0 && cx + ring >= G - 1 && cy + ring >= G - 1;
-          double rmax2 = 0.0;
-          for (const P2& v : poly) rmax2 = std::max(rmax2, (v.x - own.x) * (v.x - own.x) + (v.y - own.y) * (v.y - own.y));
-          if (covers_all || 4.0 * rmax2 <= reach * reach) break;
+        double mu_m = 0.0, rad_m = 0.0;
+        while (vor_cell(grid, m, px.data(), py.data(), qx.data(), qy.data(), capv, cd.data(), cj.data(), capc,
+                        &mu_m, &rad_m) != VOR_OK) {
+          capv *= 2;
+          capc *= 2;
+          px.resize(capv);
+          py.resize(capv);
+          qx.resize(capv);
+          qy.resize(capv);
+          cd.resize(capc);
+          cj.resize(capc);
         }
-        if (mu) mu[m] = area(poly);
-        if (rad) {
-          double r = 0.0;
-          for (const P2& v : poly) r = std::max(r, std::hypot(v.x - own.x, v.y - own.y));
-          rad[m] = r;
-        }
+        if (mu) mu[m] = mu_m;
+        if (rad) rad[m] = rad_m;
       }
     }
   };

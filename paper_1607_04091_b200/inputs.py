@@ -45,10 +45,20 @@ def gen_spiral(turns, points_per_turn, K):
     return out
 
 
-def voronoi_weights(dim, coords, K, threads=0):
+def voronoi_weights(dim, coords, K, threads=0, device=None):
+    """voronoi_weights (weights.cpp:94-133): host (multi-threaded) by default;
+    device=<ordinal> runs the 2D cells on that GPU (gs_voronoi_weights_gpu,
+    bit-identical to the host's)."""
     coords = np.ascontiguousarray(coords, dtype=np.float64).ravel()
     M = coords.size // dim
     mu = np.empty(M)
+    if device is not None:
+        from . import _check
+        L = _lib()
+        L.gs_voronoi_weights_gpu.argtypes = [C.c_int, C.c_int64, _dp, C.c_double, _dp, C.c_int, C.c_void_p]
+        _check(L.gs_voronoi_weights_gpu(dim, M, coords.ctypes.data_as(_dp), float(K), mu.ctypes.data_as(_dp),
+                                        int(device), None))
+        return mu
     _check_inputs(_lib().gs_voronoi_weights(dim, M, coords.ctypes.data_as(_dp), float(K), mu.ctypes.data_as(_dp),
                                             int(threads)))
     return mu

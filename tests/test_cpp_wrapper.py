@@ -13,8 +13,10 @@ LIBDIR = os.path.join(ROOT, "paper_1607_04091_b200")
 
 def build(tmp_path):
     exe = os.path.join(str(tmp_path), "wrapper_demo")
-    subprocess.check_call(["g++", "-std=c++20", "-O2", "-o", exe, SRC, f"-L{LIBDIR}", "-lgs_b200",
-                           f"-Wl,-rpath,{LIBDIR}"])
+    subprocess.check_call(["g++", "-std=c++20", "-O2", "-o", exe, SRC,
+                           f"-I{os.path.join(ROOT, 'tests', 'cpp', 'shim')}", f"-I{os.path.join(LIBDIR, 'cpp')}",
+                           f"-I{os.path.join(LIBDIR, 'cpp', 'include')}", f"-I{os.path.join(ROOT, 'include')}",
+                           f"-L{LIBDIR}", "-lgs_b200", f"-Wl,-rpath,{LIBDIR}"])
     return exe
 
 
