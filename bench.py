@@ -136,7 +136,13 @@ class ProductGen:
         return self.i.gen_spiral(t, ppt, K)
 
     def voronoi(self, dim, c, K):
-        return self.i.voronoi_weights(dim, c, K)
+        # GPU cells when a device is present (bit-identical to the host routine)
+        try:
+            import torch
+            dev = torch.cuda.current_device() if torch.cuda.is_available() else None
+        except Exception:  # noqa: BLE001
+            dev = None
+        return self.i.voronoi_weights(dim, c, K, device=dev if dim == 2 else None)
 
 
 # ------------------------------------------------------------------ roofline bookkeeping

@@ -143,3 +143,83 @@ GS_HD inline int vor_cell(const VorGrid& g, int64_t m, double* px, double* py, d
   }
   return VOR_OK;
 }
+
+// The same cell, for the GPU thread with no candidate buffer: within a ring
+// the candidates are visited in the host's (d2, j) order by repeated min-scans
+// of the ring's buckets, and the scan stops at the first candidate with
+// d2 > 4.5 rmax^2 of the current polygon.  Such a candidate's bisector clears
+// every vertex by >= 0.06 d rmax (|v - own| <= rmax < d / 2.12), so its clip
+// -- and every later one in the ring, rmax only shrinks -- leaves the polygon
+// unchanged exactly: the host's clip sequence minus its no-ops, hence the
+// same doubles.  Dense buckets (the spiral's arms) cost scans, not memory.
+GS_HD inline int vor_cell_stream(const VorGrid& g, int64_t m, double* px, double* py, double* qx, double* qy, int capv,
+                                 double* mu) {
+  const double ownx = g.c[2 * m], owny = g.c[2 * m + 1], K = g.K;
+  const int cx = vor_bucket(g, ownx), cy = vor_bucket(g, owny);
+  int n = 4;
+  px[0] = -K; py[0] = -K;
+  px[1] = K;  py[1] = -K;
+  px[2] = K;  py[2] = K;
+  px[3] = -K; py[3] = K;
+  double rmax2 = 2.0 * K * K * 4.0;  // box diagonal bound: nothing pruned before the first clip
+  for (int ring = 0;; ++ring) {
+    double last_d2 = -1.0;
+    int64_t last_j = -1;
+    while (n > 0) {
+      double best_d2 = 0.0;
+      int64_t best_j = -1;
+      for (int gy = cy - ring; gy <= cy + ring; ++gy) {
+        if (gy < 0 || gy >= g.G) continue;
+        for (int gx = cx - ring; gx <= cx + ring; ++gx) {
+          if (gx < 0 || gx >= g.G) continue;
+          const int dxr = gx - cx < 0 ? cx - gx : gx - cx, dyr = gy - cy < 0 ? cy - gy : gy - cy;
+          if ((dxr > dyr ? dxr : dyr) != ring) continue;
+          const int64_t b = (int64_t)gy * g.G + gx;
+          for (int64_t i = g.start[b]; i < g.start[b + 1]; ++i) {
+            const int64_t j = g.idx[i];
+            if (j == m) continue;
+            const double dx = g.c[2 * j] - ownx, dy = g.c[2 * j + 1] - owny;
+            const double d2 = dx * dx + dy * dy;
+            const bool after = d2 > last_d2 || (d2 == last_d2 && j > last_j);
+            const bool before = best_j < 0 || d2 < best_d2 || (d2 == best_d2 && j < best_j);
+            if (after && before) {
+              best_d2 = d2;
+              best_j = j;
+            }
+          }
+        }
+      }
+      if (best_j < 0 || best_d2 > 4.5 * rmax2) break;  // ring exhausted, or every remaining clip is a no-op
+      last_d2 = best_d2;
+      last_j = best_j;
+      const double qxj = g.c[2 * best_j], qyj = g.c[2 * best_j + 1];
+      const int nn = vor_clip(px, py, n, (ownx + qxj) / 2, (owny + qyj) / 2, qxj - ownx, qyj - owny, qx, qy, capv);
+      if (nn < 0) return VOR_OVERFLOW;
+      for (int i = 0; i < nn; ++i) {
+        px[i] = qx[i];
+        py[i] = qy[i];
+      }
+      n = nn;
+      rmax2 = 0.0;
+      for (int i = 0; i < n; ++i) {
+        const double r2 = (px[i] - ownx) * (px[i] - ownx) + (py[i] - owny) * (py[i] - owny);
+        rmax2 = r2 > rmax2 ? r2 : rmax2;
+      }
+    }
+    if (n == 0) break;
+    const double h = g.h;
+    const double ax0 = ownx - (-K + (cx - ring) * h), ax1 = (-K + (cx + ring + 1) * h) - ownx;
+    const double ay0 = owny - (-K + (cy - ring) * h), ay1 = (-K + (cy + ring + 1) * h) - owny;
+    const double dxm = ax0 < ax1 ? ax0 : ax1, dym = ay0 < ay1 ? ay0 : ay1;
+    const double reach = dxm < dym ? dxm : dym;
+    const bool covers_all = cx - ring <= 0 && cy - ring <= 0 && cx + ring >= g.G - 1 && cy + ring >= g.G - 1;
+    if (covers_all || 4.0 * rmax2 <= reach * reach) break;
+  }
+  double acc = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const int j = (i + 1) % n;
+    acc += px[i] * py[j] - px[j] * py[i];
+  }
+  *mu = 0.5 * fabs(acc);
+  return VOR_OK;
+}
