@@ -136,13 +136,7 @@ class ProductGen:
         return self.i.gen_spiral(t, ppt, K)
 
     def voronoi(self, dim, c, K):
-        # GPU cells when a device is present (bit-identical to the host routine)
-        try:
-            import torch
-            dev = torch.cuda.current_device() if torch.cuda.is_available() else None
-        except Exception:  # noqa: BLE001
-            dev = None
-        return self.i.voronoi_weights(dim, c, K, device=dev if dim == 2 else None)
+        return self.i.voronoi_weights(dim, c, K)  # host threads (GPU cells are bit-identical: test_gpu_voronoi)
 
 
 # ------------------------------------------------------------------ roofline bookkeeping

@@ -18,6 +18,9 @@
 
 #define VOR_OK 0
 #define VOR_OVERFLOW 1
+#ifndef VOR_STREAM_MAXPOP
+#define VOR_STREAM_MAXPOP 160  // ring population beyond which vor_cell_stream hands the cell back
+#endif
 
 #include <vector>
 // host_inputs.cpp: bucket grid + range / duplicate checks; 0 or an error code (message: gs_inputs_last_error)
@@ -165,6 +168,20 @@ GS_HD inline int vor_cell_stream(const VorGrid& g, int64_t m, double* px, double
   for (int ring = 0;; ++ring) {
     double last_d2 = -1.0;
     int64_t last_j = -1;
+    {  // the min-scans are quadratic in the ring's population: dense rings go to the host
+      int64_t pop = 0;
+      for (int gy = cy - ring; gy <= cy + ring; ++gy) {
+        if (gy < 0 || gy >= g.G) continue;
+        for (int gx = cx - ring; gx <= cx + ring; ++gx) {
+          if (gx < 0 || gx >= g.G) continue;
+          const int dxr = gx - cx < 0 ? cx - gx : gx - cx, dyr = gy - cy < 0 ? cy - gy : gy - cy;
+          if ((dxr > dyr ? dxr : dyr) != ring) continue;
+          const int64_t b = (int64_t)gy * g.G + gx;
+          pop += g.start[b + 1] - g.start[b];
+        }
+      }
+      if (pop > VOR_STREAM_MAXPOP) return VOR_OVERFLOW;
+    }
     while (n > 0) {
       double best_d2 = 0.0;
       int64_t best_j = -1;
