@@ -577,12 +577,28 @@ def gs_solve_host(op, b_host, x_host, iters):
     return x_host, stats
 
 
-# ------------------------------------------------------------------ CPU legs (oracle = test infrastructure)
-def _cpu_problem(workload, b):
-    """The workload's problem b on the oracle alone (test infrastructure; the
-    product library is never loaded by the CPU legs).  2D Voronoi weights of
-    the large configs come from the oracle's bucketed exact clipping (the
-    reference's O(M^2) loop is infeasible at 2^18-2^20 points)."""
+# ------------------------------------------------------------------ CPU legs (oracle/ = test infrastructure)
+def _cpu_backend():
+    """(module, kind, description): the reference ITSELF when oracle/_ref/libgs_ref.so
+    is present (its unmodified sources compiled with Eigen / FFTW stand-ins,
+    oracle/Makefile), else the restated port (oracle/gs_oracle.cpp)."""
+    import oracle
+    from oracle import ref
+    if os.environ.get("GS_BENCH_CPU", "") != "port" and ref.available():
+        ref.lib()
+        return ref, "reference", ("oracle/_ref/libgs_ref.so: the reference's own sources (proj/src/*.cpp, unmodified) "
+                                  "built -O3 with an Eigen subset and a radix-2 / mixed-radix FFTW stand-in")
+    oracle.lib()
+    return oracle, "port", "oracle/gs_oracle.cpp, the reference algorithm restated"
+
+
+def _cpu_problem(workload, b, impl):
+    """The workload's problem b on the CPU implementation `impl` alone (the
+    product library is never loaded by the CPU legs).  Inputs come from the
+    oracle's generators (bit-identical to the reference's, tests/
+    test_reference_itself.py); 2D Voronoi weights of the large configs from the
+    oracle's bucketed exact clipping (the reference's O(M^2) loop is infeasible
+    at 2^18-2^20 points).  Input generation is outside every timed region."""
     import oracle
 
     class OracleGen:
@@ -597,11 +613,11 @@ def _cpu_problem(workload, b):
             return oracle.voronoi(dim, c, K)
 
     dim, p, J, c, mu, bw, sig = problem_inputs(workload, b, OracleGen)
-    op_u = oracle.Op(dim, p, J, c, bandwidth=bw)
+    op_u = impl.Op(dim, p, J, c, bandwidth=bw)
     x, nz = coeffs_and_noise(b, op_u.cols, op_u.rows, sig)
     data = op_u.forward(x) + nz
     del op_u
-    op = oracle.Op(dim, p, J, c, weights=mu, bandwidth=bw)
+    op = impl.Op(dim, p, J, c, weights=mu, bandwidth=bw)
     return op, data
 
 
@@ -617,32 +633,36 @@ def _cpu_iter_seconds(op, data, k):
 
 
 def cpu_baseline(workload):
-    """Rank 0, N=1: the oracle (restated reference, single thread like the
-    reference itself) on one problem of the workload."""
+    """Rank 0, N=1: the reference (single-threaded, as it is) on one problem of
+    the workload -- the reference itself when its library is here, else the port."""
     cpu = host_cpu()
+    kind = "port"
     try:
+        impl, kind, what = _cpu_backend()
         t = time.perf_counter()
-        op, data = _cpu_problem(workload, 0)
+        op, data = _cpu_problem(workload, 0, impl)
         build = time.perf_counter() - t
         k = 2 if workload in ("c4", "c5", "c3") else 20
         per_it, _, _ = _cpu_iter_seconds(op, data, k)
-        return {"value": round(1.0 / per_it, 4), "unit": "problem-iterations/s", "cores": 1, "kind": "port",
+        return {"value": round(1.0 / per_it, 4), "unit": "problem-iterations/s", "cores": 1, "kind": kind,
                 "cpu_model": cpu["model"], "physical_cores": cpu["physical_cores"],
                 "sample": f"{workload.upper()} problem 0, {k} CGLS iterations (difference of solves of 1 and "
-                          f"{1 + k} iterations), 1 thread, construction ({build:.1f} s) excluded"}
+                          f"{1 + k} iterations), 1 thread, construction ({build:.1f} s) excluded; {what}"}
     except Exception as e:  # noqa: BLE001
-        return {"value": None, "unit": "problem-iterations/s", "cores": 1, "kind": "port", "sample": f"failed: {e}"}
+        return {"value": None, "unit": "problem-iterations/s", "cores": 1, "kind": kind, "sample": f"failed: {e}"}
 
 
 def run_reference(args):
-    """--impl reference: the CPU restatement of the reference path (oracle/) on
-    the host cores, all threads, same workload / metric; rank 0 only."""
+    """--impl reference: the reference's CPU implementation of the path on the
+    host cores (oracle/_ref, the reference itself, when present; else the
+    restated port), all threads it can use -- the reference is single-threaded,
+    so one problem per thread on the batched config -- same workload / metric;
+    rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return None
-    import oracle
-    oracle.lib()
+    impl, kind, what = _cpu_backend()
     cpu = host_cpu()
     ncpu = cpu["logical_cpus_available"]
     P = args.problems or problem_count(args.workload)
@@ -653,7 +673,7 @@ def run_reference(args):
 
     def work(i):
         try:
-            op, data = _cpu_problem(args.workload, i)
+            op, data = _cpu_problem(args.workload, i, impl)
             per_it, _, _ = _cpu_iter_seconds(op, data, k)
             rates[i] = 1.0 / per_it
         except Exception as e:  # noqa: BLE001
@@ -673,9 +693,9 @@ def run_reference(args):
            "dtype": "c128 (f64)", "data": "synthetic (same generators and seeds as the GPU arm)",
            "config": config_for(args.workload, P, world),
            "cpu_baseline": {"value": round(value, 4), "unit": "problem-iterations/s", "cores": threads,
-                            "kind": "port", "cpu_model": cpu["model"], "physical_cores": cpu["physical_cores"],
-                            "sample": f"{threads} concurrent problems x {k} CGLS iterations each (oracle/gs_oracle.cpp,"
-                                      f" the reference algorithm restated; construction excluded); wall {wall:.0f} s"},
+                            "kind": kind, "cpu_model": cpu["model"], "physical_cores": cpu["physical_cores"],
+                            "sample": f"{threads} concurrent problems x {k} CGLS iterations each ({what}; "
+                                      f"construction excluded); wall {wall:.0f} s"},
            "e2e": {"value": round(value, 4), "unit": "problem-iterations/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     if errs:

@@ -1,6 +1,7 @@
-"""bench.py's reference arm (--impl reference) on CPU: it times the oracle
-(restated reference) with the GPU arm's config dict, reports the host CPU
-model / physical core count, and never maps the product library."""
+"""bench.py's reference arm (--impl reference) on CPU: it times the reference
+itself (oracle/_ref/libgs_ref.so) when that library is present, else the
+restated port, with the GPU arm's config dict, reports the host CPU model /
+physical core count, and never maps the product library."""
 import json
 import os
 import subprocess
@@ -31,5 +32,7 @@ def test_reference_arm_is_product_free_and_shares_config():
     line, mapped = run("c1")
     assert mapped == 0
     assert line["impl"] == "reference" and line["config"] == bench.config_for("c1", 1, 1)
-    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cpu_model"]
+    from oracle import ref
+    assert line["cpu_baseline"]["kind"] == ("reference" if ref.available() else "port")
+    assert line["cpu_baseline"]["cpu_model"]
     assert line["value"] > 0 and line["e2e"]["value"] == line["value"]
