@@ -124,7 +124,8 @@ struct gs_op {
   bool fast2d = false;  // kernels_nfft2d_fast.cuh path (w = 6, p <= 4)
   int cap = 1;          // chunk capacity per problem (2D work list)
   DBuf<int> ch_tile, ch_s0, ch_s1, ch_count, tcs;
-  DBuf<uint4> ch_rows;  // per chunk: row starts (k2f_chunk_rows)
+  DBuf<uint4> ch_rows;  // per chunk: row starts + warps per band (k2f_chunk_rows)
+  bool balanced = false;  // uneven static bands: the DMMA kernels run the balanced band schedule
   DBuf<int> fs_start;  // per (problem, tile): range of fold sources (k2_fold_src)
   DBuf<int4> fsrc;
   DBuf<int2> cov;        // per grid coordinate: (tile, offset) of the regions covering it
@@ -197,14 +198,22 @@ void set_smem_attrs() {
   allow_big_smem(k2f_spread<2>);
   allow_big_smem(k2f_spread<3>);
   allow_big_smem(k2f_spread<4>);
-  allow_big_smem(k2f_interp_mma<1>);
-  allow_big_smem(k2f_interp_mma<2>);
-  allow_big_smem(k2f_interp_mma<3>);
-  allow_big_smem(k2f_interp_mma<4>);
-  allow_big_smem(k2f_spread_mma<1>);
-  allow_big_smem(k2f_spread_mma<2>);
-  allow_big_smem(k2f_spread_mma<3>);
-  allow_big_smem(k2f_spread_mma<4>);
+  allow_big_smem(k2f_interp_mma<1, false>);
+  allow_big_smem(k2f_interp_mma<1, true>);
+  allow_big_smem(k2f_interp_mma<2, false>);
+  allow_big_smem(k2f_interp_mma<2, true>);
+  allow_big_smem(k2f_interp_mma<3, false>);
+  allow_big_smem(k2f_interp_mma<3, true>);
+  allow_big_smem(k2f_interp_mma<4, false>);
+  allow_big_smem(k2f_interp_mma<4, true>);
+  allow_big_smem(k2f_spread_mma<1, false>);
+  allow_big_smem(k2f_spread_mma<1, true>);
+  allow_big_smem(k2f_spread_mma<2, false>);
+  allow_big_smem(k2f_spread_mma<2, true>);
+  allow_big_smem(k2f_spread_mma<3, false>);
+  allow_big_smem(k2f_spread_mma<3, true>);
+  allow_big_smem(k2f_spread_mma<4, false>);
+  allow_big_smem(k2f_spread_mma<4, true>);
   if ((int)done_dev.size() <= dev) done_dev.resize(dev + 1, 0);
   done_dev[dev] = 1;
 }
@@ -754,10 +763,20 @@ gs_op* create(const gs_op_desc* dsc) {
       op->tcs.upload(tcs.data(), tcs.size(), st);
       if (op->fast2d) {
         op->ch_rows.alloc((size_t)B * cap);
+        // row starts + the balanced schedule's warps per band; the balanced DMMA kernels are used
+        // when the longest static band of a chunk exceeds the balanced run by > 5 % over the operator
+        DBuf<unsigned long long> bal;
+        bal.alloc(2);
+        CK(cudaMemsetAsync(bal.p, 0, 2 * sizeof(unsigned long long), st));
         k2f_chunk_rows<<<nblk((int64_t)B * cap, 128), 128, 0, st>>>(op->ch_tile.p, op->ch_s0.p, op->ch_s1.p,
-                                                                   (int64_t)B * cap, cap, M, P.nt, op->base_y.p,
-                                                                   op->ch_rows.p);
+                                                                   op->ch_count.p, (int64_t)B * cap, cap, M, P.nt,
+                                                                   op->base_y.p, op->ch_rows.p, bal.p);
         CKL();
+        unsigned long long hb[2] = {0, 0};
+        CK(cudaMemcpyAsync(hb, bal.p, sizeof(hb), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        static const char* benv = getenv("GS_B200_BALANCE");  // 0 / 1 force the static / balanced kernels (A/B)
+        op->balanced = benv ? atoi(benv) != 0 : (double)hb[0] > 1.05 * (double)hb[1];
       }
       if (op->fast2d) {  // fold sources per tile (k2_fold_src): same order as k2_fold_tiles' coverage loops
         std::vector<int> fst((size_t)B * (ntiles + 1));
@@ -1036,8 +1055,12 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
         const dim3 grid(op->cap, B);
         const int* pp = perm_io ? op->perm.p : nullptr;
 #define GS_F_INTERP(PP)                                                                                            \
-  if (interp_mma())                                                                                                \
-    k2f_interp_mma<PP><<<grid, 32 * F_IWARPS * F_IMSPLIT, FInterpM<PP>::bytes(), st>>>(                                       \
+  if (interp_mma() && op->balanced)                                                                                \
+    k2f_interp_mma<PP, true><<<grid, 32 * F_IWARPS * F_IMSPLIT, FInterpM<PP>::bytes(), st>>>(                      \
+        P, op->ch_tile.p, op->ch_s0.p, op->ch_s1.p, op->ch_count.p, op->ch_rows.p, op->cap, op->base_x.p, op->base_y.p,            \
+        op->wts_x.p, op->wts_y.p, op->rec_x.p, op->rec_y.p, op->G.p, op->lines.p, x, pp, y);                        \
+  else if (interp_mma())                                                                                           \
+    k2f_interp_mma<PP, false><<<grid, 32 * F_IWARPS * F_IMSPLIT, FInterpM<PP>::bytes(), st>>>(                     \
         P, op->ch_tile.p, op->ch_s0.p, op->ch_s1.p, op->ch_count.p, op->ch_rows.p, op->cap, op->base_x.p, op->base_y.p,            \
         op->wts_x.p, op->wts_y.p, op->rec_x.p, op->rec_y.p, op->G.p, op->lines.p, x, pp, y);                        \
   else                                                                                                             \
@@ -1137,8 +1160,12 @@ bool adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
         const dim3 grid(op->cap, B);
         const int* pp = perm_io ? op->perm.p : nullptr;
 #define GS_F_SPREAD(PP)                                                                                          \
-  if (spread_mma())                                                                                              \
-    k2f_spread_mma<PP><<<grid, 32 * F_MWARPS, FSpreadM<PP>::bytes(), st>>>(                                     \
+  if (spread_mma() && op->balanced)                                                                              \
+    k2f_spread_mma<PP, true><<<grid, 32 * F_MWARPS, FSpreadM<PP>::bytes(), st>>>(                               \
+        P, op->ch_tile.p, op->ch_s0.p, op->ch_s1.p, op->ch_count.p, op->ch_rows.p, op->cap, op->base_x.p, op->base_y.p,          \
+        op->wts_x.p, op->wts_y.p, op->rec_x.p, op->rec_y.p, y, pp, op->TB.p, op->TL.p, op->TC.p);                 \
+  else if (spread_mma())                                                                                         \
+    k2f_spread_mma<PP, false><<<grid, 32 * F_MWARPS, FSpreadM<PP>::bytes(), st>>>(                              \
         P, op->ch_tile.p, op->ch_s0.p, op->ch_s1.p, op->ch_count.p, op->ch_rows.p, op->cap, op->base_x.p, op->base_y.p,          \
         op->wts_x.p, op->wts_y.p, op->rec_x.p, op->rec_y.p, y, pp, op->TB.p, op->TL.p, op->TC.p);                 \
   else                                                                                                           \

@@ -137,12 +137,18 @@ __device__ __forceinline__ unsigned char* bulk_stage(unsigned char* dst, const v
 // Row starts of every chunk (built once per operator): byte r of ch_rows[chunk]
 // = first sample (relative to the chunk start) whose window row is >= tile
 // row r, r = 0..F_T (samples are sorted by cell, row-major, inside a tile).
+// Bytes 13-14: the balanced schedule's warps per band (3 bits each, see
+// f_band_schedule); bal[0] / bal[1] accumulate the chunks' longest static band
+// and longest balanced warp run (in K steps of 4 samples) -- the operator uses
+// the balanced kernels when the static bands are measurably uneven.
 __global__ void k2f_chunk_rows(const int* __restrict__ ch_tile, const int* __restrict__ ch_s0,
-                               const int* __restrict__ ch_s1, int64_t nchunks, int cap, int64_t M, int nt,
-                               const int* __restrict__ base_y, uint4* __restrict__ ch_rows) {
+                               const int* __restrict__ ch_s1, const int* __restrict__ ch_count, int64_t nchunks,
+                               int cap, int64_t M, int nt, const int* __restrict__ base_y, uint4* __restrict__ ch_rows,
+                               unsigned long long* __restrict__ bal) {
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= nchunks) return;
   const int prob = (int)(q / cap), a = ch_s0[q], n = ch_s1[q] - a;
+  const bool live = (int)(q - (int64_t)prob * cap) < ch_count[prob];
   const int ty0 = (ch_tile[q] / nt) * F_T;
   const int* by = base_y + (int64_t)prob * M + a;
   unsigned char r8[16] = {0};
@@ -155,11 +161,87 @@ __global__ void k2f_chunk_rows(const int* __restrict__ ch_tile, const int* __res
     }
     r8[r] = (unsigned char)lo;
   }
+  // warps per band: one per non-empty band, the spare ones to the band with the most steps per warp
+  constexpr int NW = 4, BAND = F_T / NW;
+  int steps[NW], nw[NW], used = 0, smax = 0;
+  for (int b = 0; b < NW; ++b) {
+    steps[b] = (r8[(b + 1) * BAND] - r8[b * BAND] + 3) / 4;
+    nw[b] = steps[b] > 0 ? 1 : 0;
+    used += nw[b];
+    smax = steps[b] > smax ? steps[b] : smax;
+  }
+  for (int k = used; k < NW && used > 0; ++k) {
+    int best = 0, load = -1;
+    for (int b = 0; b < NW; ++b) {
+      const int l = nw[b] > 0 ? (steps[b] + nw[b] - 1) / nw[b] : -1;
+      if (l > load) load = l, best = b;
+    }
+    ++nw[best];
+  }
+  if (used == 0)
+    for (int b = 0; b < NW; ++b) nw[b] = 1;
+  int bmax = 0;
+  for (int b = 0; b < NW; ++b) {
+    const int l = nw[b] > 0 ? (steps[b] + nw[b] - 1) / nw[b] : 0;
+    bmax = l > bmax ? l : bmax;
+  }
+  const unsigned code = (unsigned)nw[0] | ((unsigned)nw[1] << 3) | ((unsigned)nw[2] << 6) | ((unsigned)nw[3] << 9);
+  r8[13] = (unsigned char)(code & 0xffu);
+  r8[14] = (unsigned char)(code >> 8);
   ch_rows[q] = *reinterpret_cast<const uint4*>(r8);
+  if (live && bal) {
+    atomicAdd(bal, (unsigned long long)smax);
+    atomicAdd(bal + 1, (unsigned long long)bmax);
+  }
 }
 __device__ __forceinline__ int row_start(const uint4& rw, int r) {
   const unsigned w = r < 4 ? rw.x : (r < 8 ? rw.y : (r < 12 ? rw.z : rw.w));
   return (int)((w >> (8 * (r & 3))) & 0xffu);
+}
+
+// Balanced band schedule of the DMMA kernels (template flag BAL).  A tile's
+// samples are sorted band-major (NW bands of BAND cell rows); statically warp w
+// takes band w, which idles warps whenever a sampling pattern loads the bands
+// unevenly (a spiral arm crossing a tile sits in one or two bands: C4's longest
+// band holds 1.55x the mean).  In the balanced schedule every non-empty band
+// gets one warp and the spare warps go, one at a time, to the band with the
+// most K steps per warp (decided once per chunk by k2f_chunk_rows, bytes 13-14
+// of ch_rows); a band's warps take equal contiguous runs of its steps (STEP
+// samples each).  Any warp's samples still lie in ONE band, so its accumulator
+// window (band rows + 12) is unchanged; the chunk fold sums the warp records by
+// band.  The operator picks the balanced kernels only when its static bands
+// are uneven (gs_capi.cu), so evenly loaded patterns (C5's jittered grid) keep
+// the static kernels.  wb[w] = band of warp w; [sa, sb) = this warp's samples.
+template <int NW, int BAND, int STEP, bool BAL>
+__device__ __forceinline__ void f_band_schedule(const uint4& rw, int warp, int (&wb)[NW], int& sa, int& sb) {
+  static_assert(NW == 4, "warps-per-band code of k2f_chunk_rows is for 4 bands");
+  sa = sb = 0;
+  if (!BAL) {
+#pragma unroll
+    for (int b = 0; b < NW; ++b) {
+      wb[b] = b;
+      if (b == warp) sa = row_start(rw, b * BAND), sb = row_start(rw, (b + 1) * BAND);
+    }
+    return;
+  }
+  const unsigned code = (rw.w >> 8) & 0xfffu;  // bytes 13-14
+  int off = 0;
+#pragma unroll
+  for (int b = 0; b < NW; ++b) {
+    const int nwb = (int)((code >> (3 * b)) & 7u);
+    const int s0 = row_start(rw, b * BAND), s1 = row_start(rw, (b + 1) * BAND);
+#pragma unroll
+    for (int w = 0; w < NW; ++w)
+      if (w >= off && w < off + nwb) wb[w] = b;
+    if (warp >= off && warp < off + nwb) {
+      const int steps = (s1 - s0 + STEP - 1) / STEP;
+      const int per = (steps + nwb - 1) / nwb * STEP;
+      const int a = s0 + (warp - off) * per;
+      sa = a < s1 ? a : s1;
+      sb = a + per < s1 ? a + per : s1;
+    }
+    off += nwb;
+  }
 }
 
 // Debug-only CTA timeline (build with -DF_TIMELINE): per chunk, the SM id and
@@ -801,7 +883,7 @@ struct FSpreadM {
 #ifndef F_SBLOCKS
 #define F_SBLOCKS 3  // resident spreading CTAs per SM the register budget is sized for (smem allows 3 at F_CHUNK 144)
 #endif
-template <int P>
+template <int P, bool BAL>
 __global__ void __launch_bounds__(32 * F_MWARPS, F_SBLOCKS)
 k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ ch_s0, const int* __restrict__ ch_s1,
                const int* __restrict__ ch_count, const uint4* __restrict__ ch_rows, int cap, const int* __restrict__ base_x,
@@ -871,9 +953,24 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   bar_wait(&stage_bar, 0);
   F_TLS(1);
   const int ty0 = ty * T, tx0 = tx * T;
+#if F_MSPLIT == 1
+  // balanced schedule: this warp's band and its run of the band's K steps (f_band_schedule)
+  constexpr int half = 0;
+  int wband[F_WARPS], sa, sb;
+  f_band_schedule<F_WARPS, BAND, 4, BAL>(rw, warp, wband, sa, sb);
+  const int band = warp;  // fold record of this warp
+  int band0 = 0;
+#pragma unroll
+  for (int w = 0; w < F_WARPS; ++w)
+    if (w == warp) band0 = wband[w] * BAND;
+#else
   const int band = warp % F_WARPS, half = warp / F_WARPS;  // band of rows, K-step parity
   const int band0 = band * BAND;
   const int sa = row_start(rw, band0), sb = row_start(rw, band0 + BAND);  // precomputed band starts
+  int wband[F_WARPS];
+#pragma unroll
+  for (int w = 0; w < F_WARPS; ++w) wband[w] = w;
+#endif
   double rg[2][6][2], ly[2][2][2], lx[2][3][2], co[2][2][2];
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
@@ -1008,7 +1105,7 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
     cplx a = mk(0, 0);
 #pragma unroll
     for (int w = 0; w < F_WARPS; ++w) {
-      const int rr = r - w * BAND;
+      const int rr = r - wband[w] * BAND;
       if (rr >= 0 && rr < 16) a = cadd(a, buf[w * FM::PER_WARP + rr * R + cc]);
     }
     tb[i] = a;
@@ -1021,7 +1118,7 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
 #pragma unroll
       for (int w = 0; w < F_WARPS; ++w) {
         const cplx* wb = buf + w * FM::PER_WARP;
-        const int rr = r - w * BAND;
+        const int rr = r - wband[w] * BAND;
         if (rr >= 0 && rr < 16) a = cadd(a, wb[FM::REG + e * 16 + rr]);
         bx = cadd(bx, wb[FM::REG + FM::LYN + e * R + r]);
       }
@@ -1320,7 +1417,7 @@ __device__ __forceinline__ void f_interp_band(int band0, int half, int sa, int s
   }
 }
 
-template <int P>
+template <int P, bool BAL>
 __global__ void __launch_bounds__(32 * F_IWARPS * F_IMSPLIT, F_IBLOCKS_M)
 k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ ch_s0, const int* __restrict__ ch_s1,
                const int* __restrict__ ch_count, const uint4* __restrict__ ch_rows, int cap,
@@ -1427,8 +1524,18 @@ k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   __syncthreads();  // barrier initialised, region / lines / corners landed
   bar_wait(&stage_bar, 0);
   F_TL(1);
+#if F_IMSPLIT == 1
+  // balanced schedule: this warp's band and its run of the band's 8-sample tiles (f_band_schedule)
+  constexpr int half = 0;
+  int wband[F_IWARPS], sa, sb, band0 = 0;
+  f_band_schedule<F_IWARPS, BAND, 8, BAL>(rw, warp, wband, sa, sb);
+#pragma unroll
+  for (int w = 0; w < F_IWARPS; ++w)
+    if (w == warp) band0 = wband[w] * BAND;
+#else
   const int band0 = (warp % F_IWARPS) * BAND, half = warp / F_IWARPS;
   const int sa = row_start(rw, band0), sb = row_start(rw, band0 + BAND);  // precomputed band starts
+#endif
   f_interp_band<P, F_IMSPLIT>(band0, half, sa, sb, ty0, tx0, s_wx, s_wy, s_rx, s_ry, s_bx, s_by, gre, gim, lxre, lxim,
                               lys, cxs, (int64_t)prob * Pp.M, g0, s0, out_perm, y);
   F_TL_SYNC();
