@@ -892,6 +892,19 @@ bool rows_fft8() {  // row FFTs with global I/O in the first / last pass (defaul
   }();
   return on;
 }
+// seeded pseudo-random complex fill in [-1, 1)^2 (splitmix64 of the index): profiling inputs
+__global__ void k_fill_hash(cplx* __restrict__ v, int64_t n, unsigned long long seed) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  auto mix = [](unsigned long long z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  };
+  const unsigned long long a = mix(seed + 2 * (unsigned long long)i), b = mix(seed + 2 * (unsigned long long)i + 1);
+  v[i] = mk((double)(a >> 11) * (2.0 / 9007199254740992.0) - 1.0, (double)(b >> 11) * (2.0 / 9007199254740992.0) - 1.0);
+}
 bool spread_mma() {
   static const bool on = [] {
     const char* e = std::getenv("GS_B200_SPREAD");
@@ -1891,8 +1904,9 @@ int gs_profile_pair(gs_op* op, int reps, void* stream, int max_kernels, double* 
     x.alloc(op->Nc * op->B);
     y.alloc(op->M * op->B);
     z.alloc(op->Nc * op->B);
-    CK(cudaMemsetAsync(x.p, 0, x.bytes(), st));
-    CK(cudaMemsetAsync(y.p, 0, y.bytes(), st));
+    // live data, not zeros: x = seeded pseudo-random coefficients, y = T x from the warm-up apply
+    k_fill_hash<<<nblk(op->Nc * op->B, 256), 256, 0, st>>>(x.p, op->Nc * op->B, 0x9E3779B97F4A7C15ull);
+    CKL();
     forward_dev(op, x.p, y.p, false, st);  // warm
     adjoint_dev(op, y.p, z.p, false, st);
     CK(cudaStreamSynchronize(st));

@@ -71,10 +71,11 @@ def test_gpu_matches_reference_golden(name):
     assert st.iterations == K
     ex = float(np.linalg.norm(x[ic] - fx["x_val"]) / np.linalg.norm(fx["x_val"]))
     h = np.asarray(st.history)
-    eh = float(np.max(np.abs(h - fx["history"]) / fx["history"]))
+    big = fx["history"] > 1e-6  # residuals well above their own roundoff
+    eh = float(np.max(np.abs(h[big] - fx["history"][big]) / fx["history"][big]))
     sens = float(fx["oracle_sens"]) if "oracle_sens" in fx else 0.0
     print(f"{name} ({op.route}) vs the reference itself: b {eb:.1e}, T x {ey:.1e}, T* y {ez:.1e}; "
-          f"CGLS iterate after {K} iterations {ex:.3e} (1e-15-data sensitivity {sens:.1e}); history {eh:.1e}")
+          f"CGLS iterate after {K} iterations {ex:.3e} (1e-15-data sensitivity {sens:.1e}); residual history (entries > 1e-6) {eh:.1e}")
     assert max(eb, ey, ez) <= TOL_APPLY
     if ex > TOL_CGLS:
         ops = os.path.join(GOLD, f"cgls_{workload}_opsens.npz")

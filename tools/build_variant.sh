@@ -7,4 +7,4 @@ name=$1; shift
 mkdir -p "$ROOT/ablibs"
 cd "$ROOT/paper_1607_04091_b200/csrc"
 nvcc -O3 -lineinfo -std=c++17 -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC,-pthread "$@" \
-  -shared -o "$ROOT/ablibs/$name.so" gs_capi.cu host_inputs.cpp
+  -shared -o "$ROOT/ablibs/$name.so" gs_capi.cu gs_ndft.cu gs_plan.cu host_inputs.cpp gs_voronoi.cu

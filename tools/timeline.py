@@ -20,12 +20,13 @@ import paper_1607_04091_b200 as gs  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--problems", type=int, default=8)
+ap.add_argument("--workload", default="c5", help="c5 | c4 | c3 (2D NFFT configs)")
 a = ap.parse_args()
 gen = bench.ProductGen()
-inp = [bench.problem_inputs("c5", b, gen) for b in range(a.problems)]
+inp = [bench.problem_inputs(a.workload, b, gen) for b in range(min(a.problems, bench.problem_count(a.workload)))]
 sets = [gs.SamplingSet(2, x[3]) for x in inp]
-mu = np.concatenate([x[4] for x in inp])
-op = gs.freq2wave(sets, 4, 8, bandwidth=max(x[5] for x in inp), weights=mu)
+mu = np.concatenate([x[4] for x in inp]) if inp[0][4] is not None else None
+op = gs.freq2wave(sets, inp[0][1], inp[0][2], bandwidth=max(x[5] for x in inp), weights=mu)
 L = gs.load_library()
 y = torch.randn(op.rows() * op.batch, dtype=torch.complex128, device="cuda")
 sess = gs.CglsSession(op, y)
