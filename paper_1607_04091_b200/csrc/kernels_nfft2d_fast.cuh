@@ -862,7 +862,9 @@ template <int P>
 struct FSpreadM {
   static constexpr int E = P >= 2 ? 2 * P : 0;
   // per-warp fold record: region 16 x 24 (complex), y-lines 8 x 16, x-lines 8 x 24 (complex), corner P 16 x 16 (real)
-  static constexpr int REG = 16 * F_R, LYN = 8 * 16, LXN = 8 * F_R, PN = 16 * 16 / 2;  // in complex units
+  // (rows of RP = F_R + 1 complex: the 8 row groups of a DMMA fragment store land in distinct banks)
+  static constexpr int RP = F_R + 1;
+  static constexpr int REG = 16 * RP, LYN = 8 * 17, LXN = 8 * RP, PN = 16 * 16 / 2;  // in complex units
   static constexpr int PER_WARP = REG + LYN + LXN + PN;
   static constexpr size_t FOLD = sizeof(cplx) * F_WARPS * PER_WARP;  // one record per band
   // staging (structure of arrays, sample order; 16 B of slack each); the factor
@@ -880,6 +882,12 @@ struct FSpreadM {
   static constexpr size_t bytes() { return (MAIN + 15) / 16 * 16; }
 };
 
+#ifndef F_DESC_HOIST
+#define F_DESC_HOIST 0  // 1: chunk descriptor loads issued before the live-chunk test resolves (measured slower on C5: off)
+#endif
+#ifndef F_FOLD_UNROLL
+#define F_FOLD_UNROLL 1  // chunk fold with compile-time trip counts (all of a thread's loads in flight)
+#endif
 #ifndef F_SBLOCKS
 #define F_SBLOCKS 3  // resident spreading CTAs per SM the register budget is sized for (smem allows 3 at F_CHUNK 144)
 #endif
@@ -893,13 +901,21 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   using F = FSpread<P>;
   using FM = FSpreadM<P>;
   constexpr int S = F_S, T = F_T, R = F_R, BAND = F_BAND, E = F::E, RR = F::RR, NCE = F::NCE, MU = F_MUNROLL;
+  constexpr int RP = FM::RP;
   extern __shared__ __align__(16) unsigned char fsm_raw[];
   cplx* s_ys = reinterpret_cast<cplx*>(fsm_raw + FM::YS);
   const int prob = blockIdx.y, c = blockIdx.x;
+  // descriptor loads issued with the live-chunk test, not behind it (one L2 round trip, not two)
+#if F_DESC_HOIST
+  const int nlive = ch_count[prob];
+#else
   if (c >= ch_count[prob]) return;
-  F_TLS(0);
+  constexpr int nlive = 0x7fffffff;
+#endif
   const int tile = ch_tile[prob * cap + c], s0 = ch_s0[prob * cap + c], s1 = ch_s1[prob * cap + c];
   const uint4 rw = ch_rows[prob * cap + c];
+  if (c >= nlive) return;
+  F_TLS(0);
   const int n = s1 - s0;
   const int ty = tile / Pp.nt, tx = tile - ty * Pp.nt;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
@@ -1080,53 +1096,65 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
         for (int nt = 0; nt < 3; ++nt)
 #pragma unroll
           for (int j = 0; j < 2; ++j)
-            put(&mreg[(mt * 8 + g) * R + nt * 8 + 2 * t + j], mk(rg[mt][nt][j], rg[mt][nt + 3][j]));
+            put(&mreg[(mt * 8 + g) * RP + nt * 8 + 2 * t + j], mk(rg[mt][nt][j], rg[mt][nt + 3][j]));
       if (E > 0) {
 #pragma unroll
         for (int nn = 0; nn < 2; ++nn)
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
-            put(&mly[g * 16 + nn * 8 + 2 * t + j], mk(ly[0][nn][j], ly[1][nn][j]));
+            put(&mly[g * 17 + nn * 8 + 2 * t + j], mk(ly[0][nn][j], ly[1][nn][j]));
 #pragma unroll
             for (int mm = 0; mm < 2; ++mm) putd(&mp[(mm * 8 + g) * 16 + nn * 8 + 2 * t + j], co[mm][nn][j]);
           }
 #pragma unroll
         for (int nt = 0; nt < 3; ++nt)
 #pragma unroll
-          for (int j = 0; j < 2; ++j) put(&mlx[g * R + nt * 8 + 2 * t + j], mk(lx[0][nt][j], lx[1][nt][j]));
+          for (int j = 0; j < 2; ++j) put(&mlx[g * RP + nt * 8 + 2 * t + j], mk(lx[0][nt][j], lx[1][nt][j]));
       }
     }
     __syncthreads();
   }
+  // chunk fold: every output sums the warp records that cover it, in warp order.  Trip counts
+  // are compile-time (NT threads), so the loads of a thread's outputs are all in flight together.
+  constexpr int NT = 32 * F_MWARPS;
+  constexpr int FU_TB = F_FOLD_UNROLL ? (R * R + NT - 1) / NT : 1, FU_TL = F_FOLD_UNROLL ? (E * R + NT - 1) / NT + 1 : 1;
   const int64_t chunk = (int64_t)prob * cap + c;
   cplx* tb = TB + chunk * R * R;
-  for (int i = threadIdx.x; i < R * R; i += blockDim.x) {
-    const int r = i / R, cc = i - r * R;
-    cplx a = mk(0, 0);
+#pragma unroll FU_TB
+  for (int it = 0; it < (R * R + NT - 1) / NT; ++it) {
+    const int i = it * NT + (int)threadIdx.x;
+    if (i < R * R) {
+      const int r = i / R, cc = i - r * R;
+      cplx a = mk(0, 0);
 #pragma unroll
-    for (int w = 0; w < F_WARPS; ++w) {
-      const int rr = r - wband[w] * BAND;
-      if (rr >= 0 && rr < 16) a = cadd(a, buf[w * FM::PER_WARP + rr * R + cc]);
+      for (int w = 0; w < F_WARPS; ++w) {
+        const int rr = r - wband[w] * BAND;
+        if (rr >= 0 && rr < 16) a = cadd(a, buf[w * FM::PER_WARP + rr * RP + cc]);
+      }
+      tb[i] = a;
     }
-    tb[i] = a;
   }
   if (E > 0) {
     cplx* tl = TL + chunk * 2 * E * R;  // [y-lines e][row] then [x-lines e][column]
-    for (int i = threadIdx.x; i < E * R; i += blockDim.x) {
-      const int e = i / R, r = i - e * R;
-      cplx a = mk(0, 0), bx = mk(0, 0);
+#pragma unroll FU_TL
+    for (int it = 0; it < (E * R + NT - 1) / NT; ++it) {
+      const int i = it * NT + (int)threadIdx.x;
+      if (i < E * R) {
+        const int e = i / R, r = i - e * R;
+        cplx a = mk(0, 0), bx = mk(0, 0);
 #pragma unroll
-      for (int w = 0; w < F_WARPS; ++w) {
-        const cplx* wb = buf + w * FM::PER_WARP;
-        const int rr = r - wband[w] * BAND;
-        if (rr >= 0 && rr < 16) a = cadd(a, wb[FM::REG + e * 16 + rr]);
-        bx = cadd(bx, wb[FM::REG + FM::LYN + e * R + r]);
+        for (int w = 0; w < F_WARPS; ++w) {
+          const cplx* wb = buf + w * FM::PER_WARP;
+          const int rr = r - wband[w] * BAND;
+          if (rr >= 0 && rr < 16) a = cadd(a, wb[FM::REG + e * 17 + rr]);
+          bx = cadd(bx, wb[FM::REG + FM::LYN + e * RP + r]);
+        }
+        tl[i] = a;
+        tl[E * R + i] = bx;
       }
-      tl[i] = a;
-      tl[E * R + i] = bx;
     }
     cplx* tc = TC + chunk * NCE;
-    for (int q = threadIdx.x; q < NCE; q += blockDim.x) {
+    for (int q = threadIdx.x; q < NCE; q += NT) {
       const int k = q / (P * P), rem = q - k * P * P, i = rem / P, j = rem - i * P;
       const int ip = (k < 2 ? 0 : P) + i, jp = (k % 2 == 0 ? 0 : P) + j;  // ca index (Lx | Rx), b index (Ly | Ry)
       double re = 0.0, im = 0.0;
@@ -1438,11 +1466,18 @@ k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   __shared__ __align__(16) cplx cxs[P >= 2 ? 4 * P * P : 1];
   __shared__ __align__(8) uint64_t stage_bar;
   const int prob = blockIdx.y, c = blockIdx.x;
-  if (c >= ch_count[prob]) return;
   const int64_t chunk = (int64_t)prob * cap + c;
-  F_TL(0);
+  // descriptor loads issued with the live-chunk test, not behind it (one L2 round trip, not two)
+#if F_DESC_HOIST
+  const int nlive = ch_count[prob];
+#else
+  if (c >= ch_count[prob]) return;
+  constexpr int nlive = 0x7fffffff;
+#endif
   const int tile = ch_tile[chunk], s0 = ch_s0[chunk], s1 = ch_s1[chunk];
   const uint4 rw = ch_rows[chunk];
+  if (c >= nlive) return;
+  F_TL(0);
   const int n = s1 - s0;
   const int ty = tile / Pp.nt, tx = tile - ty * Pp.nt;
   const int ty0 = ty * T, tx0 = tx * T;
