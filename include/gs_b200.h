@@ -210,11 +210,17 @@ int gs_densify(int dim, int family_p, int J, int64_t M, const double* coords, co
                int64_t entry_cap, double* out, void* stream);
 
 /* Per-kernel device time of one T + T* pair (no reference counterpart; the
- * measurement hook bench.py uses for the roofline): `reps` pairs on zeroed
- * buffers, CUDA events between consecutive launches on `stream`.  Writes up
- * to max_kernels average durations (ms) and 32-byte kernel names. */
+ * measurement hook bench.py uses for the roofline): `reps` pairs on live data
+ * (seeded pseudo-random coefficients x, y = T x), CUDA events between
+ * consecutive launches on `stream`.  Writes up to max_kernels average
+ * durations (ms) and 32-byte kernel names. */
 int gs_profile_pair(gs_op* op, int reps, void* stream, int max_kernels, double* ms_out,
                     char* names_out, int* count);
+
+/* 1 when the handle's 2D gridding kernels run the balanced band schedule (the
+ * sampling pattern loads the 3-row bands of its tiles unevenly, e.g. a
+ * spiral), 0 for the static one; no reference counterpart (diagnostic). */
+int gs_op_balanced_schedule(const gs_op* op);
 
 /* Dyadic-grid evaluation (dyadic.hpp:27-64; front-end row SURVEY 8(f)4).
  * Tables of the interior scaling function / of edge function k of one side

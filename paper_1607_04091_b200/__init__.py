@@ -251,6 +251,8 @@ class Freq2WaveOp:
         self._weighted = bool(info.weighted)
         self.n_over = info.n_over
         self.device_bytes = info.device_bytes
+        # 2D gridding kernels on the balanced band schedule (uneven patterns, e.g. spirals)
+        self.balanced_schedule = bool(load_library().gs_op_balanced_schedule(handle))
 
     def rows(self):
         return self._rows

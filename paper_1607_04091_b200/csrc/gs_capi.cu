@@ -775,7 +775,7 @@ gs_op* create(const gs_op_desc* dsc) {
         unsigned long long hb[2] = {0, 0};
         CK(cudaMemcpyAsync(hb, bal.p, sizeof(hb), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        static const char* benv = getenv("GS_B200_BALANCE");  // 0 / 1 force the static / balanced kernels (A/B)
+        const char* benv = getenv("GS_B200_BALANCE");  // 0 / 1 force the static / balanced kernels (A/B, tests)
         op->balanced = benv ? atoi(benv) != 0 : (double)hb[0] > 1.05 * (double)hb[1];
       }
       if (op->fast2d) {  // fold sources per tile (k2_fold_src): same order as k2_fold_tiles' coverage loops
@@ -2155,6 +2155,8 @@ int gs_densify(int dim, int family_p, int J, int64_t M, const double* coords, co
     CK(cudaStreamSynchronize(st));
   });
 }
+
+int gs_op_balanced_schedule(const gs_op* op) { return op && op->balanced ? 1 : 0; }
 
 #ifdef F_TIMELINE
 // debug builds only: copy the CTA timeline of the last fast-path launch (kernels_nfft2d_fast.cuh)

@@ -426,3 +426,31 @@ print("ok" + json.dumps(out, default=lambda z: [z.real, z.imag]))
             assert a[3] == b[3], k
         else:
             assert a[1] == b[1]
+
+
+def test_balanced_band_schedule_matches_static(monkeypatch):
+    """A spiral loads the 3-row bands of its tiles unevenly: the operator picks
+    the balanced band schedule of the DMMA kernels by itself, a jittered grid
+    keeps the static one, and the two schedules agree to roundoff (they sum the
+    same products in a different warp order)."""
+    import paper_1607_04091_b200 as gs
+    c = oracle.gen_spiral(12, 2048.0, 60.0)
+    ops = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("GS_B200_BALANCE", flag)
+        ops[flag] = gs.freq2wave(gs.SamplingSet(2, c), "db4", 6, bandwidth=64.0)
+    monkeypatch.delenv("GS_B200_BALANCE")
+    auto = gs.freq2wave(gs.SamplingSet(2, c), "db4", 6, bandwidth=64.0)
+    assert ops["1"].route == "nfft_2d" and ops["1"].balanced_schedule and not ops["0"].balanced_schedule
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal(auto.cols()) + 1j * rng.standard_normal(auto.cols())
+    y = rng.standard_normal(auto.rows()) + 1j * rng.standard_normal(auto.rows())
+    ref = oracle.Op(2, 4, 6, c, bandwidth=64.0)
+    for name, op in (("balanced", ops["1"]), ("static", ops["0"])):
+        ef, ea = rel_error(gs.apply_forward(op, x), ref.forward(x)), rel_error(gs.apply_adjoint(op, y), ref.adjoint(y))
+        print(f"spiral, {name} schedule: T x {ef:.1e}, T* y {ea:.1e}")
+        assert ef <= TOL_APPLY and ea <= TOL_APPLY
+    print("auto-selected schedule on the spiral:", "balanced" if auto.balanced_schedule else "static")
+    assert auto.balanced_schedule
+    cj = oracle.gen_jitter(64, 0.5, 0.2, 3, 2)
+    assert not gs.freq2wave(gs.SamplingSet(2, cj), "db4", 5, bandwidth=17.0).balanced_schedule
