@@ -622,13 +622,21 @@ def _cpu_problem(workload, b, impl):
 
 
 def _cpu_iter_seconds(op, data, k):
-    """Seconds per CGLS iteration: (T(solve 1+k) - T(solve 1)) / k (removes the preamble)."""
-    t = time.perf_counter()
-    op.solve(data, max_iterations=1, tolerance=1e-300)
-    t1 = time.perf_counter() - t
-    t = time.perf_counter()
-    op.solve(data, max_iterations=1 + k, tolerance=1e-300)
-    t2 = time.perf_counter() - t
+    """Seconds per CGLS iteration: (T(solve 1+k) - T(solve 1)) / k (removes the
+    preamble), each solve repeated until it has run for ~0.5 s in total so that
+    the microsecond-scale configs are timed over thousands of iterations."""
+    def solve(n):
+        t = time.perf_counter()
+        op.solve(data, max_iterations=n, tolerance=1e-300)
+        return time.perf_counter() - t
+
+    probe = solve(1 + k)
+    reps = int(max(1, min(2000, math.ceil(0.5 / max(probe, 1e-6)))))
+    if reps == 1:
+        t1, t2 = solve(1), probe
+    else:
+        t1 = min(sum(solve(1) for _ in range(reps)) / reps for _ in range(2))
+        t2 = min(sum(solve(1 + k) for _ in range(reps)) / reps for _ in range(2))
     return max(1e-9, (t2 - t1) / k), t1, t2
 
 
@@ -667,7 +675,9 @@ def run_reference(args):
     ncpu = cpu["logical_cpus_available"]
     P = args.problems or problem_count(args.workload)
     threads = max(1, min(ncpu, P, 64 if args.workload == "c5" else 1))
-    k = max(1, min(args.steps, 3 if args.workload in ("c4", "c5", "c3") else 20))
+    # CGLS iterations per timed solve: bounded on the large configs (seconds per iteration on a
+    # core), the small ones repeat the solve until ~0.5 s has been timed (_cpu_iter_seconds)
+    k = max(1, min(args.steps, 3)) if args.workload in ("c4", "c5", "c3") else 20
     rates = [0.0] * threads
     errs = []
 

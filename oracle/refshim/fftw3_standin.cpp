@@ -12,6 +12,9 @@
 #include <cmath>
 #include <complex>
 #include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <vector>
 
 namespace {
@@ -52,15 +55,30 @@ struct Axis {
     void run(const cd* in, long is, cd* out, cd* scratch) const {
         if (pow2) {
             for (int i = 0; i < n; ++i) out[rev[static_cast<size_t>(i)]] = in[static_cast<long>(i) * is];
-            for (int half = 1; half < n; half <<= 1) {
+            auto mul = [](const cd& a, const cd& b) {  // plain complex product (finite operands)
+                return cd(a.real() * b.real() - a.imag() * b.imag(), a.real() * b.imag() + a.imag() * b.real());
+            };
+            int half = 1;
+            if (n >= 2) {  // first stage: twiddle 1
+                for (int base = 0; base < n; base += 2) {
+                    const cd u = out[base], t = out[base + 1];
+                    out[base] = u + t;
+                    out[base + 1] = u - t;
+                }
+                half = 2;
+            }
+            for (; half < n; half <<= 1) {
                 const int stride = n / (2 * half);
-                for (int base = 0; base < n; base += 2 * half)
+                for (int base = 0; base < n; base += 2 * half) {
+                    cd* lo = out + base;
+                    cd* hi = lo + half;
                     for (int k = 0; k < half; ++k) {
-                        cd t = out[base + half + k] * tw[static_cast<size_t>(k * stride)];
-                        cd u = out[base + k];
-                        out[base + k] = u + t;
-                        out[base + half + k] = u - t;
+                        const cd t = mul(hi[k], tw[static_cast<size_t>(k * stride)]);
+                        const cd u = lo[k];
+                        lo[k] = u + t;
+                        hi[k] = u - t;
                     }
+                }
             }
         } else {
             rec(in, is, out, scratch, n, 0);
@@ -86,11 +104,27 @@ struct Axis {
         }
     }
 };
+
+// Twiddle / bit-reversal tables are kept per (length, sign) for the life of the
+// process, as FFTW keeps its own twiddle caches across plans: the reference plans
+// the uniform reductions anew on every call (nufft.cpp:410, 440).
+std::shared_ptr<const Axis> axis_for(int n, int sign) {
+    static std::mutex mu;
+    static std::map<std::pair<int, int>, std::shared_ptr<const Axis>> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    auto& slot = cache[{n, sign}];
+    if (!slot) {
+        auto a = std::make_shared<Axis>();
+        a->init(n, sign);
+        slot = a;
+    }
+    return slot;
+}
 }  // namespace
 
 struct fftw_standin_plan {
     int rank = 1;
-    Axis ax[2];
+    std::shared_ptr<const Axis> ax[2];
 };
 
 extern "C" {
@@ -99,34 +133,40 @@ fftw_plan fftw_plan_dft(int rank, const int* n, fftw_complex*, fftw_complex*, in
     if (rank < 1 || rank > 2) return nullptr;
     auto* p = new fftw_standin_plan;
     p->rank = rank;
-    for (int a = 0; a < rank; ++a) p->ax[a].init(n[a], sign < 0 ? -1 : 1);
+    for (int a = 0; a < rank; ++a) p->ax[a] = axis_for(n[a], sign < 0 ? -1 : 1);
     return p;
 }
 
 void fftw_execute_dft(const fftw_plan p, fftw_complex* in_, fftw_complex* out_) {
     const cd* in = reinterpret_cast<const cd*>(in_);
     cd* out = reinterpret_cast<cd*>(out_);
+    // per-thread work buffers, grown on demand (no allocation per transform)
+    thread_local std::vector<cd> line, res, scratch;
     if (p->rank == 1) {
-        const int n = p->ax[0].n;
-        std::vector<cd> scratch(static_cast<size_t>(2 * n + 2));
+        const int n = p->ax[0]->n;
+        if (!p->ax[0]->pow2 && scratch.size() < static_cast<size_t>(2 * n + 2)) scratch.resize(static_cast<size_t>(2 * n + 2));
         if (in == out) {
-            std::vector<cd> tmp(in, in + n);
-            p->ax[0].run(tmp.data(), 1, out, scratch.data());
+            if (line.size() < static_cast<size_t>(n)) line.resize(static_cast<size_t>(n));
+            std::memcpy(static_cast<void*>(line.data()), static_cast<const void*>(in), sizeof(cd) * static_cast<size_t>(n));
+            p->ax[0]->run(line.data(), 1, out, scratch.data());
         } else {
-            p->ax[0].run(in, 1, out, scratch.data());
+            p->ax[0]->run(in, 1, out, scratch.data());
         }
         return;
     }
-    const int n0 = p->ax[0].n, n1 = p->ax[1].n;
-    std::vector<cd> line(static_cast<size_t>(std::max(n0, n1))), res(line.size()), scratch(2 * line.size() + 2);
+    const int n0 = p->ax[0]->n, n1 = p->ax[1]->n;
+    const size_t nm = static_cast<size_t>(std::max(n0, n1));
+    if (line.size() < nm) line.resize(nm);
+    if (res.size() < nm) res.resize(nm);
+    if (scratch.size() < 2 * nm + 2) scratch.resize(2 * nm + 2);
     for (int i = 0; i < n0; ++i) {  // rows (contiguous)
         std::memcpy(static_cast<void*>(line.data()), static_cast<const void*>(in + static_cast<size_t>(i) * n1),
                     sizeof(cd) * static_cast<size_t>(n1));
-        p->ax[1].run(line.data(), 1, out + static_cast<size_t>(i) * n1, scratch.data());
+        p->ax[1]->run(line.data(), 1, out + static_cast<size_t>(i) * n1, scratch.data());
     }
     for (int j = 0; j < n1; ++j) {  // columns
         for (int i = 0; i < n0; ++i) line[static_cast<size_t>(i)] = out[static_cast<size_t>(i) * n1 + j];
-        p->ax[0].run(line.data(), 1, res.data(), scratch.data());
+        p->ax[0]->run(line.data(), 1, res.data(), scratch.data());
         for (int i = 0; i < n0; ++i) out[static_cast<size_t>(i) * n1 + j] = res[static_cast<size_t>(i)];
     }
 }
