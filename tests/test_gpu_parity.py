@@ -452,5 +452,6 @@ def test_balanced_band_schedule_matches_static(monkeypatch):
         assert ef <= TOL_APPLY and ea <= TOL_APPLY
     print("auto-selected schedule on the spiral:", "balanced" if auto.balanced_schedule else "static")
     assert auto.balanced_schedule
-    cj = oracle.gen_jitter(64, 0.5, 0.2, 3, 2)
-    assert not gs.freq2wave(gs.SamplingSet(2, cj), "db4", 5, bandwidth=17.0).balanced_schedule
+    # a jittered grid fills the bands evenly (C5's shape, smaller): static kernels
+    cj = oracle.gen_jitter(256, 0.5, 0.2, 3, 2)
+    assert not gs.freq2wave(gs.SamplingSet(2, cj), "db4", 7, bandwidth=65.0).balanced_schedule

@@ -22,6 +22,9 @@ cases = [
     ("nfft1d db4", 1, 4, 6, oracle.gen_jitter(200, 0.5, 0.2, 3, 1), None, "w"),
     ("tensor db2", 2, 2, 4, oracle.gen_grid(32, 1.0, 2), 16.0, None),
     ("nfft2d db4", 2, 4, 5, oracle.gen_jitter(48, 0.5, 0.2, 4, 2), None, "w"),
+    # spiral: uneven bands -> the balanced band schedule of the DMMA kernels, multi-chunk tiles
+    ("nfft2d db4 spiral", 2, 4, 5, oracle.gen_spiral(6, 1024.0, 15.0), 16.0, None),
+    ("nfft2d db2 spiral", 2, 2, 5, oracle.gen_spiral(6, 1024.0, 15.0), 16.0, None),
 ]
 for name, dim, p, J, c, bw, w in cases:
     K = bw if bw is not None else float(np.max(np.abs(c))) + 1e-9
@@ -30,5 +33,6 @@ for name, dim, p, J, c, bw, w in cases:
     y = gs.apply_forward(op, rc(op.cols()))
     z = gs.apply_adjoint(op, rc(op.rows()))
     x, st = gs.solve_least_squares(op, y + 1e-3 * rc(op.rows()), max_iterations=4, tolerance=1e-300)
-    print(name, op.route, st.iterations, float(np.linalg.norm(x)), float(np.linalg.norm(z)))
+    print(name, op.route, "balanced" if getattr(op, "balanced_schedule", False) else "static", st.iterations,
+          float(np.linalg.norm(x)), float(np.linalg.norm(z)))
 print("sanitize ok")
