@@ -722,6 +722,8 @@ gs_op* create(const gs_op_desc* dsc) {
       std::vector<int> starts((size_t)B * (ntiles + 1));
       CK(cudaMemcpy(starts.data(), op->bins.p, starts.size() * sizeof(int), cudaMemcpyDeviceToHost));
       const int kChunk = F_CHUNK;
+      const char* ec_env = getenv("GS_B200_EVEN_CHUNKS");
+      const bool even_chunks = !(ec_env && atoi(ec_env) == 0);
       std::vector<std::vector<int>> ct(B), c0(B), c1(B);
       std::vector<int> tcs((size_t)B * (ntiles + 1));
       int cap = 1;
@@ -737,10 +739,17 @@ gs_op* create(const gs_op_desc* dsc) {
             c1[b].push_back(e);
             continue;
           }
-          for (int s = a; s < e; s += kChunk) {
+          // dense tiles: equal chunks (a tile of 150 samples is 75 + 75, not 144 + 6), rounded
+          // up to whole K steps of 4 samples; GS_B200_EVEN_CHUNKS=0 restores the greedy split
+          int step = kChunk;
+          if (even_chunks && e - a > kChunk) {
+            const int k = (e - a + kChunk - 1) / kChunk;
+            step = std::min(kChunk, ((e - a + k - 1) / k + 3) / 4 * 4);
+          }
+          for (int s = a; s < e; s += step) {
             ct[b].push_back((int)t);
             c0[b].push_back(s);
-            c1[b].push_back(std::min(e, s + kChunk));
+            c1[b].push_back(std::min(e, s + step));
           }
         }
         tb[ntiles] = (int)ct[b].size();

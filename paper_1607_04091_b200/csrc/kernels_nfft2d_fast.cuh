@@ -906,6 +906,12 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   cplx* s_ys = reinterpret_cast<cplx*>(fsm_raw + FM::YS);
   const int prob = blockIdx.y, c = blockIdx.x;
   // descriptor loads issued with the live-chunk test, not behind it (one L2 round trip, not two)
+#if F_DESC_HOIST == 2
+  // dead work-list slots hold an empty sample range: no ch_count round trip before the descriptors
+  const int tile = ch_tile[prob * cap + c], s0 = ch_s0[prob * cap + c], s1 = ch_s1[prob * cap + c];
+  const uint4 rw = ch_rows[prob * cap + c];
+  if (s1 <= s0) return;
+#else
 #if F_DESC_HOIST
   const int nlive = ch_count[prob];
 #else
@@ -915,6 +921,7 @@ k2f_spread_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   const int tile = ch_tile[prob * cap + c], s0 = ch_s0[prob * cap + c], s1 = ch_s1[prob * cap + c];
   const uint4 rw = ch_rows[prob * cap + c];
   if (c >= nlive) return;
+#endif
   F_TLS(0);
   const int n = s1 - s0;
   const int ty = tile / Pp.nt, tx = tile - ty * Pp.nt;
@@ -1468,6 +1475,11 @@ k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   const int prob = blockIdx.y, c = blockIdx.x;
   const int64_t chunk = (int64_t)prob * cap + c;
   // descriptor loads issued with the live-chunk test, not behind it (one L2 round trip, not two)
+#if F_DESC_HOIST == 2
+  const int tile = ch_tile[chunk], s0 = ch_s0[chunk], s1 = ch_s1[chunk];
+  const uint4 rw = ch_rows[chunk];
+  if (s1 <= s0) return;
+#else
 #if F_DESC_HOIST
   const int nlive = ch_count[prob];
 #else
@@ -1477,6 +1489,7 @@ k2f_interp_mma(NfP Pp, const int* __restrict__ ch_tile, const int* __restrict__ 
   const int tile = ch_tile[chunk], s0 = ch_s0[chunk], s1 = ch_s1[chunk];
   const uint4 rw = ch_rows[chunk];
   if (c >= nlive) return;
+#endif
   F_TL(0);
   const int n = s1 - s0;
   const int ty = tile / Pp.nt, tx = tile - ty * Pp.nt;
