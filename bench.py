@@ -412,6 +412,31 @@ def run_gpu(args):
         roofline_fp64[k] = {"bound": "fp64", "achieved": round(tf, 3), "peak": fpeak, "unit": "TFLOP/s",
                             "frac": round(tf / fpeak, 4), "flops_per_launch": fl * B, "launch_ms": round(prof[k], 4),
                             "peak_source": fpeak_src}
+    # HBM-bound passes of the 2D NFFT route (FFT / fold kernels): compulsory bytes of one launch
+    # per problem / the live launch time.  n = coefficients per axis, n_ov = oversampled length;
+    # the embedded block has n non-zero rows, so row passes touch n * n_ov entries and column
+    # passes n * n_ov on one side and the full n_ov^2 grid on the other.  Folds: the per-chunk
+    # partials are counted once per tile (>= one chunk per non-empty tile: a lower bound).
+    roofline_passes = {}
+    n_ov = int(getattr(op, "n_over", 0) or 0)
+    if dim == 2 and n_ov and any(k.startswith("k2_") for k in prof):
+        n_ax = int(round(Nc ** 0.5))
+        ntile = ((n_ov + 11) // 12) ** 2
+        R, E = 24, (2 * p if p >= 2 else 0)
+        pass_bytes = {
+            "k2_rows_embed_fft": 16 * Nc + 16 * n_ax * n_ov,
+            "k2_cols_fft": 16 * n_ax * n_ov + 16 * n_ov * n_ov,
+            "k2_fold_tiles": 16 * R * R * ntile + 16 * n_ov * n_ov,
+            "k2_cols_ifft": 16 * n_ov * n_ov + 16 * n_ax * n_ov,
+            "k2_rows_ifft_crop": 16 * n_ax * n_ov + 16 * Nc,
+            "k2_fold_lines": 16 * 2 * E * R * ntile,
+        }
+        for k, bts in pass_bytes.items():
+            if k in prof and prof[k] > 0 and bts > 0:
+                g = bts * B / (prof[k] / 1e3) / 1e9
+                roofline_passes[k] = {"bound": "hbm", "achieved": round(g, 1), "peak": peak, "unit": "GB/s",
+                                      "frac": round(g / peak, 4), "bytes_per_launch": bts * B,
+                                      "launch_ms": round(prof[k], 4)}
     pair_b, it_b = iteration_bytes(dim, p, M, Nc, uaxis)
     it_gbs = it_b * P / (ms_per_step / 1e3) / 1e9
     roof_iter = {"bytes_per_problem_iteration": it_b, "achieved_gbs": round(it_gbs, 2),
@@ -455,6 +480,7 @@ def run_gpu(args):
             "gpu_launches": int(launches),
             "roofline": roofline, "roofline_iteration": roof_iter,
             "roofline_fp64": roofline_fp64 or None,
+            "roofline_passes": roofline_passes or None,
             "kernel_ms_per_pair": {k: round(v, 4) for k, v in prof.items()},
             "e2e": {"value": round(e2e_value, 3), "unit": "problem-iterations/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "h2d_bytes_per_call": h2d_call, "d2h_bytes_per_call": d2h_call,

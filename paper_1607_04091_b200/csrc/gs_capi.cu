@@ -674,7 +674,10 @@ gs_op* create(const gs_op_desc* dsc) {
 #endif
     P.CW = std::max(1, std::min(F_CWMAX, (int)((F_CWBUDGET) / ((fpad_len(n_ov) + 1) * (int)sizeof(cplx)))));
     while (n_ov % P.CW) --P.CW;
-    P.RW = std::max(1, std::min(8, 2048 / n_ov));
+#ifndef F_RWPTS  // grid points per row-FFT CTA (256 threads, one 8-point group each at 2048)
+#define F_RWPTS 2048
+#endif
+    P.RW = std::max(1, std::min(8, F_RWPTS / n_ov));
     d_xi_x.upload(xi_x.data(), total, st);
     if (d.dim == 2) d_xi_y.upload(xi_y.data(), total, st);
     // 1. windows in the caller's order -> bin keys -> sort
