@@ -227,6 +227,8 @@ __device__ __forceinline__ void f_band_schedule(const uint4& rw, int warp, int (
   const unsigned code = (rw.w >> 8) & 0xfffu;  // bytes 13-14
   int off = 0;
 #pragma unroll
+  for (int w = 0; w < NW; ++w) wb[w] = w;  // (a live chunk's code always covers all NW warps)
+#pragma unroll
   for (int b = 0; b < NW; ++b) {
     const int nwb = (int)((code >> (3 * b)) & 7u);
     const int s0 = row_start(rw, b * BAND), s1 = row_start(rw, (b + 1) * BAND);
