@@ -1057,14 +1057,14 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
       const NfP& P = op->np;
       if (op->logLmax == P.log_nov && rows_fft8())
         k2_rows_fft8<true><<<dim3((P.n + P.RW - 1) / P.RW, B), 256,
-                              ((size_t)P.RW * (fpad_len(P.n_ov) + 1) + P.n_ov / 2) * sizeof(cplx), st>>>(
+                              ((size_t)P.RW * (rpad_len(P.n_ov) + 1) + P.n_ov / 2) * sizeof(cplx), st>>>(
             P, x, op->deconv.p, op->G.p, op->tw.p);
       else
         k2_rows_embed_fft<<<dim3((P.n + P.RW - 1) / P.RW, B), 256, (size_t)P.RW * (fpad_len(P.n_ov) + 1) * sizeof(cplx), st>>>(P, x, op->deconv.p, op->G.p, op->tw.p,
                                                                           op->logLmax);
       pmark("k2_rows_embed_fft", st);
       if (op->logLmax == P.log_nov && cols_fft8())
-        k2_cols_fft8<true><<<dim3(P.n_ov / P.CW, B), 256,
+        k2_cols_fft8<true><<<dim3(P.n_ov / P.CW, B), F_COLS_THREADS,
                               ((size_t)P.CW * (fpad_len(P.n_ov) + 1) + P.n_ov / 2) * sizeof(cplx), st>>>(P, op->G.p,
                                                                                                         op->tw.p);
       else
@@ -1220,7 +1220,7 @@ bool adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
                                                                                   op->cov.p, op->covn.p, op->G.p);
       pmark("k2_fold_tiles", st);
       if (op->logLmax == P.log_nov && cols_fft8())
-        k2_cols_fft8<false><<<dim3(P.n_ov / P.CW, B), 256,
+        k2_cols_fft8<false><<<dim3(P.n_ov / P.CW, B), F_COLS_THREADS,
                                ((size_t)P.CW * (fpad_len(P.n_ov) + 1) + P.n_ov / 2) * sizeof(cplx), st>>>(P, op->G.p,
                                                                                                          op->tw.p);
       else
@@ -1229,7 +1229,7 @@ bool adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
       pmark("k2_cols_ifft", st);
       if (op->logLmax == P.log_nov && rows_fft8())
         k2_rows_fft8<false><<<dim3((P.n + P.RW - 1) / P.RW, B), 256,
-                               ((size_t)P.RW * (fpad_len(P.n_ov) + 1) + P.n_ov / 2) * sizeof(cplx), st>>>(
+                               ((size_t)P.RW * (rpad_len(P.n_ov) + 1) + P.n_ov / 2) * sizeof(cplx), st>>>(
             P, op->G.p, op->deconv.p, z, op->tw.p);
       else
         k2_rows_ifft_crop<<<dim3((P.n + P.RW - 1) / P.RW, B), 256, (size_t)P.RW * (fpad_len(P.n_ov) + 1) * sizeof(cplx), st>>>(P, op->G.p, op->deconv.p, z, op->tw.p,

@@ -837,8 +837,14 @@ __device__ __forceinline__ void cols_pass(const NfP& P, cplx* __restrict__ g, cp
   }
 }
 
+#ifndef F_COLS_THREADS
+#define F_COLS_THREADS 256  // threads of a column-FFT CTA
+#endif
+#ifndef F_COLS_MINB
+#define F_COLS_MINB 2
+#endif
 template <bool FWD>
-__global__ void k2_cols_fft8(NfP P, cplx* __restrict__ G, const cplx* __restrict__ tw) {
+__global__ void __launch_bounds__(F_COLS_THREADS, F_COLS_MINB) k2_cols_fft8(NfP P, cplx* __restrict__ G, const cplx* __restrict__ tw) {
   extern __shared__ cplx sm[];
   const int L = P.log_nov, N = P.n_ov, CW = P.CW;
   const int ls = fpad_len(N) + 1;
@@ -864,6 +870,14 @@ __global__ void k2_cols_fft8(NfP P, cplx* __restrict__ G, const cplx* __restrict
 // embedded, deconvolved row of X for the forward; the row of G for the
 // inverse) and the last pass writes its outputs (the whole row of G; the
 // cropped, deconvolved row of Z), twiddles in shared memory.
+// Row-FFT shared-memory layout: one pad per 8 and per 64 elements, so that the
+// first pass's stores (groups in bit-reversed order, F_ROWS_COAL) as well as the
+// strided accesses of the later passes spread over the 16-B bank groups.
+#ifndef F_ROWS_COAL
+#define F_ROWS_COAL 1  // coalesced first-pass loads of the row FFTs
+#endif
+__host__ __device__ __forceinline__ int rpad(int i) { return i + (i >> 3) + (i >> 6); }
+__host__ __device__ __forceinline__ int rpad_len(int L) { return L + (L >> 3) + (L >> 6); }
 template <bool FWD, int NST>
 __device__ __forceinline__ void rows_pass(const NfP& P, const cplx* __restrict__ src, cplx* __restrict__ dst,
                                           const double* __restrict__ deconv, cplx* sm, const cplx* __restrict__ tws,
@@ -873,7 +887,10 @@ __device__ __forceinline__ void rows_pass(const NfP& P, const cplx* __restrict__
   const int h = 1 << (s - 1);
   const int groups = N / GN, nthr = groups * P.RW;
   for (int tix = threadIdx.x; tix < nthr; tix += blockDim.x) {
-    const int rr = tix / groups, j = tix - rr * groups;
+    const int rr = tix / groups, jn = tix - rr * groups;
+    // first pass: thread jn takes the group whose 8 bit-reversed input positions are
+    // rev3(m) * groups + jn, so a warp's loads cover contiguous segments of the row
+    const int j = (F_ROWS_COAL && first) ? bitrev(jn, L - NST) : jn;
     const int jy = j0 + rr;  // coefficient row (y index) of this line
     const int jh = j & (h - 1);
     const int i0 = (j >> (s - 1)) * (GN * h) + jh;
@@ -897,7 +914,7 @@ __device__ __forceinline__ void rows_pass(const NfP& P, const cplx* __restrict__
       }
     } else {
 #pragma unroll
-      for (int m = 0; m < GN; ++m) v[m] = base[fpad(i0 + m * h)];
+      for (int m = 0; m < GN; ++m) v[m] = base[rpad(i0 + m * h)];
     }
     r8_pass<FWD, NST>(v, jh, h, tws, L, s);
     if (last) {
@@ -919,17 +936,20 @@ __device__ __forceinline__ void rows_pass(const NfP& P, const cplx* __restrict__
       }
     } else {
 #pragma unroll
-      for (int m = 0; m < GN; ++m) base[fpad(i0 + m * h)] = v[m];
+      for (int m = 0; m < GN; ++m) base[rpad(i0 + m * h)] = v[m];
     }
   }
 }
 
+#ifndef F_ROWS_MINB
+#define F_ROWS_MINB 4  // resident row-FFT CTAs per SM the register budget is sized for
+#endif
 template <bool FWD>
-__global__ void k2_rows_fft8(NfP P, const cplx* __restrict__ src, const double* __restrict__ deconv,
+__global__ void __launch_bounds__(256, F_ROWS_MINB) k2_rows_fft8(NfP P, const cplx* __restrict__ src, const double* __restrict__ deconv,
                              cplx* __restrict__ dst, const cplx* __restrict__ tw) {
   extern __shared__ cplx sm[];
   const int L = P.log_nov, N = P.n_ov;
-  const int ls = fpad_len(N) + 1;
+  const int ls = rpad_len(N) + 1;
   cplx* tws = sm + P.RW * ls;
   const int j0 = blockIdx.x * P.RW, prob = blockIdx.y, nr = min(P.RW, P.n - j0);
   const cplx* s = FWD ? src + (int64_t)prob * P.n * P.n : src + (int64_t)prob * N * N;
