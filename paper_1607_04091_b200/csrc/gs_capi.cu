@@ -1065,7 +1065,7 @@ void forward_dev(gs_op* op, const cplx* x, cplx* y, bool perm_io, cudaStream_t s
       pmark("k2_rows_embed_fft", st);
       if (op->logLmax == P.log_nov && cols_fft8())
         k2_cols_fft8<true><<<dim3(P.n_ov / P.CW, B), F_COLS_THREADS,
-                              ((size_t)P.CW * (fpad_len(P.n_ov) + 1) + P.n_ov / 2) * sizeof(cplx), st>>>(P, op->G.p,
+                              ((size_t)P.CW * (fpad_len(P.n_ov) + 1) + P.n_ov / (F_COLS_QW ? 4 : 2)) * sizeof(cplx), st>>>(P, op->G.p,
                                                                                                         op->tw.p);
       else
         k2_cols_fft<<<dim3(P.n_ov / P.CW, B), 256, (size_t)P.CW * (fpad_len(P.n_ov) + 1) * sizeof(cplx), st>>>(
@@ -1221,7 +1221,7 @@ bool adjoint_dev(gs_op* op, const cplx* y, cplx* z, bool perm_io, cudaStream_t s
       pmark("k2_fold_tiles", st);
       if (op->logLmax == P.log_nov && cols_fft8())
         k2_cols_fft8<false><<<dim3(P.n_ov / P.CW, B), F_COLS_THREADS,
-                               ((size_t)P.CW * (fpad_len(P.n_ov) + 1) + P.n_ov / 2) * sizeof(cplx), st>>>(P, op->G.p,
+                               ((size_t)P.CW * (fpad_len(P.n_ov) + 1) + P.n_ov / (F_COLS_QW ? 4 : 2)) * sizeof(cplx), st>>>(P, op->G.p,
                                                                                                          op->tw.p);
       else
         k2_cols_ifft<<<dim3(P.n_ov / P.CW, B), 256, (size_t)P.CW * (fpad_len(P.n_ov) + 1) * sizeof(cplx), st>>>(

@@ -781,7 +781,12 @@ __global__ void k2_edges(NfP P, const cplx* __restrict__ TLF, const cplx* __rest
 // FWD: forward (FFT_-), only the n rows carrying data are read (the zero rows
 // of the embedded block are skipped); else inverse (FFT_+), only the n rows
 // the crop keeps are stored.
-template <bool FWD, int NST>
+#ifndef F_COLS_QW
+#define F_COLS_QW 1  // quarter-wave twiddle table in the column FFTs: 2 KB less shared memory, 3 CTAs of 8 columns per SM
+#endif
+// QW: tws holds the first quarter of the table only (k < 2^L / 4);
+// exp(-2 pi i (k + 2^L / 4) / 2^L) = -i exp(-2 pi i k / 2^L)
+template <bool FWD, int NST, bool QW = false>
 __device__ __forceinline__ void r8_pass(cplx* v, int jh, int h, const cplx* __restrict__ tws, int L, int s) {
   constexpr int GN = 1 << NST;
 #pragma unroll
@@ -790,7 +795,16 @@ __device__ __forceinline__ void r8_pass(cplx* v, int jh, int h, const cplx* __re
     for (int m = 0; m < GN; ++m) {
       if ((m >> q) & 1) continue;
       const int k = jh + (m & ((1 << q) - 1)) * h;
-      cplx w = tws[k << (L - (s + q))];
+      const int idx = k << (L - (s + q));
+      cplx w;
+      if (QW) {
+        const int qn = 1 << (L - 2);
+        const bool hi = idx >= qn;
+        const cplx t = tws[hi ? idx - qn : idx];
+        w = hi ? mk(t.y, -t.x) : t;
+      } else {
+        w = tws[idx];
+      }
       if (!FWD) w.y = -w.y;
       const cplx u = v[m], x = cmul(v[m + (1 << q)], w);
       v[m] = cadd(u, x);
@@ -823,7 +837,7 @@ __device__ __forceinline__ void cols_pass(const NfP& P, cplx* __restrict__ g, cp
 #pragma unroll
       for (int m = 0; m < GN; ++m) v[m] = base[fpad(i0 + m * h)];
     }
-    r8_pass<FWD, NST>(v, jh, h, tws, L, s);
+    r8_pass<FWD, NST, F_COLS_QW != 0>(v, jh, h, tws, L, s);
     if (last) {
 #pragma unroll
       for (int m = 0; m < GN; ++m) {
@@ -840,18 +854,21 @@ __device__ __forceinline__ void cols_pass(const NfP& P, cplx* __restrict__ g, cp
 #ifndef F_COLS_THREADS
 #define F_COLS_THREADS 256  // threads of a column-FFT CTA
 #endif
+#ifndef F_COLS_QW
+#define F_COLS_QW 1  // quarter-wave twiddle table in the column FFTs: 2 KB less shared memory, 3 CTAs of 8 columns per SM
+#endif
 #ifndef F_COLS_MINB
-#define F_COLS_MINB 2
+#define F_COLS_MINB (F_COLS_QW ? 3 : 2)
 #endif
 template <bool FWD>
 __global__ void __launch_bounds__(F_COLS_THREADS, F_COLS_MINB) k2_cols_fft8(NfP P, cplx* __restrict__ G, const cplx* __restrict__ tw) {
   extern __shared__ cplx sm[];
   const int L = P.log_nov, N = P.n_ov, CW = P.CW;
   const int ls = fpad_len(N) + 1;
-  cplx* tws = sm + CW * ls;  // N / 2 twiddles
+  cplx* tws = sm + CW * ls;  // N / 2 twiddles (N / 4 with F_COLS_QW)
   const int c0 = blockIdx.x * CW, prob = blockIdx.y;
   cplx* g = G + (int64_t)prob * N * N;
-  for (int i = threadIdx.x; i < N / 2; i += blockDim.x) tws[i] = tw[i];
+  for (int i = threadIdx.x; i < (F_COLS_QW ? N / 4 : N / 2); i += blockDim.x) tws[i] = tw[i];
   __syncthreads();
   for (int s = 1; s <= L;) {
     const int nst = L - s + 1 >= 3 ? 3 : L - s + 1;
