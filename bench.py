@@ -666,6 +666,22 @@ def _cpu_iter_seconds(op, data, k):
     return max(1e-9, (t2 - t1) / k), t1, t2
 
 
+def _cpu_pair_seconds(op, data):
+    """Seconds per T x + T* y pair on the CPU operator (warm; repeated until ~0.5 s is timed)."""
+    rng = np.random.default_rng(SEED)
+    x = rng.standard_normal(op.cols) + 1j * rng.standard_normal(op.cols)
+
+    def pair():
+        t = time.perf_counter()
+        op.forward(x)
+        op.adjoint(data)
+        return time.perf_counter() - t
+
+    probe = pair()
+    reps = int(max(1, min(5000, math.ceil(0.5 / max(probe, 1e-6)))))
+    return probe if reps == 1 else min(sum(pair() for _ in range(reps)) / reps for _ in range(2))
+
+
 def cpu_baseline(workload):
     """Rank 0, N=1: the reference (single-threaded, as it is) on one problem of
     the workload -- the reference itself when its library is here, else the port."""
@@ -678,7 +694,9 @@ def cpu_baseline(workload):
         build = time.perf_counter() - t
         k = 2 if workload in ("c4", "c5", "c3") else 20
         per_it, _, _ = _cpu_iter_seconds(op, data, k)
+        per_pair = _cpu_pair_seconds(op, data)
         return {"value": round(1.0 / per_it, 4), "unit": "problem-iterations/s", "cores": 1, "kind": kind,
+                "pairs_per_sec": round(1.0 / per_pair, 4),
                 "cpu_model": cpu["model"], "physical_cores": cpu["physical_cores"],
                 "sample": f"{workload.upper()} problem 0, {k} CGLS iterations (difference of solves of 1 and "
                           f"{1 + k} iterations), 1 thread, construction ({build:.1f} s) excluded; {what}"}
